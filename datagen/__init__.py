@@ -1,0 +1,226 @@
+"""Seeded synthetic workloads for the LOGAN X-drop hot path.
+
+This module is shared by the oracle tests and the CUDA path and holds none of
+the method's arithmetic (no scoring, no DP): it only produces reads, seeds and
+the per-workload constants (scoring scheme and X are *inputs* of the method).
+
+Pair ``p`` of a workload is a pure function of ``(seed, p)`` (counter-based
+RNG in ``gen.c``), so shards generated on different ranks are slices of the
+same global batch.  Recipe: DESIGN.md §5 and the header of ``gen.c``.
+"""
+from __future__ import annotations
+
+import ctypes
+import math
+import os
+import subprocess
+from dataclasses import dataclass, field, replace
+
+import numpy as np
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+_SRC = os.path.join(_HERE, "gen.c")
+_LIB = os.path.join(_HERE, "_libgen.so")
+
+#: base seed: the arXiv id; config c uses SEED_BASE + c.
+SEED_BASE = 2002052000
+
+
+def build(force: bool = False) -> str:
+    if force or not os.path.exists(_LIB) or os.path.getmtime(_LIB) < os.path.getmtime(_SRC):
+        tmp = _LIB + ".tmp"
+        subprocess.check_call(["gcc", "-O2", "-std=c11", "-fPIC", "-shared", "-pthread", "-o",
+                               tmp, _SRC, "-lm"])
+        os.replace(tmp, _LIB)
+    return _LIB
+
+
+class _Cfg(ctypes.Structure):
+    _fields_ = [("seed", ctypes.c_uint64), ("n_pairs", ctypes.c_int64),
+                ("pair_base", ctypes.c_int64), ("mode", ctypes.c_int32),
+                ("tlen_min", ctypes.c_int32), ("tlen_max", ctypes.c_int32),
+                ("err", ctypes.c_double), ("k", ctypes.c_int32), ("spurious", ctypes.c_double),
+                ("len_lo", ctypes.c_int32), ("len_hi", ctypes.c_int32), ("burst", ctypes.c_double)]
+
+
+_lib = None
+
+
+def _load():
+    global _lib
+    if _lib is None:
+        lib = ctypes.CDLL(build())
+        P = ctypes.POINTER
+        lib.gen_lengths.argtypes = [P(_Cfg)] + [P(ctypes.c_int32)] * 4 + [ctypes.c_int]
+        lib.gen_lengths.restype = ctypes.c_int
+        lib.gen_bases.argtypes = [P(_Cfg), P(ctypes.c_int64), P(ctypes.c_uint8),
+                                  P(ctypes.c_uint8), ctypes.c_int]
+        lib.gen_bases.restype = ctypes.c_int
+        _lib = lib
+    return _lib
+
+
+@dataclass(frozen=True)
+class Workload:
+    """A workload recipe (one of BASELINE.json's configs, or a variant)."""
+    name: str
+    n_pairs: int
+    mode: int = 0            # 0 template pairs, 1 BELLA-like
+    tlen_min: int = 1000
+    tlen_max: int = 1000
+    err: float = 0.15
+    k: int = 17
+    spurious: float = 0.0
+    len_lo: int = 1000
+    len_hi: int = 30000
+    burst: float = 0.0
+    # method inputs (not generator arithmetic): scoring scheme and X
+    match: int = 1
+    mismatch: int = -1
+    gap: int = -1
+    xdrop: int = 50
+    seed: int = SEED_BASE
+
+    def with_(self, **kw) -> "Workload":
+        return replace(self, **kw)
+
+    @property
+    def max_read_len(self) -> int:
+        # a read is at most twice its template (one insertion per base) plus a burst block
+        base = self.len_hi if self.mode == 1 else self.tlen_max
+        return 2 * base + 320
+
+
+#: BASELINE.json configs.  C3 is listed at X = 20; the sweep
+#: varies ``xdrop``.  C4 is ~1M pairs at full size.
+CONFIGS = {
+    1: Workload("c1_1k_x50", 1_000, tlen_min=1000, tlen_max=1000, err=0.15, xdrop=50,
+                seed=SEED_BASE + 1),
+    2: Workload("c2_2.5k_x20", 100_000, tlen_min=2500, tlen_max=2500, err=0.15, xdrop=20,
+                seed=SEED_BASE + 2),
+    3: Workload("c3_10k_x20", 100_000, tlen_min=10000, tlen_max=10000, err=0.15, xdrop=20,
+                seed=SEED_BASE + 3),
+    4: Workload("c4_bella_x50", 1_000_000, mode=1, err=0.15, spurious=0.30, len_lo=1000,
+                len_hi=30000, xdrop=50, seed=SEED_BASE + 4),
+    5: Workload("c5_long_x100", 20_000, tlen_min=50000, tlen_max=100000, err=0.12, xdrop=100,
+                seed=SEED_BASE + 5),
+}
+
+
+@dataclass
+class Batch:
+    """Generated pairs.  Offsets/lengths in bases; pools in both formats on request."""
+    workload: Workload
+    pair_base: int
+    q_off: np.ndarray
+    q_len: np.ndarray
+    t_off: np.ndarray
+    t_len: np.ndarray
+    q_seed: np.ndarray
+    t_seed: np.ndarray
+    pool_len: int
+    pool_u8: np.ndarray | None = None
+    pool_2bit: np.ndarray | None = None
+    meta: dict = field(default_factory=dict)
+
+    @property
+    def n_pairs(self) -> int:
+        return len(self.q_len)
+
+    def max_ext_len(self) -> int:
+        if self.n_pairs == 0:
+            return 0
+        k = self.workload.k
+        return int(max(self.q_seed.max(), self.t_seed.max(),
+                       (self.q_len - self.q_seed - k).max(), (self.t_len - self.t_seed - k).max(), 0))
+
+
+def _pad16(n: int) -> int:
+    return (n + 15) // 16 * 16
+
+
+def generate(w: Workload, n_pairs: int | None = None, pair_base: int = 0, u8: bool = True,
+             two_bit: bool = True, n_threads: int | None = None) -> Batch:
+    """Generate pairs ``[pair_base, pair_base + n_pairs)`` of workload ``w``.
+
+    The pools are padded with zero bytes to a multiple of 16 bytes + 16 (the
+    library reads whole words).
+    """
+    n = w.n_pairs if n_pairs is None else int(n_pairs)
+    if n_threads is None:
+        n_threads = len(os.sched_getaffinity(0))
+    cfg = _Cfg(w.seed, n, pair_base, w.mode, w.tlen_min, w.tlen_max, w.err, w.k, w.spurious,
+               w.len_lo, w.len_hi, w.burst)
+    P = ctypes.POINTER
+    ql = np.zeros(n, np.int32); tl = np.zeros(n, np.int32)
+    qs = np.zeros(n, np.int32); ts = np.zeros(n, np.int32)
+    lib = _load()
+    if n > 0:
+        st = lib.gen_lengths(ctypes.byref(cfg), ql.ctypes.data_as(P(ctypes.c_int32)),
+                             tl.ctypes.data_as(P(ctypes.c_int32)), qs.ctypes.data_as(P(ctypes.c_int32)),
+                             ts.ctypes.data_as(P(ctypes.c_int32)), n_threads)
+        if st != 0:
+            raise RuntimeError("gen_lengths failed")
+    region = (ql.astype(np.int64) + tl + 3) // 4 * 4
+    off = np.zeros(n, np.int64)
+    if n > 1:
+        np.cumsum(region[:-1], out=off[1:])
+    pool_len = int(off[-1] + region[-1]) if n else 0
+    pu8 = np.zeros(_pad16(pool_len) + 16, np.uint8) if u8 else None
+    p2 = np.zeros(_pad16((pool_len + 3) // 4) + 16, np.uint8) if two_bit else None
+    if n > 0 and (u8 or two_bit):
+        st = lib.gen_bases(ctypes.byref(cfg), off.ctypes.data_as(P(ctypes.c_int64)),
+                           pu8.ctypes.data_as(P(ctypes.c_uint8)) if u8 else None,
+                           p2.ctypes.data_as(P(ctypes.c_uint8)) if two_bit else None, n_threads)
+        if st != 0:
+            raise RuntimeError("gen_bases failed")
+    return Batch(w, pair_base, off, ql, off + ql, tl, qs, ts, pool_len, pu8, p2)
+
+
+def decode_2bit(pool: np.ndarray, start: int, length: int) -> bytes:
+    """ACGT text of ``length`` bases from a 2-bit pool (test helper)."""
+    idx = np.arange(start, start + length, dtype=np.int64)
+    codes = (pool[idx >> 2] >> (2 * (idx & 3)).astype(np.uint8)) & 3
+    return bytes(np.frombuffer(b"ACGT", np.uint8)[codes])
+
+
+def pack_2bit(text: bytes | str) -> np.ndarray:
+    """Pack an ACGT string into the 2-bit pool format (test helper), padded."""
+    if isinstance(text, str):
+        text = text.encode()
+    lut = np.full(256, 255, np.uint8)
+    for c, v in zip(b"ACGT", range(4)):
+        lut[c] = v
+    codes = lut[np.frombuffer(text, np.uint8)]
+    if (codes == 255).any():
+        raise ValueError("2-bit pool holds A/C/G/T only")
+    out = np.zeros(_pad16((len(codes) + 3) // 4) + 16, np.uint8)
+    for s in range(4):
+        part = codes[s::4].astype(np.uint8) << (2 * s)
+        out[:len(part)] |= part
+    return out
+
+
+def from_strings(pairs, k: int, w: Workload | None = None) -> Batch:
+    """Build a Batch from explicit (q, t, qs, ts) tuples (test helper)."""
+    w = w or Workload("explicit", len(pairs), k=k)
+    w = w.with_(k=k, n_pairs=len(pairs))
+    qs_, ts_, ql_, tl_, qo_, to_ = [], [], [], [], [], []
+    text = bytearray()
+    for q, t, a, b in pairs:
+        q = q.encode() if isinstance(q, str) else bytes(q)
+        t = t.encode() if isinstance(t, str) else bytes(t)
+        qo_.append(len(text)); text += q; to_.append(len(text)); text += t
+        while len(text) % 4:
+            text += b"A"
+        ql_.append(len(q)); tl_.append(len(t)); qs_.append(a); ts_.append(b)
+    pool_len = len(text)
+    pu8 = np.zeros(_pad16(pool_len) + 16, np.uint8)
+    pu8[:pool_len] = np.frombuffer(bytes(text), np.uint8)
+    try:
+        p2 = pack_2bit(bytes(text))
+    except ValueError:
+        p2 = None
+    return Batch(w, 0, np.array(qo_, np.int64), np.array(ql_, np.int32), np.array(to_, np.int64),
+                 np.array(tl_, np.int32), np.array(qs_, np.int32), np.array(ts_, np.int32),
+                 pool_len, pu8, p2)

@@ -1,0 +1,172 @@
+/*
+ * logan_xdrop.h — C ABI v1 of the B200-native batched X-drop seed-and-extend
+ * library (LOGAN, Zeni et al., arXiv 2002.05200).
+ *
+ * Citations are PAPER.md line numbers ("P:<line>") with the section, equation
+ * or algorithm they fall in; "c-amb-N" refers to the numbered readings of the
+ * paper listed in DESIGN.md §3.
+ *
+ * What one call computes (§III-A problem statement; Fig. 5 and
+ * P:209 §IV-B seed split): for every (query, target, seed) pair
+ *   - the LEFT extension  E(reverse q[0:qs), reverse t[0:ts))  and
+ *   - the RIGHT extension E(q[qs+k:M), t[ts+k:N))
+ * where E(A, B) is the X-drop antidiagonal sweep of Alg. 1 with
+ * the cell rule of eq. P:85, the drop rule of P:89 (a cell with
+ * S(i,j) < best - X is -inf and never considered again), `best` updated only
+ * after an antidiagonal is complete and the band trimmed to the cells
+ * that can still have a live predecessor (c-amb-6).
+ * The pair result is
+ *   score   = seed_score + best_L + best_R              (c-amb-10)
+ *   q_begin = qs - i*_L,  q_end = qs + k + i*_R          ([begin, end), 0-based)
+ *   t_begin = ts - j*_L,  t_end = ts + k + j*_R
+ * where (i*, j*) is the cell at which each extension's best was FIRST reached
+ * (smallest antidiagonal, then smallest query offset i; (0,0) if best = 0)
+ * (c-amb-8, c-amb-9), and seed_score = sum_u (q[qs+u]==t[ts+u] ? match : mismatch).
+ * `cells` counts, per extension, the interior cells of every antidiagonal band
+ * [lo_d, hi_d] (DESIGN.md §3 "cell count"); the pair value is L + R.
+ *
+ * All arithmetic is int32; there is no floating point anywhere on the path.
+ */
+#ifndef LOGAN_XDROP_H
+#define LOGAN_XDROP_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define LOGAN_ABI_VERSION 1
+
+/* Linear scoring scheme (eq. P:85, read with signed addends, c-amb-2).
+ * Requirements: 0 < match <= 127, -127 <= mismatch < 0, -127 <= gap < 0,
+ * 0 <= xdrop <= 2^20 (X >= (m+n)*127 disables pruning: "X = infinity"). */
+typedef struct {
+    int32_t match;
+    int32_t mismatch;
+    int32_t gap;
+    int32_t xdrop;
+} logan_scoring_t;
+
+/* Per-pair result, 20 bytes. Coordinates are 0-based half-open [begin, end)
+ * in read coordinates. A pair whose seed or read range is invalid gets
+ * {INT32_MIN, -1, -1, -1, -1}. */
+typedef struct {
+    int32_t score;
+    int32_t q_begin;
+    int32_t q_end;
+    int32_t t_begin;
+    int32_t t_end;
+} logan_result_t;
+
+/* Sequence pool formats.
+ *  LOGAN_SEQ_U8   : one byte per base, bases compared by raw byte equality.
+ *  LOGAN_SEQ_2BIT : A=0 C=1 G=2 T=3, four bases per byte, base b stored at
+ *                   bits 2*(b mod 4) of byte floor(b/4) (LSB first). */
+enum { LOGAN_SEQ_U8 = 0, LOGAN_SEQ_2BIT = 1 };
+
+/* Status codes. */
+enum {
+    LOGAN_OK = 0,
+    LOGAN_EINVAL = 1, /* bad scalar, null pointer or misaligned buffer */
+    LOGAN_ECUDA = 2,  /* a CUDA launch or copy failed */
+    LOGAN_ENOSPC = 3  /* workspace smaller than logan_workspace_bytes()  */
+};
+
+/* Kernel-selection hint (0 = automatic). Values 1..5 force the first
+ * register-window level (window of 32, 64, 128, 256, 1024 diagonal slots);
+ * 6 forces every task onto the unbounded CTA path. Results never depend on
+ * it (tests assert this); only speed does. */
+typedef struct {
+    int32_t first_level;   /* 0 = auto from xdrop */
+    int32_t reserved[7];
+} logan_options_t;
+
+/* Per-call device-side statistics (optional output, device memory, may be
+ * NULL): number of tasks that ran at each level (6 entries) and the number
+ * of window shifts. Filled after the stream syncs. */
+typedef struct {
+    uint64_t tasks_per_level[6];
+    uint64_t window_shifts;
+    uint64_t cells_total;
+} logan_stats_t;
+
+/* Bytes of device workspace a call with n_pairs pairs needs.
+ * max_ext_len = the largest extension length (bases) on either side of any
+ * seed, i.e. an upper bound on max(qs, ts, M-qs-k, N-ts-k); it sizes the
+ * scratch of the unbounded CTA path. Returns 0 if n_pairs < 0. */
+size_t logan_workspace_bytes(int64_t n_pairs, int64_t max_ext_len);
+
+/*
+ * logan_xdrop_batch — the whole hot path on one device, asynchronously on
+ * `stream` (a cudaStream_t; NULL = legacy default stream).
+ *
+ * ALL pointers are DEVICE pointers owned by the caller; the library allocates
+ * nothing, keeps no global state and is reentrant given distinct workspaces.
+ *
+ *  seq_pool   : the read pool, format `seq_fmt`, pool_len bases. The buffer
+ *               must be 4-byte aligned and readable up to the next multiple
+ *               of 16 bytes past its last byte (the kernels load whole words).
+ *  q_off,t_off: int64[n_pairs] base offsets of query / target read in the pool
+ *               (reads may be shared between pairs).
+ *  q_len,t_len: int32[n_pairs] read lengths (bases), 0 <= len < 2^30.
+ *  q_seed,t_seed: int32[n_pairs] seed start inside query / target read.
+ *  k          : seed length (>= 0; k = 0 is a point seed).
+ *  sc         : scoring and X.
+ *  opt        : may be NULL (automatic).
+ *  out        : logan_result_t[n_pairs] (device).
+ *  cells      : uint64[n_pairs] (device) or NULL.
+ *  stats      : logan_stats_t (device) or NULL.
+ *  workspace  : device buffer of >= logan_workspace_bytes(n_pairs, max_ext_len)
+ *               bytes, 256-byte aligned. Its contents are scratch.
+ *
+ * Errors: invalid scalars / NULL required pointers -> LOGAN_EINVAL and a too
+ * small workspace -> LOGAN_ENOSPC, both returned synchronously with nothing
+ * launched. A pair whose ranges are invalid (q_seed < 0, q_seed + k > q_len,
+ * likewise for t, or a read outside [0, pool_len)) gets the invalid result and
+ * cells = 0; the rest of the batch is unaffected. A launch failure returns
+ * LOGAN_ECUDA. n_pairs = 0 is a no-op returning LOGAN_OK.
+ * Results are valid once `stream` has been synchronised.
+ */
+int logan_xdrop_batch(const uint8_t *seq_pool, int32_t seq_fmt, int64_t pool_len,
+                      const int64_t *q_off, const int32_t *q_len,
+                      const int64_t *t_off, const int32_t *t_len,
+                      const int32_t *q_seed, const int32_t *t_seed,
+                      int64_t n_pairs, int32_t k, logan_scoring_t sc,
+                      const logan_options_t *opt,
+                      logan_result_t *out, uint64_t *cells, logan_stats_t *stats,
+                      void *workspace, size_t workspace_bytes, void *stream);
+
+/*
+ * Host-buffer entry point (the end-to-end call): the same computation with
+ * every input and output in HOST memory (pinned memory gives full-speed
+ * copies). The caller provides one DEVICE arena of at least
+ * logan_host_arena_bytes(...) bytes; the call copies the inputs into it
+ * (host->device), runs logan_xdrop_batch on `stream`, copies `out` (and
+ * `cells` if non-NULL) back (device->host) and synchronises `stream` before
+ * returning. Same error behaviour as logan_xdrop_batch; additionally returns
+ * LOGAN_ECUDA if a copy or the final synchronisation fails.
+ */
+size_t logan_host_arena_bytes(int64_t n_pairs, int64_t pool_len, int32_t seq_fmt,
+                              int64_t max_ext_len);
+int logan_xdrop_batch_host(const uint8_t *seq_pool, int32_t seq_fmt, int64_t pool_len,
+                           const int64_t *q_off, const int32_t *q_len,
+                           const int64_t *t_off, const int32_t *t_len,
+                           const int32_t *q_seed, const int32_t *t_seed,
+                           int64_t n_pairs, int32_t k, logan_scoring_t sc,
+                           const logan_options_t *opt,
+                           logan_result_t *out, uint64_t *cells,
+                           void *device_arena, size_t arena_bytes, void *stream);
+
+/* Human-readable text for a status code (static storage). */
+const char *logan_strerror(int status);
+
+/* ABI version the library was built with (LOGAN_ABI_VERSION). */
+int logan_abi_version(void);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* LOGAN_XDROP_H */
