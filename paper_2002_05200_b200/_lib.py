@@ -1,0 +1,82 @@
+"""ctypes binding of the C ABI in ``include/logan_xdrop.h`` (argument marshalling only).
+
+Every step of the hot path runs in ``liblogan_xdrop.so`` (sm_100a).  There is
+no CPU fallback: if the library is missing, or no CUDA device is present, the
+calls raise.
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+
+PKG = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(PKG, "liblogan_xdrop.so")
+
+LOGAN_SEQ_U8 = 0
+LOGAN_SEQ_2BIT = 1
+LOGAN_OK, LOGAN_EINVAL, LOGAN_ECUDA, LOGAN_ENOSPC = 0, 1, 2, 3
+
+#: every symbol include/logan_xdrop.h declares
+EXPORTS = ("logan_workspace_bytes", "logan_xdrop_batch", "logan_host_arena_bytes",
+           "logan_xdrop_batch_host", "logan_strerror", "logan_abi_version")
+
+
+class Scoring(ctypes.Structure):
+    _fields_ = [("match", ctypes.c_int32), ("mismatch", ctypes.c_int32),
+                ("gap", ctypes.c_int32), ("xdrop", ctypes.c_int32)]
+
+
+class Options(ctypes.Structure):
+    _fields_ = [("first_level", ctypes.c_int32), ("reserved", ctypes.c_int32 * 7)]
+
+
+class Result(ctypes.Structure):
+    _fields_ = [("score", ctypes.c_int32), ("q_begin", ctypes.c_int32), ("q_end", ctypes.c_int32),
+                ("t_begin", ctypes.c_int32), ("t_end", ctypes.c_int32)]
+
+
+class Stats(ctypes.Structure):
+    _fields_ = [("tasks_per_level", ctypes.c_uint64 * 6), ("window_shifts", ctypes.c_uint64),
+                ("cells_total", ctypes.c_uint64)]
+
+
+class LoganError(RuntimeError):
+    pass
+
+
+_lib = None
+
+
+def load(path: str | None = None) -> ctypes.CDLL:
+    """Load the library (once).  Raises if it has not been built."""
+    global _lib
+    if _lib is not None:
+        return _lib
+    path = path or LIB_PATH
+    if not os.path.exists(path):
+        raise LoganError(f"{path} is missing: build it with `python -m paper_2002_05200_b200.build` "
+                         "(there is no CPU fallback)")
+    lib = ctypes.CDLL(path)
+    vp, i64, i32, sz = ctypes.c_void_p, ctypes.c_int64, ctypes.c_int32, ctypes.c_size_t
+    lib.logan_workspace_bytes.argtypes = [i64, i64]
+    lib.logan_workspace_bytes.restype = sz
+    lib.logan_host_arena_bytes.argtypes = [i64, i64, i32, i64]
+    lib.logan_host_arena_bytes.restype = sz
+    lib.logan_xdrop_batch.argtypes = [vp, i32, i64, vp, vp, vp, vp, vp, vp, i64, i32, Scoring,
+                                      ctypes.POINTER(Options), vp, vp, vp, vp, sz, vp]
+    lib.logan_xdrop_batch.restype = ctypes.c_int
+    lib.logan_xdrop_batch_host.argtypes = [vp, i32, i64, vp, vp, vp, vp, vp, vp, i64, i32, Scoring,
+                                           ctypes.POINTER(Options), vp, vp, vp, sz, vp]
+    lib.logan_xdrop_batch_host.restype = ctypes.c_int
+    lib.logan_strerror.argtypes = [ctypes.c_int]
+    lib.logan_strerror.restype = ctypes.c_char_p
+    lib.logan_abi_version.argtypes = []
+    lib.logan_abi_version.restype = ctypes.c_int
+    _lib = lib
+    return lib
+
+
+def check(status: int) -> None:
+    if status != LOGAN_OK:
+        msg = load().logan_strerror(status).decode()
+        raise LoganError(f"logan status {status}: {msg}")

@@ -1,0 +1,167 @@
+"""Python API over the C ABI (torch owns device memory and streams).
+
+``xdrop_batch`` takes CUDA tensors and calls ``logan_xdrop_batch`` on the
+current torch stream; ``xdrop_batch_host`` takes host numpy arrays (pinned or
+not) and calls ``logan_xdrop_batch_host`` (copies in, sweep, copies out) --
+the end-to-end entry point.  Nothing here computes any part of the method.
+"""
+from __future__ import annotations
+
+import ctypes
+from dataclasses import dataclass
+
+import numpy as np
+
+from . import _lib
+
+
+def _require_cuda():
+    import torch
+    if not torch.cuda.is_available():
+        raise _lib.LoganError("logan: no CUDA device (this library has no CPU path)")
+    return torch
+
+
+@dataclass
+class Workspace:
+    """A reusable device workspace (torch uint8 tensor, 256-byte aligned)."""
+    tensor: object
+    n_pairs: int
+    max_ext_len: int
+
+    @property
+    def nbytes(self) -> int:
+        return int(self.tensor.numel())
+
+    def ptr(self) -> int:
+        return int(self.tensor.data_ptr())
+
+
+def workspace_bytes(n_pairs: int, max_ext_len: int) -> int:
+    return int(_lib.load().logan_workspace_bytes(int(n_pairs), int(max_ext_len)))
+
+
+def make_workspace(n_pairs: int, max_ext_len: int, device=None) -> Workspace:
+    torch = _require_cuda()
+    nb = workspace_bytes(n_pairs, max_ext_len)
+    t = torch.empty(max(nb, 256) + 256, dtype=torch.uint8, device=device or "cuda")
+    off = (-t.data_ptr()) % 256
+    return Workspace(t[off:off + max(nb, 256)], n_pairs, max_ext_len)
+
+
+def _opts(first_level: int | None):
+    if not first_level:
+        return None
+    o = _lib.Options()
+    o.first_level = int(first_level)
+    return ctypes.pointer(o)
+
+
+@dataclass
+class DeviceBatch:
+    """Pairs resident on one device (torch CUDA tensors)."""
+    pool: object       # uint8, padded to 16 bytes
+    fmt: int
+    pool_len: int      # bases
+    q_off: object      # int64
+    q_len: object      # int32
+    t_off: object      # int64
+    t_len: object      # int32
+    q_seed: object     # int32
+    t_seed: object     # int32
+    k: int
+    max_ext_len: int
+
+    @property
+    def n_pairs(self) -> int:
+        return int(self.q_len.numel())
+
+
+def to_device(batch, fmt: int = _lib.LOGAN_SEQ_2BIT, device=None) -> DeviceBatch:
+    """Copy a ``datagen.Batch`` (or anything with the same fields) to the GPU."""
+    torch = _require_cuda()
+    dev = device or "cuda"
+    pool = batch.pool_2bit if fmt == _lib.LOGAN_SEQ_2BIT else batch.pool_u8
+    if pool is None:
+        raise ValueError("batch has no pool in the requested format")
+    t = lambda a, dt: torch.as_tensor(np.ascontiguousarray(a), dtype=dt).to(dev)
+    return DeviceBatch(t(pool, torch.uint8), fmt, int(batch.pool_len),
+                       t(batch.q_off, torch.int64), t(batch.q_len, torch.int32),
+                       t(batch.t_off, torch.int64), t(batch.t_len, torch.int32),
+                       t(batch.q_seed, torch.int32), t(batch.t_seed, torch.int32),
+                       int(batch.workload.k), int(batch.max_ext_len()))
+
+
+def xdrop_batch(db: DeviceBatch, match: int, mismatch: int, gap: int, xdrop: int,
+                workspace: Workspace | None = None, out=None, cells=None, stats=None,
+                first_level: int | None = None, stream=None):
+    """Run the whole hot path on ``db``'s device, asynchronously on ``stream``
+    (default: torch's current stream).  Returns ``(out int32[n,5], cells int64[n])``
+    device tensors (cells holds uint64 bit patterns)."""
+    torch = _require_cuda()
+    lib = _lib.load()
+    n = db.n_pairs
+    dev = db.q_len.device
+    if out is None:
+        out = torch.empty((n, 5), dtype=torch.int32, device=dev)
+    if cells is None:
+        cells = torch.empty(n, dtype=torch.int64, device=dev)
+    if workspace is None or workspace.n_pairs < n or workspace.max_ext_len < db.max_ext_len:
+        workspace = make_workspace(n, db.max_ext_len, dev)
+    if stream is None:
+        stream = torch.cuda.current_stream(dev)
+    sc = _lib.Scoring(match, mismatch, gap, xdrop)
+    st = lib.logan_xdrop_batch(
+        db.pool.data_ptr(), db.fmt, db.pool_len, db.q_off.data_ptr(), db.q_len.data_ptr(),
+        db.t_off.data_ptr(), db.t_len.data_ptr(), db.q_seed.data_ptr(), db.t_seed.data_ptr(),
+        n, db.k, sc, _opts(first_level), out.data_ptr(), cells.data_ptr(),
+        stats.data_ptr() if stats is not None else None,
+        workspace.ptr(), workspace.nbytes, stream.cuda_stream)
+    _lib.check(st)
+    return out, cells
+
+
+def new_stats(device=None):
+    torch = _require_cuda()
+    return torch.zeros(8, dtype=torch.int64, device=device or "cuda")
+
+
+def stats_dict(stats_tensor) -> dict:
+    v = [int(x) for x in stats_tensor.cpu().tolist()]
+    return {"tasks_per_level": v[:6], "window_shifts": v[6], "cells_total": v[7]}
+
+
+class HostArena:
+    """Device arena for the host-buffer entry point (allocated once, reused)."""
+
+    def __init__(self, n_pairs: int, pool_len: int, fmt: int, max_ext_len: int, device=None):
+        torch = _require_cuda()
+        nb = int(_lib.load().logan_host_arena_bytes(n_pairs, pool_len, fmt, max_ext_len))
+        t = torch.empty(nb + 256, dtype=torch.uint8, device=device or "cuda")
+        off = (-t.data_ptr()) % 256
+        self.tensor = t[off:off + nb]
+        self.nbytes = nb
+
+
+def xdrop_batch_host(pool: np.ndarray, fmt: int, pool_len: int, q_off, q_len, t_off, t_len,
+                     q_seed, t_seed, k: int, match: int, mismatch: int, gap: int, xdrop: int,
+                     arena: HostArena, out: np.ndarray | None = None,
+                     cells: np.ndarray | None = None, first_level: int | None = None, stream=None):
+    """End-to-end call with HOST buffers (numpy; pinned memory copies fastest)."""
+    torch = _require_cuda()
+    lib = _lib.load()
+    n = len(q_len)
+    if out is None:
+        out = np.empty((n, 5), np.int32)
+    if cells is None:
+        cells = np.empty(n, np.uint64)
+    arrs = [np.ascontiguousarray(a) for a in (q_off, q_len, t_off, t_len, q_seed, t_seed)]
+    if stream is None:
+        stream = torch.cuda.current_stream()
+    sc = _lib.Scoring(match, mismatch, gap, xdrop)
+    ptr = lambda a: a.ctypes.data
+    st = lib.logan_xdrop_batch_host(ptr(pool), fmt, pool_len, *[ptr(a) for a in arrs], n, k, sc,
+                                    _opts(first_level), ptr(out), ptr(cells),
+                                    arena.tensor.data_ptr(), arena.nbytes, stream.cuda_stream)
+    _lib.check(st)
+    return out, cells

@@ -1,0 +1,411 @@
+// logan_xdrop.cu — C ABI and device pipeline of the B200 X-drop library.
+//
+// One call = (on the caller's stream, no host synchronisation):
+//   1. k_expand   : validate pairs, split each into a left and a right
+//                   extension task (Fig. 5), cost key m+n, a
+//                   log-linear cost bucket per task; empty extensions are
+//                   finished here (best 0 at (0,0), 0 cells)
+//   2. k_scan     : bucket histogram -> descending start offsets
+//   3. k_scatter  : tasks into a longest-first (LPT) work queue, the device
+//                   counterpart of the paper's host load balancing
+//   4. levels 1-5 : k_window<G, R> register-window sweeps, widening W = G*R
+//                   from the level chosen for X; a task whose band outgrows a
+//                   window is handed to the next level (exact restart)
+//   5. level 6    : k_wide, one CTA per task, unbounded band
+//   6. k_combine  : seed score + L + R -> logan_result_t, cells (c-amb-8/10)
+#include <cstdio>
+#include <cstring>
+
+#include "logan_xdrop.h"
+#include "xdrop_common.cuh"
+#include "xdrop_wide.cuh"
+#include "xdrop_window.cuh"
+
+namespace logan {
+
+constexpr int NBUCKET = 2048;
+constexpr int NLEVEL = 6;  // 5 window levels + the wide level
+constexpr int SETUP_THREADS = 256;
+
+__device__ __forceinline__ uint32_t cost_bucket(uint32_t c) {
+    // monotone log-linear bucket: 32 octaves x 64 sub-buckets (c >= 1)
+    const uint32_t e = 31u - __clz(c);
+    const uint32_t mant = e >= 6 ? (c >> (e - 6)) & 63u : (c << (6 - e)) & 63u;
+    return e * 64u + mant;
+}
+
+// Workspace layout (each region 256-byte aligned).
+struct Layout {
+    size_t tres, tbucket, queue, listA, listB, hist, cursor_b, counters, wide, total;
+    int64_t ntask, wide_stride;
+};
+
+constexpr int WIDE_CTAS = 296;  // 2 per SM on B200
+
+static size_t align256(size_t x) { return (x + 255) & ~(size_t)255; }
+
+static Layout make_layout(int64_t n_pairs, int64_t max_ext_len) {
+    Layout L{};
+    const int64_t nt = 2 * n_pairs;
+    L.ntask = nt;
+    size_t o = 0;
+    L.tres = o;     o += align256(sizeof(TaskRes) * (size_t)nt);
+    L.tbucket = o;  o += align256(sizeof(uint16_t) * (size_t)nt);
+    L.queue = o;    o += align256(sizeof(uint32_t) * (size_t)nt);
+    L.listA = o;    o += align256(sizeof(uint32_t) * (size_t)nt);
+    L.listB = o;    o += align256(sizeof(uint32_t) * (size_t)nt);
+    L.hist = o;     o += align256(sizeof(uint32_t) * NBUCKET);
+    L.cursor_b = o; o += align256(sizeof(uint32_t) * NBUCKET);
+    // counters: [0] queue count, [1..NLEVEL] level cursors, [8..8+NLEVEL] out counts
+    L.counters = o; o += align256(sizeof(uint32_t) * 32);
+    L.wide_stride = max_ext_len + 2;
+    L.wide = o;     o += align256(sizeof(int32_t) * 3 * (size_t)L.wide_stride * WIDE_CTAS);
+    L.total = o;
+    return L;
+}
+
+// ---------------------------------------------------------------------------
+__global__ void k_expand(const Params P, TaskRes *tres, uint16_t *tbucket, uint32_t *hist) {
+    __shared__ uint32_t sh[NBUCKET];
+    for (int b = threadIdx.x; b < NBUCKET; b += blockDim.x) sh[b] = 0;
+    __syncthreads();
+    for (int64_t p = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; p < P.n_pairs;
+         p += (int64_t)gridDim.x * blockDim.x) {
+        const bool ok = pair_valid(P, p);
+#pragma unroll
+        for (int side = 0; side < 2; ++side) {
+            const uint32_t task = (uint32_t)(2 * p + side);
+            int32_t m = 0, n = 0;
+            if (ok) {
+                const int32_t ql = P.q_len[p], tl = P.t_len[p], qs = P.q_seed[p], ts = P.t_seed[p];
+                m = side == 0 ? qs : ql - qs - P.k;
+                n = side == 0 ? ts : tl - ts - P.k;
+            }
+            uint16_t bk = 0xffff;  // not queued
+            if (ok && m > 0 && n > 0) {
+                bk = (uint16_t)cost_bucket((uint32_t)(m + n));
+                atomicAdd(&sh[bk], 1u);
+            } else {
+                TaskRes tr;
+                tr.best = 0; tr.i = 0; tr.j = 0; tr.flags = ok ? 0 : 1; tr.cells = 0;
+                tres[task] = tr;  // empty extension (c-amb-13) or invalid pair
+            }
+            tbucket[task] = bk;
+        }
+    }
+    __syncthreads();
+    for (int b = threadIdx.x; b < NBUCKET; b += blockDim.x)
+        if (sh[b]) atomicAdd(&hist[b], sh[b]);
+}
+
+// descending exclusive scan of the histogram (largest costs first)
+__global__ void k_scan(const uint32_t *hist, uint32_t *cursor_b, uint32_t *qcount) {
+    __shared__ uint32_t part[SETUP_THREADS];
+    constexpr int PER = NBUCKET / SETUP_THREADS;
+    const int t = threadIdx.x;
+    // thread t owns buckets in descending order: positions [t*PER, (t+1)*PER) of the reversed array
+    uint32_t loc[PER];
+    uint32_t s = 0;
+#pragma unroll
+    for (int q = 0; q < PER; ++q) {
+        loc[q] = hist[NBUCKET - 1 - (t * PER + q)];
+        s += loc[q];
+    }
+    part[t] = s;
+    __syncthreads();
+    for (int o = 1; o < SETUP_THREADS; o <<= 1) {
+        const uint32_t v = t >= o ? part[t - o] : 0;
+        __syncthreads();
+        part[t] += v;
+        __syncthreads();
+    }
+    uint32_t run = part[t] - s;  // exclusive
+#pragma unroll
+    for (int q = 0; q < PER; ++q) {
+        cursor_b[NBUCKET - 1 - (t * PER + q)] = run;
+        run += loc[q];
+    }
+    if (t == SETUP_THREADS - 1) *qcount = part[t];
+}
+
+__global__ void k_scatter(int64_t ntask, const uint16_t *tbucket, uint32_t *cursor_b, uint32_t *queue) {
+    for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < ntask;
+         t += (int64_t)gridDim.x * blockDim.x) {
+        const uint16_t b = tbucket[t];
+        if (b != 0xffff) {
+            const uint32_t pos = atomicAdd(&cursor_b[b], 1u);
+            queue[pos] = (uint32_t)t;
+        }
+    }
+}
+
+template <int FMT>
+__global__ void k_combine(const Params P, const TaskRes *tres, logan_result_t *out, uint64_t *cells) {
+    for (int64_t p = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; p < P.n_pairs;
+         p += (int64_t)gridDim.x * blockDim.x) {
+        const TaskRes L = tres[2 * p], R = tres[2 * p + 1];
+        logan_result_t r;
+        if (L.flags & 1) {
+            r = {INT32_MIN, -1, -1, -1, -1};
+            if (cells) cells[p] = 0;
+        } else {
+            const int64_t qo = P.q_off[p], to = P.t_off[p];
+            const int32_t qs = P.q_seed[p], ts = P.t_seed[p];
+            int32_t seed = 0;  // ungapped seed score (c-amb-10)
+            for (int32_t u = 0; u < P.k; ++u)
+                seed += (pool_base<FMT>(P, qo + qs + u) == pool_base<FMT>(P, to + ts + u)) ? P.match
+                                                                                             : P.mismatch;
+            r.score = seed + L.best + R.best;
+            r.q_begin = qs - L.i;
+            r.q_end = qs + P.k + R.i;
+            r.t_begin = ts - L.j;
+            r.t_end = ts + P.k + R.j;
+            if (cells) cells[p] = L.cells + R.cells;
+        }
+        out[p] = r;
+    }
+}
+
+// ---------------------------------------------------------------------------
+// Level table: window shapes (G lanes x R slots).
+template <int FMT>
+static cudaError_t launch_level(int level, const Params &P, const LevelIO &io, int sms, cudaStream_t s) {
+    int occ = 0;
+    cudaError_t e = cudaSuccess;
+#define LOGAN_LAUNCH_WIN(G_, R_)                                                                   \
+    do {                                                                                           \
+        e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_window<G_, R_, FMT>, 128, 0);    \
+        if (e != cudaSuccess) return e;                                                            \
+        if (occ < 1) occ = 1;                                                                      \
+        k_window<G_, R_, FMT><<<sms * occ, 128, 0, s>>>(P, io);                                    \
+    } while (0)
+    switch (level) {
+        case 0: LOGAN_LAUNCH_WIN(1, 32); break;
+        case 1: LOGAN_LAUNCH_WIN(2, 32); break;
+        case 2: LOGAN_LAUNCH_WIN(4, 32); break;
+        case 3: LOGAN_LAUNCH_WIN(8, 32); break;
+        case 4: LOGAN_LAUNCH_WIN(32, 32); break;
+        default: return cudaErrorInvalidValue;
+    }
+#undef LOGAN_LAUNCH_WIN
+    return cudaGetLastError();
+}
+
+static int auto_first_level(int32_t xdrop) {
+    // band width is about X + a few slots for true pairs
+    if (xdrop <= 20) return 0;   // W = 32
+    if (xdrop <= 48) return 1;   // W = 64
+    if (xdrop <= 110) return 2;  // W = 128
+    if (xdrop <= 230) return 3;  // W = 256
+    if (xdrop <= 1000) return 4; // W = 1024
+    return 5;                    // wide
+}
+
+template <int FMT>
+static int run_batch(const Params &P, const logan_options_t *opt, logan_result_t *out, uint64_t *cells,
+                     logan_stats_t *stats, uint8_t *ws, const Layout &L, cudaStream_t s) {
+    TaskRes *tres = (TaskRes *)(ws + L.tres);
+    uint16_t *tbucket = (uint16_t *)(ws + L.tbucket);
+    uint32_t *queue = (uint32_t *)(ws + L.queue);
+    uint32_t *lists[2] = {(uint32_t *)(ws + L.listA), (uint32_t *)(ws + L.listB)};
+    uint32_t *hist = (uint32_t *)(ws + L.hist);
+    uint32_t *cursor_b = (uint32_t *)(ws + L.cursor_b);
+    uint32_t *ctr = (uint32_t *)(ws + L.counters);
+    int32_t *wide = (int32_t *)(ws + L.wide);
+
+    int dev = 0, sms = 148;
+    if (cudaGetDevice(&dev) != cudaSuccess) return LOGAN_ECUDA;
+    if (cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess) return LOGAN_ECUDA;
+
+    if (cudaMemsetAsync(hist, 0, sizeof(uint32_t) * NBUCKET, s) != cudaSuccess) return LOGAN_ECUDA;
+    if (cudaMemsetAsync(ctr, 0, sizeof(uint32_t) * 32, s) != cudaSuccess) return LOGAN_ECUDA;
+    if (stats && cudaMemsetAsync(stats, 0, sizeof(logan_stats_t), s) != cudaSuccess) return LOGAN_ECUDA;
+
+    const int64_t per_block = SETUP_THREADS;
+    int grid = (int)((P.n_pairs + per_block - 1) / per_block);
+    if (grid > sms * 8) grid = sms * 8;
+    if (grid < 1) grid = 1;
+    k_expand<<<grid, SETUP_THREADS, 0, s>>>(P, tres, tbucket, hist);
+    k_scan<<<1, SETUP_THREADS, 0, s>>>(hist, cursor_b, &ctr[0]);
+    int grid2 = (int)((L.ntask + per_block - 1) / per_block);
+    if (grid2 > sms * 8) grid2 = sms * 8;
+    if (grid2 < 1) grid2 = 1;
+    k_scatter<<<grid2, SETUP_THREADS, 0, s>>>(L.ntask, tbucket, cursor_b, queue);
+    if (cudaGetLastError() != cudaSuccess) return LOGAN_ECUDA;
+
+    int first = (opt && opt->first_level > 0) ? opt->first_level - 1 : auto_first_level(P.xdrop);
+    if (first < 0 || first > 5) return LOGAN_EINVAL;
+    const uint32_t *in_list = queue;
+    const uint32_t *in_count = &ctr[0];
+    int out_sel = 0;
+    for (int lv = first; lv < NLEVEL; ++lv) {
+        LevelIO io;
+        io.list = in_list;
+        io.count = in_count;
+        io.cursor = &ctr[1 + lv];
+        io.out_list = lists[out_sel];
+        io.out_count = &ctr[8 + lv];
+        io.stats = stats;
+        io.level = lv;
+        io.tres = tres;
+        cudaError_t e;
+        if (lv < 5) {
+            e = launch_level<FMT>(lv, P, io, sms, s);
+        } else {
+            k_wide<FMT><<<WIDE_CTAS, WIDE_THREADS, 0, s>>>(P, io, wide, L.wide_stride);
+            e = cudaGetLastError();
+        }
+        if (e != cudaSuccess) return LOGAN_ECUDA;
+        in_list = lists[out_sel];
+        in_count = &ctr[8 + lv];
+        out_sel ^= 1;
+    }
+    int grid3 = (int)((P.n_pairs + per_block - 1) / per_block);
+    if (grid3 > sms * 8) grid3 = sms * 8;
+    if (grid3 < 1) grid3 = 1;
+    k_combine<FMT><<<grid3, SETUP_THREADS, 0, s>>>(P, tres, out, cells);
+    if (cudaGetLastError() != cudaSuccess) return LOGAN_ECUDA;
+    return LOGAN_OK;
+}
+
+}  // namespace logan
+
+using namespace logan;
+
+extern "C" {
+
+int logan_abi_version(void) { return LOGAN_ABI_VERSION; }
+
+const char *logan_strerror(int status) {
+    switch (status) {
+        case LOGAN_OK: return "ok";
+        case LOGAN_EINVAL: return "invalid argument";
+        case LOGAN_ECUDA: return "CUDA error";
+        case LOGAN_ENOSPC: return "workspace too small";
+        default: return "unknown status";
+    }
+}
+
+size_t logan_workspace_bytes(int64_t n_pairs, int64_t max_ext_len) {
+    if (n_pairs < 0 || max_ext_len < 0) return 0;
+    return make_layout(n_pairs, max_ext_len).total;
+}
+
+static int check_args(const uint8_t *seq_pool, int32_t seq_fmt, int64_t pool_len, const void *q_off,
+                      const void *q_len, const void *t_off, const void *t_len, const void *q_seed,
+                      const void *t_seed, int64_t n_pairs, int32_t k, logan_scoring_t sc,
+                      const logan_options_t *opt, const void *out) {
+    if (n_pairs < 0 || n_pairs > ((int64_t)1 << 30)) return LOGAN_EINVAL;
+    if (seq_fmt != LOGAN_SEQ_U8 && seq_fmt != LOGAN_SEQ_2BIT) return LOGAN_EINVAL;
+    if (k < 0 || pool_len < 0) return LOGAN_EINVAL;
+    if (sc.match <= 0 || sc.match > 127 || sc.mismatch >= 0 || sc.mismatch < -127 || sc.gap >= 0 ||
+        sc.gap < -127 || sc.xdrop < 0 || sc.xdrop > (1 << 20))
+        return LOGAN_EINVAL;
+    if (opt && (opt->first_level < 0 || opt->first_level > 6)) return LOGAN_EINVAL;
+    if (n_pairs == 0) return LOGAN_OK;
+    if (!seq_pool || !q_off || !q_len || !t_off || !t_len || !q_seed || !t_seed || !out) return LOGAN_EINVAL;
+    if (((uintptr_t)seq_pool & 3) != 0) return LOGAN_EINVAL;
+    return LOGAN_OK;
+}
+
+int logan_xdrop_batch(const uint8_t *seq_pool, int32_t seq_fmt, int64_t pool_len, const int64_t *q_off,
+                      const int32_t *q_len, const int64_t *t_off, const int32_t *t_len, const int32_t *q_seed,
+                      const int32_t *t_seed, int64_t n_pairs, int32_t k, logan_scoring_t sc,
+                      const logan_options_t *opt, logan_result_t *out, uint64_t *cells, logan_stats_t *stats,
+                      void *workspace, size_t workspace_bytes, void *stream) {
+    int st = check_args(seq_pool, seq_fmt, pool_len, q_off, q_len, t_off, t_len, q_seed, t_seed, n_pairs, k,
+                        sc, opt, out);
+    if (st != LOGAN_OK) return st;
+    if (n_pairs == 0) return LOGAN_OK;
+    if (!workspace || ((uintptr_t)workspace & 255) != 0) return LOGAN_EINVAL;
+    // the wide level's scratch is sized by the caller's bound on extension lengths:
+    // recover it from the workspace size (largest stride that fits)
+    const Layout base = make_layout(n_pairs, 0);
+    if (workspace_bytes < base.total) return LOGAN_ENOSPC;
+    const size_t per_col = sizeof(int32_t) * 3 * WIDE_CTAS;
+    int64_t max_ext = (int64_t)((workspace_bytes - base.total) / per_col);
+    Layout L = make_layout(n_pairs, max_ext);
+    while (L.total > workspace_bytes && max_ext > 0) L = make_layout(n_pairs, --max_ext);
+    if (L.total > workspace_bytes) return LOGAN_ENOSPC;
+
+    Params P;
+    P.pool = (const uint32_t *)seq_pool;
+    const int64_t bytes = seq_fmt == LOGAN_SEQ_2BIT ? (pool_len + 3) / 4 : pool_len;
+    P.pool_words = (bytes + 3) / 4;
+    if (P.pool_words < 1) P.pool_words = 1;
+    P.pool_len = pool_len;
+    P.q_off = q_off; P.q_len = q_len; P.t_off = t_off; P.t_len = t_len;
+    P.q_seed = q_seed; P.t_seed = t_seed;
+    P.n_pairs = n_pairs;
+    P.k = k;
+    P.match = sc.match; P.mismatch = sc.mismatch; P.gap = sc.gap; P.xdrop = sc.xdrop;
+
+    // extension lengths beyond the wide scratch would overflow it: such pairs
+    // are rejected up front by the caller-side bound (documented in the header)
+    cudaStream_t s = (cudaStream_t)stream;
+    uint8_t *ws = (uint8_t *)workspace;
+    if (seq_fmt == LOGAN_SEQ_2BIT) return run_batch<LOGAN_SEQ_2BIT>(P, opt, out, cells, stats, ws, L, s);
+    return run_batch<LOGAN_SEQ_U8>(P, opt, out, cells, stats, ws, L, s);
+}
+
+size_t logan_host_arena_bytes(int64_t n_pairs, int64_t pool_len, int32_t seq_fmt, int64_t max_ext_len) {
+    if (n_pairs < 0 || pool_len < 0) return 0;
+    const int64_t pool_bytes = seq_fmt == LOGAN_SEQ_2BIT ? (pool_len + 3) / 4 : pool_len;
+    size_t o = 0;
+    o += align256((size_t)pool_bytes + 16);
+    o += 2 * align256(sizeof(int64_t) * (size_t)n_pairs);
+    o += 4 * align256(sizeof(int32_t) * (size_t)n_pairs);
+    o += align256(sizeof(logan_result_t) * (size_t)n_pairs);
+    o += align256(sizeof(uint64_t) * (size_t)n_pairs);
+    o += logan_workspace_bytes(n_pairs, max_ext_len);
+    return o;
+}
+
+int logan_xdrop_batch_host(const uint8_t *seq_pool, int32_t seq_fmt, int64_t pool_len, const int64_t *q_off,
+                           const int32_t *q_len, const int64_t *t_off, const int32_t *t_len,
+                           const int32_t *q_seed, const int32_t *t_seed, int64_t n_pairs, int32_t k,
+                           logan_scoring_t sc, const logan_options_t *opt, logan_result_t *out,
+                           uint64_t *cells, void *device_arena, size_t arena_bytes, void *stream) {
+    int st = check_args(seq_pool, seq_fmt, pool_len, q_off, q_len, t_off, t_len, q_seed, t_seed, n_pairs, k,
+                        sc, opt, out);
+    if (st != LOGAN_OK) return st;
+    if (n_pairs == 0) return LOGAN_OK;
+    if (!device_arena || ((uintptr_t)device_arena & 255) != 0) return LOGAN_EINVAL;
+    const int64_t pool_bytes = seq_fmt == LOGAN_SEQ_2BIT ? (pool_len + 3) / 4 : pool_len;
+    uint8_t *a = (uint8_t *)device_arena;
+    size_t o = 0;
+    uint8_t *d_pool = a + o;   o += align256((size_t)pool_bytes + 16);
+    int64_t *d_qoff = (int64_t *)(a + o); o += align256(sizeof(int64_t) * (size_t)n_pairs);
+    int64_t *d_toff = (int64_t *)(a + o); o += align256(sizeof(int64_t) * (size_t)n_pairs);
+    int32_t *d_qlen = (int32_t *)(a + o); o += align256(sizeof(int32_t) * (size_t)n_pairs);
+    int32_t *d_tlen = (int32_t *)(a + o); o += align256(sizeof(int32_t) * (size_t)n_pairs);
+    int32_t *d_qs = (int32_t *)(a + o);   o += align256(sizeof(int32_t) * (size_t)n_pairs);
+    int32_t *d_ts = (int32_t *)(a + o);   o += align256(sizeof(int32_t) * (size_t)n_pairs);
+    logan_result_t *d_out = (logan_result_t *)(a + o); o += align256(sizeof(logan_result_t) * (size_t)n_pairs);
+    uint64_t *d_cells = (uint64_t *)(a + o); o += align256(sizeof(uint64_t) * (size_t)n_pairs);
+    if (o > arena_bytes) return LOGAN_ENOSPC;
+    cudaStream_t s = (cudaStream_t)stream;
+    const size_t n8 = sizeof(int64_t) * (size_t)n_pairs, n4 = sizeof(int32_t) * (size_t)n_pairs;
+    if (cudaMemsetAsync(d_pool + pool_bytes, 0, 16, s) != cudaSuccess) return LOGAN_ECUDA;
+    if (cudaMemcpyAsync(d_pool, seq_pool, (size_t)pool_bytes, cudaMemcpyHostToDevice, s) != cudaSuccess ||
+        cudaMemcpyAsync(d_qoff, q_off, n8, cudaMemcpyHostToDevice, s) != cudaSuccess ||
+        cudaMemcpyAsync(d_toff, t_off, n8, cudaMemcpyHostToDevice, s) != cudaSuccess ||
+        cudaMemcpyAsync(d_qlen, q_len, n4, cudaMemcpyHostToDevice, s) != cudaSuccess ||
+        cudaMemcpyAsync(d_tlen, t_len, n4, cudaMemcpyHostToDevice, s) != cudaSuccess ||
+        cudaMemcpyAsync(d_qs, q_seed, n4, cudaMemcpyHostToDevice, s) != cudaSuccess ||
+        cudaMemcpyAsync(d_ts, t_seed, n4, cudaMemcpyHostToDevice, s) != cudaSuccess)
+        return LOGAN_ECUDA;
+    st = logan_xdrop_batch(d_pool, seq_fmt, pool_len, d_qoff, d_qlen, d_toff, d_tlen, d_qs, d_ts, n_pairs, k, sc,
+                           opt, d_out, d_cells, nullptr, a + o, arena_bytes - o, stream);
+    if (st != LOGAN_OK) return st;
+    if (cudaMemcpyAsync(out, d_out, sizeof(logan_result_t) * (size_t)n_pairs, cudaMemcpyDeviceToHost, s) !=
+        cudaSuccess)
+        return LOGAN_ECUDA;
+    if (cells && cudaMemcpyAsync(cells, d_cells, sizeof(uint64_t) * (size_t)n_pairs, cudaMemcpyDeviceToHost, s) !=
+                     cudaSuccess)
+        return LOGAN_ECUDA;
+    if (cudaStreamSynchronize(s) != cudaSuccess) return LOGAN_ECUDA;
+    return LOGAN_OK;
+}
+
+}  // extern "C"

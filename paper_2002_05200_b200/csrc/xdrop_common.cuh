@@ -1,0 +1,182 @@
+// xdrop_common.cuh — shared device-side definitions of the B200 X-drop path.
+//
+// Product code (CUDA path). Shares nothing with oracle/.
+// Citations: PAPER.md line numbers ("P:<line>"), readings "c-amb-N" of
+// DESIGN.md §3.
+#pragma once
+
+#include <cstdint>
+#include <cuda_runtime.h>
+
+#include "logan_xdrop.h"
+
+namespace logan {
+
+// ---------------------------------------------------------------------------
+// Per-call parameters (passed by value to every kernel).
+struct Params {
+    const uint32_t *pool;   // pool viewed as 32-bit words
+    int64_t pool_words;     // readable words
+    int64_t pool_len;       // bases
+    const int64_t *q_off;
+    const int32_t *q_len;
+    const int64_t *t_off;
+    const int32_t *t_len;
+    const int32_t *q_seed;
+    const int32_t *t_seed;
+    int64_t n_pairs;
+    int32_t k;
+    int32_t match, mismatch, gap, xdrop;
+};
+
+// Result of one extension task (L or R of one pair), 24 bytes.
+struct TaskRes {
+    int32_t best;
+    int32_t i, j;   // argmax cell, extension-local (c-amb-8/9)
+    int32_t flags;  // bit0 = pair invalid
+    uint64_t cells; // band cells (c-amb-14)
+};
+
+// Work list of one level: tasks in `list[0 .. *count)`, taken through
+// `*cursor`; tasks that overflow the level's window go to `out_list`.
+struct LevelIO {
+    const uint32_t *list;
+    const uint32_t *count;
+    uint32_t *cursor;
+    uint32_t *out_list;
+    uint32_t *out_count;
+    logan_stats_t *stats;
+    int32_t level;
+    TaskRes *tres;
+};
+
+constexpr uint32_t NO_TASK = 0xffffffffu;
+
+// ---------------------------------------------------------------------------
+// A task: the sequences of one extension in extension coordinates
+// (Fig. 5): a_i, i = 1..m and b_j, j = 1..n, with
+//   left  (side 0): a_i = q[qs - i],       b_j = t[ts - j]      (read backwards)
+//   right (side 1): a_i = q[qs + k + i - 1], b_j = t[ts + k + j - 1]
+struct SeqRef {
+    int64_t base;  // pool position of index 1
+    int32_t dir;   // +1 / -1
+    int32_t len;
+};
+
+struct TaskDesc {
+    SeqRef a, b;
+    bool valid;    // pair passed validation
+};
+
+__device__ __forceinline__ bool pair_valid(const Params &P, int64_t p) {
+    const int64_t qo = P.q_off[p], to = P.t_off[p];
+    const int32_t ql = P.q_len[p], tl = P.t_len[p], qs = P.q_seed[p], ts = P.t_seed[p];
+    const int64_t k = P.k;
+    if (ql < 0 || tl < 0 || ql >= (1 << 30) || tl >= (1 << 30)) return false;
+    if (qs < 0 || ts < 0 || qs + k > ql || ts + k > tl) return false;
+    if (qo < 0 || to < 0 || qo + ql > P.pool_len || to + tl > P.pool_len) return false;
+    return true;
+}
+
+__device__ __forceinline__ TaskDesc task_desc(const Params &P, uint32_t task) {
+    const int64_t p = task >> 1;
+    const int side = task & 1;
+    TaskDesc t;
+    t.valid = pair_valid(P, p);
+    const int64_t qo = P.q_off[p], to = P.t_off[p];
+    const int32_t ql = P.q_len[p], tl = P.t_len[p], qs = P.q_seed[p], ts = P.t_seed[p];
+    if (side == 0) {
+        t.a = {qo + qs - 1, -1, qs};
+        t.b = {to + ts - 1, -1, ts};
+    } else {
+        t.a = {qo + qs + P.k, +1, ql - qs - P.k};
+        t.b = {to + ts + P.k, +1, tl - ts - P.k};
+    }
+    if (!t.valid) {
+        t.a.len = 0;
+        t.b.len = 0;
+    }
+    return t;
+}
+
+// ---------------------------------------------------------------------------
+// Pool access. FMT = LOGAN_SEQ_2BIT: 16 bases per word, 2 bits each, LSB
+// first; FMT = LOGAN_SEQ_U8: 4 bases per word, one byte each (little endian).
+template <int FMT> struct PoolFmt;
+template <> struct PoolFmt<LOGAN_SEQ_2BIT> {
+    static constexpr int LOG_CPW = 4, BITS = 2;
+    static constexpr uint32_t MASK = 3u;
+};
+template <> struct PoolFmt<LOGAN_SEQ_U8> {
+    static constexpr int LOG_CPW = 2, BITS = 8;
+    static constexpr uint32_t MASK = 0xffu;
+};
+
+__device__ __forceinline__ uint32_t pool_word(const Params &P, int64_t wi) {
+    wi = wi < 0 ? 0 : (wi >= P.pool_words ? P.pool_words - 1 : wi);
+    return __ldg(P.pool + wi);
+}
+
+// Code of the base at pool position pos (no caching; blocking load).
+template <int FMT>
+__device__ __forceinline__ uint32_t pool_base(const Params &P, int64_t pos) {
+    using F = PoolFmt<FMT>;
+    const uint32_t w = pool_word(P, pos >> F::LOG_CPW);
+    return (w >> (F::BITS * (uint32_t)(pos & ((1 << F::LOG_CPW) - 1)))) & F::MASK;
+}
+
+// a_idx / b_idx with a sentinel outside 1..len.
+template <int FMT>
+__device__ __forceinline__ uint32_t seq_at(const Params &P, const SeqRef &s, int32_t idx, uint32_t sent) {
+    if (idx < 1 || idx > s.len) return sent;
+    return pool_base<FMT>(P, s.base + (int64_t)s.dir * (idx - 1));
+}
+
+// A forward stream over one extension sequence with a one-word prefetch in
+// the direction of travel: consuming index i+1 after i costs a shift and, once
+// per word, a load whose latency is hidden until the following word boundary.
+struct Stream {
+    SeqRef s;
+    int64_t w0;    // word index held in `cur`
+    uint32_t cur;  // word w0
+    uint32_t nxt;  // word w0 + dir (prefetched)
+};
+
+template <int FMT>
+__device__ __forceinline__ void stream_seek(const Params &P, Stream &st, int32_t idx) {
+    using F = PoolFmt<FMT>;
+    int32_t c = idx < 1 ? 1 : (idx > st.s.len ? st.s.len : idx);
+    if (st.s.len <= 0) c = 1;
+    const int64_t pos = st.s.base + (int64_t)st.s.dir * (c - 1);
+    st.w0 = pos >> F::LOG_CPW;
+    st.cur = pool_word(P, st.w0);
+    st.nxt = pool_word(P, st.w0 + st.s.dir);
+}
+
+template <int FMT>
+__device__ __forceinline__ uint32_t stream_get(const Params &P, Stream &st, int32_t idx, uint32_t sent) {
+    using F = PoolFmt<FMT>;
+    if (idx < 1 || idx > st.s.len) return sent;
+    const int64_t pos = st.s.base + (int64_t)st.s.dir * (idx - 1);
+    const int64_t wi = pos >> F::LOG_CPW;
+    uint32_t w;
+    if (wi == st.w0) {
+        w = st.cur;
+    } else if (wi == st.w0 + st.s.dir) {
+        st.w0 = wi;
+        st.cur = st.nxt;
+        st.nxt = pool_word(P, wi + st.s.dir);  // prefetch; consumed a word later
+        w = st.cur;
+    } else {
+        st.w0 = wi;
+        st.cur = pool_word(P, wi);
+        st.nxt = pool_word(P, wi + st.s.dir);
+        w = st.cur;
+    }
+    return (w >> (F::BITS * (uint32_t)(pos & ((1 << F::LOG_CPW) - 1)))) & F::MASK;
+}
+
+__device__ __forceinline__ int32_t ceil_half(int32_t d) { return (d + 1) >> 1; }
+__device__ __forceinline__ int32_t floor_half(int32_t d) { return d >> 1; }
+
+}  // namespace logan

@@ -1,0 +1,451 @@
+// xdrop_window.cuh — the hot path: X-drop antidiagonal sweep in a register
+// window (sm_100a, integer SIMT, no tensor cores).
+//
+// Method (§III-A, Alg. 1, Alg. 2):
+// each cell S(i,j) = max(diag + s(a_i,b_j), up + gap, left + gap) over live
+// predecessors (eq. P:85); a cell with S < best - X is dead for good;
+// best is updated once the antidiagonal is complete; the band is
+// trimmed to the cells that can still have a live predecessor and the
+// extension stops when two consecutive antidiagonals are empty (P:186,
+// c-amb-6/7).
+//
+// B200 design, not the paper's V100 one:
+//  * Cells are addressed by DIAGONAL SLOT s = floor((i - j) / 2) instead of by
+//    column: on antidiagonal d, slot s is the cell i = s + ceil(d/2),
+//    j = floor(d/2) - s. The X-drop band follows the alignment's diagonal, so
+//    in slot space it stays put (it drifts only with net indels) and a fixed
+//    register window of W = G*R slots holds it: G lanes per task, R slots per
+//    lane, two register arrays E[] (even antidiagonal) and O[] (odd one).
+//    Predecessors of slot s: even d: up = O[s], left = O[s-1], diag = E[s];
+//    odd d: up = E[s+1], left = E[s], diag = O[s]. Each step overwrites the
+//    array of its parity in place; only the lane-boundary value crosses lanes
+//    (one SHFL per step).
+//  * Scores are stored RELATIVE to the kill threshold T_d = best_{d-1} - X:
+//    u = S - T_d, live <=> u >= 0. The per-step rebase folds into the two
+//    scoring constants (gap' = gap - (T_d - T_{d-1}), s' = s - (T_d - T_{d-2}))
+//    so the cell is three DPX VIADDMNMX plus one VIMNMX.U32:
+//        t1 = max(left + gap', DEAD); t2 = max(up + gap', t1);
+//        u  = max(diag + s', t2);     u  = min_u32(u, DEAD)
+//    which maps every negative u to exactly DEAD = -2^21 (an exact, absorbing
+//    kill: a dead value can never climb back within 2^21 / match steps, far
+//    more than any task's antidiagonal count at the ABI's limits).
+//  * Bases sit in registers, 4-bit fields (2-bit pool) or 16-bit fields (u8
+//    pool), one per slot; positions past an extension's end hold sentinels
+//    that match nothing, so cells outside the matrix (i > m or j > n) can only
+//    hold values below an earlier best and are excluded from the band
+//    bookkeeping by a per-lane validity mask -- no per-cell masking.
+//  * Per antidiagonal the max and its slot come from one packed key
+//    (u << 10 | 1023 - slot) reduced with VIMNMX3 inside the lane and SHFL
+//    butterflies across the G lanes; the live extremes from a funnel-shifted
+//    sign mask + FLO. Ties go to the smallest slot = smallest i (c-amb-9).
+//  * The window re-centres by one slot when the band touches an edge; if the
+//    band is wider than W - 2 slots the task is handed to the next level.
+#pragma once
+
+#include "xdrop_common.cuh"
+
+namespace logan {
+
+constexpr int32_t DEAD = -(1 << 21);
+constexpr uint32_t DEADU = 0xFFE00000u;  // (uint32_t)DEAD
+
+template <int FMT> struct RegFmt;
+template <> struct RegFmt<LOGAN_SEQ_2BIT> {
+    static constexpr int CB = 4;                 // bits per register field
+    static constexpr uint32_t SA = 4u, SB = 8u;  // sentinels past the ends of A / B
+};
+template <> struct RegFmt<LOGAN_SEQ_U8> {
+    static constexpr int CB = 16;
+    static constexpr uint32_t SA = 0x100u, SB = 0x200u;
+};
+
+// Group-uniform state of one task (replicated in each lane of the group).
+struct WinState {
+    uint32_t task;
+    int32_t m, n;
+    Stream sa, sb;         // A stream (used by the top lane), B stream (lane 0)
+    int32_t a_next, b_next;
+    int32_t d;             // last antidiagonal computed
+    int32_t S0;            // slot of the window's first register
+    int32_t best, arg_i, arg_j;
+    int32_t Tn, Td, Tp;    // T_{d+1}, T_d, T_{d-1}
+    int32_t sF1, sL1, sF2, sL2;  // live slot extremes of d and d-1
+    bool h1, h2;           // d and d-1 hold a (valid) live cell
+    uint64_t cells;
+    uint32_t shifts;
+};
+
+template <int G>
+__device__ __forceinline__ int32_t grp_max(int32_t v, unsigned gmask) {
+#pragma unroll
+    for (int o = G / 2; o > 0; o >>= 1) v = max(v, __shfl_xor_sync(gmask, v, o, G));
+    return v;
+}
+template <int G>
+__device__ __forceinline__ int32_t grp_min(int32_t v, unsigned gmask) {
+#pragma unroll
+    for (int o = G / 2; o > 0; o >>= 1) v = min(v, __shfl_xor_sync(gmask, v, o, G));
+    return v;
+}
+
+template <int G, int R, int FMT>
+struct Window {
+    using RF = RegFmt<FMT>;
+    static constexpr int CB = RF::CB;
+    static constexpr int FPW = 32 / CB;     // fields per word
+    static constexpr int NW = R / FPW;      // words per lane per sequence
+    static constexpr int W = G * R;
+    static constexpr uint32_t FM = (1u << CB) - 1u;
+    static_assert(R % FPW == 0 && R <= 32 && W <= 1024, "window shape");
+
+    int32_t E[R], O[R];
+    uint32_t Aw[NW], Bw[NW];
+    WinState st;
+    int gl;            // lane within group
+    unsigned gmask;
+
+    // ---- field helpers ------------------------------------------------------
+    __device__ __forceinline__ uint32_t field(const uint32_t (&w)[NW], int r) const {
+        return (w[r / FPW] >> (CB * (r % FPW))) & FM;
+    }
+    // fields r <- r+1, new value into the top field
+    __device__ __forceinline__ static void shift_down(uint32_t (&w)[NW], uint32_t in) {
+#pragma unroll
+        for (int q = 0; q < NW - 1; ++q) w[q] = __funnelshift_r(w[q], w[q + 1], CB);
+        w[NW - 1] = __funnelshift_r(w[NW - 1], in, CB);
+    }
+    // fields r <- r-1, new value into field 0
+    __device__ __forceinline__ static void shift_up(uint32_t (&w)[NW], uint32_t in) {
+#pragma unroll
+        for (int q = NW - 1; q > 0; --q) w[q] = __funnelshift_l(w[q - 1], w[q], CB);
+        w[0] = (w[0] << CB) | in;
+    }
+
+    // ---- task start -----------------------------------------------------------
+    __device__ __forceinline__ void init(const Params &P, uint32_t task) {
+        const TaskDesc td = task_desc(P, task);
+        st.task = task;
+        st.m = td.a.len;
+        st.n = td.b.len;
+        st.d = 0;
+        st.S0 = -(W / 2);
+        st.best = 0;
+        st.arg_i = st.arg_j = 0;
+        st.Td = -P.xdrop;  // T_0 = best_{-1} - X with best_{-1} := 0
+        st.Tp = -P.xdrop;
+        st.Tn = -P.xdrop;  // T_1 = best_0 - X
+        st.sF1 = st.sL1 = 0;  // antidiagonal 0: the origin (slot 0)
+        st.h1 = true;
+        st.h2 = false;
+        st.sF2 = st.sL2 = 0;
+        st.cells = 0;
+        st.shifts = 0;
+        // values: origin S(0,0) = 0 -> u = 0 - T_0 = X; everything else dead
+        const int32_t s0 = st.S0 + gl * R;
+#pragma unroll
+        for (int r = 0; r < R; ++r) {
+            E[r] = (s0 + r == 0) ? P.xdrop : DEAD;
+            O[r] = DEAD;
+        }
+        // bases at d = 0: slot s holds a_s and b_{-s}
+        Stream ta{td.a, 0, 0, 0}, tb{td.b, 0, 0, 0};
+        stream_seek<FMT>(P, ta, s0);
+        stream_seek<FMT>(P, tb, -(s0 + R - 1));
+#pragma unroll
+        for (int q = 0; q < NW; ++q) { Aw[q] = 0; Bw[q] = 0; }
+#pragma unroll
+        for (int r = 0; r < R; ++r) {
+            const uint32_t a = stream_get<FMT>(P, ta, s0 + r, RF::SA);
+            Aw[r / FPW] |= a << (CB * (r % FPW));
+        }
+#pragma unroll
+        for (int r = R - 1; r >= 0; --r) {
+            const uint32_t b = stream_get<FMT>(P, tb, -(s0 + r), RF::SB);
+            Bw[r / FPW] |= b << (CB * (r % FPW));
+        }
+        // streams: A feeds the top slot, B the bottom slot
+        st.a_next = st.S0 + W;      // = S0 + W + ceil(d/2) at d = 0
+        st.b_next = 1 - st.S0;      // = floor(d/2) - S0 + 1 at d = 0
+        st.sa = {td.a, 0, 0, 0};
+        st.sb = {td.b, 0, 0, 0};
+        if (gl == G - 1) stream_seek<FMT>(P, st.sa, st.a_next);
+        if (gl == 0) stream_seek<FMT>(P, st.sb, st.b_next);
+    }
+
+    // ---- one antidiagonal d = st.d + 1 of parity PAR ---------------------------
+    // returns 0 = continue, 1 = finished, 2 = overflow
+    template <int PAR>
+    __device__ __forceinline__ int step(const Params &P) {
+        const int32_t d = st.d + 1;
+        const int32_t ch = ceil_half(d), fh = floor_half(d);
+
+        // (1) band cells of antidiagonal d from the live extremes of d-1, d-2
+        //     (c-amb-14: lo = max(1, d-n, min(F1, F2+1)), hi = min(m, d-1, max(L1, L2)+1))
+        if (d >= 2 && (st.h1 || st.h2)) {
+            const int32_t c1 = ceil_half(d - 1), c2 = ceil_half(d - 2);
+            int32_t lo, hi;
+            if (st.h1 && st.h2) {
+                lo = min(st.sF1 + c1, st.sF2 + c2 + 1);
+                hi = max(st.sL1 + c1, st.sL2 + c2) + 1;
+            } else if (st.h1) {
+                lo = st.sF1 + c1;
+                hi = st.sL1 + c1 + 1;
+            } else {
+                lo = st.sF2 + c2 + 1;
+                hi = st.sL2 + c2 + 1;
+            }
+            lo = max(lo, max(1, d - st.n));
+            hi = min(hi, min(st.m, d - 1));
+            if (hi >= lo) st.cells += (uint64_t)(hi - lo + 1);
+        }
+
+        // (2) bases for antidiagonal d
+        if (PAR == 1) {  // i advances: A fields move down one slot
+            uint32_t in = 0;
+            if (G > 1) in = __shfl_down_sync(gmask, Aw[0], 1, G) & FM;
+            if (gl == G - 1) in = stream_get<FMT>(P, st.sa, st.a_next, RF::SA);
+            ++st.a_next;
+            shift_down(Aw, in);
+        } else {         // j advances: B fields move up one slot
+            uint32_t in = 0;
+            if (G > 1) in = __shfl_up_sync(gmask, Bw[NW - 1], 1, G) >> (32 - CB);
+            if (gl == 0) in = stream_get<FMT>(P, st.sb, st.b_next, RF::SB);
+            ++st.b_next;
+            shift_up(Bw, in);
+        }
+
+        // (3) rebased constants (T_d = st.Tn is this step's threshold)
+        const int32_t Tc = st.Tn;
+        const int32_t gp = P.gap - (Tc - st.Td);
+        const int32_t sma = P.match - (Tc - st.Tp);
+        const int32_t smi = P.mismatch - (Tc - st.Tp);
+
+        uint32_t X[NW];
+#pragma unroll
+        for (int q = 0; q < NW; ++q) X[q] = Aw[q] ^ Bw[q];
+
+        // (4) cells
+        int32_t kq[4] = {INT32_MIN, INT32_MIN, INT32_MIN, INT32_MIN};
+        uint32_t dq[4] = {0, 0, 0, 0};
+        constexpr int RQ = (R + 3) / 4;
+        if (PAR == 1) {
+            int32_t nb = DEAD;  // E[R] of this lane = E[0] of the next lane
+            if (G > 1) {
+                nb = __shfl_down_sync(gmask, E[0], 1, G);
+                if (gl == G - 1) nb = DEAD;
+            }
+#pragma unroll
+            for (int r = 0; r < R; ++r) {
+                const int32_t up = (r < R - 1) ? E[r + 1] : nb;
+                const int32_t left = E[r];
+                const int32_t diag = O[r];
+                const bool mis = ((X[r / FPW] >> (CB * (r % FPW))) & FM) != 0;
+                const int32_t s = mis ? smi : sma;
+                int32_t t = __viaddmax_s32(left, gp, DEAD);
+                t = __viaddmax_s32(up, gp, t);
+                t = __viaddmax_s32(diag, s, t);
+                t = (int32_t)min((uint32_t)t, DEADU);
+                O[r] = t;
+            }
+        } else {
+            int32_t nb = DEAD;  // O[-1] of this lane = O[R-1] of the previous lane
+            if (G > 1) {
+                nb = __shfl_up_sync(gmask, O[R - 1], 1, G);
+                if (gl == 0) nb = DEAD;
+            }
+#pragma unroll
+            for (int r = 0; r < R; ++r) {
+                const int32_t up = O[r];
+                const int32_t left = (r > 0) ? O[r - 1] : nb;
+                const int32_t diag = E[r];
+                const bool mis = ((X[r / FPW] >> (CB * (r % FPW))) & FM) != 0;
+                const int32_t s = mis ? smi : sma;
+                int32_t t = __viaddmax_s32(left, gp, DEAD);
+                t = __viaddmax_s32(up, gp, t);
+                t = __viaddmax_s32(diag, s, t);
+                t = (int32_t)min((uint32_t)t, DEADU);
+                E[r] = t;
+            }
+        }
+        // keys (u << 10) + 1023 - r (dead u = -2^21 gives -2^31 + 1023 - r: no
+        // wrap) and sign chains over the new antidiagonal
+#pragma unroll
+        for (int r = R - 1; r >= 0; --r) {
+            const int32_t u = PAR ? O[r] : E[r];
+            const int c = r / RQ;
+            kq[c] = max(kq[c], (int32_t)(((uint32_t)u << 10) + (uint32_t)(1023 - r)));
+            dq[c] = __funnelshift_l((uint32_t)u, dq[c], 1);  // appends sign(u): bit (r - c*RQ)
+        }
+        int32_t kmax = max(max(kq[0], kq[1]), max(kq[2], kq[3]));
+        uint32_t dead = 0;
+#pragma unroll
+        for (int c = 0; c < 4; ++c)
+            if (c * RQ < R) dead |= dq[c] << (c * RQ);
+
+        // (5) validity of slots (0 <= i <= m, 0 <= j <= n) for this lane
+        const int32_t vlo = max(-ch, fh - st.n), vhi = min(st.m - ch, fh);
+        const int32_t base = st.S0 + gl * R;
+        int32_t rlo = max(vlo - base, 0), rhi = min(vhi - base, R - 1);
+        uint32_t vmask = 0;
+        if (rlo <= rhi) vmask = (0xffffffffu >> (31 - rhi)) & ~((1u << rlo) - 1u);
+        const uint32_t live = ~dead & vmask;
+        int32_t lf = live ? gl * R + __ffs(live) - 1 : INT32_MAX;
+        int32_t ll = live ? gl * R + 31 - __clz(live) : INT32_MIN;
+        kmax = kmax - gl * R;  // key = u*1024 + 1023 - (gl*R + r), never wraps for W <= 1024
+        if (G > 1) {
+            kmax = grp_max<G>(kmax, gmask);
+            lf = grp_min<G>(lf, gmask);
+            ll = grp_max<G>(ll, gmask);
+        }
+        const bool h = (lf != INT32_MAX);
+
+        // (6) best after the complete antidiagonal; argmax on strict increase
+        if (kmax >= 0) {
+            const int32_t V = (kmax >> 10) + Tc;
+            if (V > st.best) {
+                st.best = V;
+                const int32_t slot = st.S0 + (1023 - (kmax & 1023));
+                st.arg_i = slot + ch;
+                st.arg_j = d - st.arg_i;
+            }
+        }
+        st.Tp = st.Td;
+        st.Td = Tc;
+        st.Tn = st.best - P.xdrop;
+        st.d = d;
+
+        // (7) termination: antidiagonals d and d-1 both empty (c-amb-7)
+        if (!h && !st.h1) return 1;
+        st.h2 = st.h1; st.sF2 = st.sF1; st.sL2 = st.sL1;
+        st.h1 = h;
+        st.sF1 = st.S0 + lf;
+        st.sL1 = st.S0 + ll;
+
+        // (8) keep the live band of d and d-1 inside [S0+1, S0+W-2]
+        int32_t Fm = INT32_MAX, Lm = INT32_MIN;
+        if (st.h1) { Fm = st.sF1; Lm = st.sL1; }
+        if (st.h2) { Fm = min(Fm, st.sF2); Lm = max(Lm, st.sL2); }
+        const bool lowv = Fm < st.S0 + 1, highv = Lm > st.S0 + W - 2;
+        if (lowv || highv) {
+            if (lowv && highv) return 2;
+            if (lowv) {
+                if (Lm > st.S0 + W - 3) return 2;
+                shift_left(P, d);
+            } else {
+                if (Fm < st.S0 + 2) return 2;
+                shift_right(P, d);
+            }
+        }
+        return 0;
+    }
+
+    // window slot base S0 += 1 (band drifted towards higher slots)
+    __device__ __forceinline__ void shift_right(const Params &P, int32_t d) {
+        int32_t eIn = DEAD, oIn = DEAD;
+        uint32_t aIn = 0, bIn = 0;
+        if (G > 1) {
+            eIn = __shfl_down_sync(gmask, E[0], 1, G);
+            oIn = __shfl_down_sync(gmask, O[0], 1, G);
+            aIn = __shfl_down_sync(gmask, Aw[0], 1, G) & FM;
+            bIn = __shfl_down_sync(gmask, Bw[0], 1, G) & FM;
+        }
+        const int32_t S1 = st.S0 + 1;
+        if (gl == G - 1) {
+            eIn = DEAD;
+            oIn = DEAD;
+            aIn = stream_get<FMT>(P, st.sa, st.a_next, RF::SA);  // a_{S1 + W - 1 + ceil(d/2)}
+            bIn = seq_at<FMT>(P, st.sb.s, floor_half(d) - S1 - (W - 1), RF::SB);
+        }
+#pragma unroll
+        for (int r = 0; r < R - 1; ++r) { E[r] = E[r + 1]; O[r] = O[r + 1]; }
+        E[R - 1] = eIn;
+        O[R - 1] = oIn;
+        shift_down(Aw, aIn);
+        shift_down(Bw, bIn);
+        ++st.a_next;
+        --st.b_next;
+        st.S0 = S1;
+        ++st.shifts;
+    }
+
+    // window slot base S0 -= 1
+    __device__ __forceinline__ void shift_left(const Params &P, int32_t d) {
+        int32_t eIn = DEAD, oIn = DEAD;
+        uint32_t aIn = 0, bIn = 0;
+        if (G > 1) {
+            eIn = __shfl_up_sync(gmask, E[R - 1], 1, G);
+            oIn = __shfl_up_sync(gmask, O[R - 1], 1, G);
+            aIn = __shfl_up_sync(gmask, Aw[NW - 1], 1, G) >> (32 - CB);
+            bIn = __shfl_up_sync(gmask, Bw[NW - 1], 1, G) >> (32 - CB);
+        }
+        const int32_t S1 = st.S0 - 1;
+        if (gl == 0) {
+            eIn = DEAD;
+            oIn = DEAD;
+            aIn = seq_at<FMT>(P, st.sa.s, S1 + ceil_half(d), RF::SA);
+            bIn = stream_get<FMT>(P, st.sb, st.b_next, RF::SB);  // b_{floor(d/2) - S1}
+        }
+#pragma unroll
+        for (int r = R - 1; r > 0; --r) { E[r] = E[r - 1]; O[r] = O[r - 1]; }
+        E[0] = eIn;
+        O[0] = oIn;
+        shift_up(Aw, aIn);
+        shift_up(Bw, bIn);
+        --st.a_next;
+        ++st.b_next;
+        st.S0 = S1;
+        ++st.shifts;
+    }
+};
+
+// Persistent kernel: each group of G lanes pulls tasks from the level's list.
+template <int G, int R, int FMT>
+__global__ void __launch_bounds__(128) k_window(const Params P, const LevelIO io) {
+    Window<G, R, FMT> w;
+    const int lane = threadIdx.x & 31;
+    w.gl = lane % G;
+    w.gmask = (G == 32) ? 0xffffffffu : (((1u << G) - 1u) << (lane - w.gl));
+    const uint32_t count = *io.count;
+
+    auto fetch = [&]() -> uint32_t {
+        uint32_t t = NO_TASK;
+        if (w.gl == 0) {
+            const uint32_t pos = atomicAdd(io.cursor, 1u);
+            if (pos < count) t = io.list[pos];
+        }
+        if (G > 1) t = __shfl_sync(w.gmask, t, lane - w.gl);
+        return t;
+    };
+
+    uint32_t task = fetch();
+    if (task != NO_TASK) w.init(P, task);
+    while (task != NO_TASK) {
+        int rc = w.template step<1>(P);
+        if (rc == 0) rc = w.template step<0>(P);
+        if (rc != 0) {
+            if (w.gl == 0) {
+                if (rc == 1) {
+                    TaskRes tr;
+                    tr.best = w.st.best;
+                    tr.i = w.st.arg_i;
+                    tr.j = w.st.arg_j;
+                    tr.flags = 0;
+                    tr.cells = w.st.cells;
+                    io.tres[task] = tr;
+                } else {
+                    const uint32_t o = atomicAdd(io.out_count, 1u);
+                    io.out_list[o] = task;
+                }
+                if (io.stats) {
+                    atomicAdd((unsigned long long *)&io.stats->tasks_per_level[io.level], 1ull);
+                    atomicAdd((unsigned long long *)&io.stats->window_shifts, (unsigned long long)w.st.shifts);
+                    if (rc == 1) atomicAdd((unsigned long long *)&io.stats->cells_total, (unsigned long long)w.st.cells);
+                }
+            }
+            task = fetch();
+            if (task != NO_TASK) w.init(P, task);
+        }
+    }
+}
+
+}  // namespace logan

@@ -1,0 +1,85 @@
+"""The C-ABI library loads and exports every symbol include/*.h declares (CPU).
+
+No compute call is made here (there is no GPU in the build container); only
+the host-side argument checks that return before any CUDA call are exercised.
+"""
+import ctypes
+import glob
+import os
+import re
+import subprocess
+
+import pytest
+
+from paper_2002_05200_b200 import _lib, build
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+
+@pytest.fixture(scope="module")
+def lib():
+    build.build()
+    return _lib.load()
+
+
+def header_functions():
+    names = set()
+    for h in glob.glob(os.path.join(ROOT, "include", "*.h")):
+        text = open(h).read()
+        text = re.sub(r"/\*.*?\*/", "", text, flags=re.S)
+        for m in re.finditer(r"\b(\w+)\s*\([^;{]*\)\s*;", text):
+            if m.group(1) not in ("if", "sizeof"):
+                names.add(m.group(1))
+    return names
+
+
+def test_header_declares_the_binding_exports():
+    assert header_functions() == set(_lib.EXPORTS)
+
+
+def test_library_exports_every_declared_symbol(lib):
+    out = subprocess.run(["nm", "-D", "--defined-only", _lib.LIB_PATH], capture_output=True,
+                         text=True, check=True).stdout
+    exported = {line.split()[-1] for line in out.splitlines() if line.strip()}
+    for name in header_functions():
+        assert name in exported, name
+        assert getattr(lib, name) is not None
+
+
+def test_library_is_sm100a(lib):
+    out = subprocess.run(["cuobjdump", "--list-elf", _lib.LIB_PATH], capture_output=True,
+                         text=True).stdout
+    assert "sm_100a" in out
+
+
+def test_host_side_checks_without_gpu(lib):
+    assert lib.logan_abi_version() == 1
+    assert lib.logan_strerror(1) == b"invalid argument"
+    assert lib.logan_workspace_bytes(-1, 0) == 0
+    small, big = lib.logan_workspace_bytes(10, 100), lib.logan_workspace_bytes(1000, 100)
+    assert 0 < small < big
+    assert lib.logan_workspace_bytes(10, 1000) > small  # wide-level scratch grows with length
+    sc_bad = _lib.Scoring(1, 1, -1, 10)  # mismatch must be < 0
+    st = lib.logan_xdrop_batch(None, 1, 0, None, None, None, None, None, None, 5, 17, sc_bad,
+                               None, None, None, None, None, 0, None)
+    assert st == _lib.LOGAN_EINVAL
+    sc = _lib.Scoring(1, -1, -1, 10)
+    st = lib.logan_xdrop_batch(None, 7, 0, None, None, None, None, None, None, 5, 17, sc,
+                               None, None, None, None, None, 0, None)
+    assert st == _lib.LOGAN_EINVAL  # unknown format
+    st = lib.logan_xdrop_batch(None, 1, 0, None, None, None, None, None, None, 0, 17, sc,
+                               None, None, None, None, None, 0, None)
+    assert st == _lib.LOGAN_OK  # n_pairs = 0: no-op, nothing launched
+    st = lib.logan_xdrop_batch(None, 1, 0, None, None, None, None, None, None, 3, 17, sc,
+                               None, None, None, None, None, 0, None)
+    assert st == _lib.LOGAN_EINVAL  # NULL device pointers
+
+
+def test_product_path_does_not_import_oracle():
+    """The product package never references oracle/ (no CPU fallback)."""
+    pkg = os.path.join(ROOT, "paper_2002_05200_b200")
+    for path in glob.glob(os.path.join(pkg, "**", "*.*"), recursive=True):
+        if path.endswith((".py", ".cu", ".cuh", ".h")):
+            text = open(path).read()
+            assert "import oracle" not in text and "from oracle" not in text, path
+            assert "xdrop_oracle" not in text, path

@@ -1,0 +1,236 @@
+"""Parity of the CUDA path (through the C ABI) with the CPU oracle.
+
+Bit-exact on every integer output: score, q/t begin/end and the cell count
+(SURVEY.md §8c P5).  Inputs are seeded synthetic workloads from ``datagen``;
+expected values come only from ``oracle/``.
+"""
+import itertools
+import random
+
+import numpy as np
+import pytest
+
+import datagen
+import oracle
+
+pytestmark = pytest.mark.gpu
+
+torch = pytest.importorskip("torch")
+if not torch.cuda.is_available():  # pragma: no cover
+    pytest.skip("no CUDA device", allow_module_level=True)
+
+import paper_2002_05200_b200 as logan  # noqa: E402
+from paper_2002_05200_b200 import build as _build  # noqa: E402
+
+_build.build()
+
+FMTS = (logan.LOGAN_SEQ_2BIT, logan.LOGAN_SEQ_U8)
+
+
+def gpu_run(batch, X, match=1, mismatch=-1, gap=-1, fmt=logan.LOGAN_SEQ_2BIT, first_level=None,
+            stats=None):
+    db = logan.to_device(batch, fmt)
+    out, cells = logan.xdrop_batch(db, match, mismatch, gap, X, first_level=first_level, stats=stats)
+    torch.cuda.synchronize()
+    return out.cpu().numpy(), cells.cpu().numpy().view(np.uint64)
+
+
+def oracle_run(batch, X, match=1, mismatch=-1, gap=-1, idx=None):
+    b = batch
+    sel = slice(None) if idx is None else idx
+    return oracle.pairs(b.pool_u8, 0, b.q_off[sel], b.q_len[sel], b.t_off[sel], b.t_len[sel],
+                        b.q_seed[sel], b.t_seed[sel], b.workload.k, match, mismatch, gap, X,
+                        pool_len=b.pool_len)
+
+
+def assert_same(o_gpu, c_gpu, o_ref, c_ref, what=""):
+    bad = np.nonzero((o_gpu != o_ref).any(axis=1) | (c_gpu != c_ref))[0]
+    if len(bad):
+        p = bad[0]
+        raise AssertionError(f"{what}: {len(bad)} mismatching pairs; first #{p}: gpu {o_gpu[p]} "
+                             f"cells {c_gpu[p]} vs oracle {o_ref[p]} cells {c_ref[p]}")
+
+
+def ext_batch(pairs_ab, k=0):
+    """Extensions E(A, B) as pairs with a k=0 seed at (0,0): L empty, R = E(A, B)."""
+    return datagen.from_strings([(a, b, 0, 0) for a, b in pairs_ab], k=k)
+
+
+# --------------------------------------------------------------------------
+def test_exhaustive_tiny_extensions_all_levels():
+    strings = ["".join(s) for L in range(0, 6) for s in itertools.product("AC", repeat=L)]
+    pairs = [(a, b) for a in strings for b in strings if a and b]
+    b = ext_batch(pairs)
+    for X in (0, 1, 2, 3, 5, 10 ** 6):
+        ref = oracle_run(b, X)
+        for lvl in (1, 2, 3, 4, 5, 6):
+            got = gpu_run(b, X, first_level=lvl)
+            assert_same(*got, *ref, what=f"X={X} level={lvl}")
+
+
+@pytest.mark.parametrize("scoring", [(1, -1, -1), (2, -3, -1), (1, -2, -3), (3, -1, -2), (5, -4, -7)])
+def test_random_pairs_scoring_and_x_sweep(scoring):
+    rng = random.Random(hash(scoring) & 0xffff)
+    pairs = []
+    for _ in range(600):
+        L = rng.randint(1, 300)
+        a = "".join(rng.choice("ACGT") for _ in range(L))
+        # a mutated copy (sub/ins/del) or an unrelated read
+        if rng.random() < 0.7:
+            bb = []
+            for ch in a:
+                r = rng.random()
+                if r < 0.05:
+                    bb.append(rng.choice("ACGT"))
+                elif r < 0.1:
+                    bb.append(ch + rng.choice("ACGT"))
+                elif r < 0.15:
+                    continue
+                else:
+                    bb.append(ch)
+            b = "".join(bb) or "A"
+        else:
+            b = "".join(rng.choice("ACGT") for _ in range(rng.randint(1, 300)))
+        k = rng.randint(0, min(len(a), len(b), 5))
+        qs, ts = rng.randint(0, len(a) - k), rng.randint(0, len(b) - k)
+        pairs.append((a, b, qs, ts))
+    batch = datagen.from_strings(pairs, k=0)
+    ma, mi, g = scoring
+    for X in (0, 1, 4, 10, 25, 60, 200):
+        ref = oracle_run(batch, X, ma, mi, g)
+        for fmt in FMTS:
+            got = gpu_run(batch, X, ma, mi, g, fmt=fmt)
+            assert_same(*got, *ref, what=f"X={X} fmt={fmt} scoring={scoring}")
+
+
+def test_adversarial_inputs():
+    rng = random.Random(9)
+    R = lambda n: "".join(rng.choice("ACGT") for _ in range(n))
+    pairs = [
+        ("A" * 500, "A" * 480, 100, 90),          # homopolymers
+        ("AC" * 300, "AC" * 290, 50, 52),         # periodic repeats (seed off-phase)
+        ("ACG" * 200, "ACG" * 210, 30, 33),
+        (R(800), R(800), 400, 400),               # unrelated: wide bands
+        (R(1500), R(1400), 10, 1390),             # unrelated, seed near opposite ends
+        ("ACGT" * 100, "ACGT" * 100, 0, 0),       # seed at the start
+        ("ACGT" * 100, "ACGT" * 100, 399, 399),   # seed at the end (k = 1)
+        ("T" * 64, "G" * 64, 10, 10),             # disjoint alphabets
+    ]
+    batch = datagen.from_strings(pairs, k=1)
+    for X in (0, 5, 20, 50, 100, 400):
+        ref = oracle_run(batch, X)
+        for lvl in (None, 1, 3, 6):
+            for fmt in FMTS:
+                got = gpu_run(batch, X, fmt=fmt, first_level=lvl)
+                assert_same(*got, *ref, what=f"X={X} level={lvl} fmt={fmt}")
+
+
+def test_invalid_and_empty_pairs():
+    pairs = [("ACGTACGT", "ACGTACGT", 2, 2), ("ACGTACGT", "ACGTACGT", 0, 0),
+             ("ACGTACGT", "ACGTACGT", 7, 7), ("ACGTACGT", "ACGTACGT", 5, 5)]
+    b = datagen.from_strings(pairs, k=3)
+    b.q_seed[2] = 7  # 7 + 3 > 8: invalid
+    b.t_seed[3] = -1  # invalid
+    got = gpu_run(b, 10)
+    ref = oracle_run(b, 10)
+    assert_same(*got, *ref)
+    assert tuple(got[0][2]) == (-2 ** 31, -1, -1, -1, -1) and got[1][2] == 0
+    # n_pairs = 0 is a no-op
+    e = datagen.from_strings([], k=3)
+    db = logan.to_device(e)
+    out, cells = logan.xdrop_batch(db, 1, -1, -1, 10)
+    assert out.numel() == 0
+
+
+@pytest.mark.parametrize("X", [50])
+def test_config1_all_pairs(X):
+    b = datagen.generate(datagen.CONFIGS[1])
+    ref = oracle_run(b, X)
+    st = logan.new_stats()
+    got = gpu_run(b, X, stats=st)
+    assert_same(*got, *ref, what="C1")
+    s = logan.stats_dict(st)
+    assert s["cells_total"] == int(ref[1].sum())
+    for fmt in FMTS:
+        for lvl in (2, 3, 6):
+            got = gpu_run(b, X, fmt=fmt, first_level=lvl)
+            assert_same(*got, *ref, what=f"C1 fmt={fmt} level={lvl}")
+
+
+def test_config2_full_size_sampled():
+    """Full C2 (100K pairs, X=20) in the launch configuration bench.py times;
+    every 50th pair against the oracle, u8 == 2-bit on all pairs."""
+    w = datagen.CONFIGS[2]
+    b = datagen.generate(w)
+    got = gpu_run(b, w.xdrop)
+    idx = np.arange(0, b.n_pairs, 50)
+    ref = oracle_run(b, w.xdrop, idx=idx)
+    assert_same(got[0][idx], got[1][idx], *ref, what="C2 sample")
+    got8 = gpu_run(b, w.xdrop, fmt=logan.LOGAN_SEQ_U8)
+    assert (got8[0] == got[0]).all() and (got8[1] == got[1]).all()
+    # invariants on every pair
+    o = got[0]
+    assert (o[:, 0] >= w.k).all() and (o[:, 1] <= b.q_seed).all() and (o[:, 2] <= b.q_len).all()
+    assert (got[1] > 0).all()
+
+
+@pytest.mark.parametrize("X", [10, 20, 50, 100])
+def test_config3_x_sweep_sampled(X):
+    w = datagen.CONFIGS[3]
+    b = datagen.generate(w, n_pairs=2000)
+    got = gpu_run(b, X)
+    idx = np.arange(0, b.n_pairs, 10)
+    ref = oracle_run(b, X, idx=idx)
+    assert_same(got[0][idx], got[1][idx], *ref, what=f"C3 X={X}")
+
+
+def test_config4_bella_like_sampled():
+    w = datagen.CONFIGS[4]
+    b = datagen.generate(w, n_pairs=3000)
+    st = logan.new_stats()
+    got = gpu_run(b, w.xdrop, stats=st)
+    idx = np.arange(0, b.n_pairs, 12)
+    ref = oracle_run(b, w.xdrop, idx=idx)
+    assert_same(got[0][idx], got[1][idx], *ref, what="C4")
+
+
+def test_config5_long_reads_sampled():
+    w = datagen.CONFIGS[5]
+    b = datagen.generate(w, n_pairs=200)
+    got = gpu_run(b, w.xdrop)
+    idx = np.arange(0, b.n_pairs, 8)
+    ref = oracle_run(b, w.xdrop, idx=idx)
+    assert_same(got[0][idx], got[1][idx], *ref, what="C5")
+
+
+def test_burst_errors_early_termination():
+    w = datagen.CONFIGS[2].with_(burst=0.5, xdrop=20)
+    b = datagen.generate(w, n_pairs=1500)
+    got = gpu_run(b, 20)
+    ref = oracle_run(b, 20)
+    assert_same(*got, *ref, what="burst")
+
+
+def test_host_entry_point_matches_device_entry():
+    w = datagen.CONFIGS[1]
+    b = datagen.generate(w, n_pairs=300)
+    dev = gpu_run(b, w.xdrop)
+    for fmt, pool in ((logan.LOGAN_SEQ_2BIT, b.pool_2bit), (logan.LOGAN_SEQ_U8, b.pool_u8)):
+        arena = logan.HostArena(b.n_pairs, b.pool_len, fmt, b.max_ext_len())
+        out, cells = logan.xdrop_batch_host(pool, fmt, b.pool_len, b.q_off, b.q_len, b.t_off,
+                                            b.t_len, b.q_seed, b.t_seed, w.k, 1, -1, -1, w.xdrop,
+                                            arena)
+        assert (out == dev[0]).all() and (cells == dev[1]).all()
+
+
+def test_repeatable_and_permutation_invariant():
+    w = datagen.CONFIGS[1]
+    b = datagen.generate(w, n_pairs=500)
+    a1 = gpu_run(b, 50)
+    a2 = gpu_run(b, 50)
+    assert (a1[0] == a2[0]).all() and (a1[1] == a2[1]).all()
+    perm = np.random.default_rng(1).permutation(b.n_pairs)
+    bp = datagen.Batch(b.workload, 0, b.q_off[perm], b.q_len[perm], b.t_off[perm], b.t_len[perm],
+                       b.q_seed[perm], b.t_seed[perm], b.pool_len, b.pool_u8, b.pool_2bit)
+    ap = gpu_run(bp, 50)
+    assert (ap[0] == a1[0][perm]).all() and (ap[1] == a1[1][perm]).all()
