@@ -74,20 +74,35 @@ enum {
     LOGAN_ENOSPC = 3  /* workspace smaller than logan_workspace_bytes()  */
 };
 
-/* Kernel-selection hint (0 = automatic). Values 1..5 force the first
- * register-window level (window of 32, 64, 128, 256, 1024 diagonal slots);
- * 6 forces every task onto the unbounded CTA path. Results never depend on
- * it (tests assert this); only speed does. */
+/* Options (may be passed as NULL = all defaults).
+ *  first_level   : 0 = automatic from xdrop; 1..5 force the first
+ *                  register-window level (windows of 32, 64, 128, 256, 1024
+ *                  diagonal slots); 6 forces every task onto the unbounded CTA
+ *                  level. Results never depend on it (tests assert this);
+ *                  only speed does.
+ *  timing_events : NULL, or LOGAN_N_STAGES * 2 cudaEvent_t created by the
+ *                  caller (timing enabled). Event [2s] is recorded on `stream`
+ *                  just before stage s and [2s+1] just after it, for every
+ *                  stage the call launches: stage 0 = setup (task expansion,
+ *                  LPT bucketing), stages 1..6 = levels 1..6, stage 7 =
+ *                  combine. Stages not launched leave their events untouched.
+ */
+#define LOGAN_N_STAGES 8
 typedef struct {
-    int32_t first_level;   /* 0 = auto from xdrop */
-    int32_t reserved[7];
+    int32_t first_level;
+    int32_t reserved0;
+    void *const *timing_events;
+    int64_t reserved[6];
 } logan_options_t;
 
-/* Per-call device-side statistics (optional output, device memory, may be
- * NULL): number of tasks that ran at each level (6 entries) and the number
- * of window shifts. Filled after the stream syncs. */
+/* Per-call device-side statistics (optional output in DEVICE memory, may be
+ * NULL; filled once the stream syncs): per level, the tasks that started
+ * there, the tasks that finished there and their band cells; window shifts
+ * summed over all tasks. */
 typedef struct {
-    uint64_t tasks_per_level[6];
+    uint64_t tasks_started[6];
+    uint64_t tasks_finished[6];
+    uint64_t cells_per_level[6];
     uint64_t window_shifts;
     uint64_t cells_total;
 } logan_stats_t;

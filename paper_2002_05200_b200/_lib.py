@@ -26,8 +26,12 @@ class Scoring(ctypes.Structure):
                 ("gap", ctypes.c_int32), ("xdrop", ctypes.c_int32)]
 
 
+N_STAGES = 8  # LOGAN_N_STAGES: 0 setup, 1..6 levels, 7 combine
+
+
 class Options(ctypes.Structure):
-    _fields_ = [("first_level", ctypes.c_int32), ("reserved", ctypes.c_int32 * 7)]
+    _fields_ = [("first_level", ctypes.c_int32), ("reserved0", ctypes.c_int32),
+                ("timing_events", ctypes.c_void_p), ("reserved", ctypes.c_int64 * 6)]
 
 
 class Result(ctypes.Structure):
@@ -36,7 +40,8 @@ class Result(ctypes.Structure):
 
 
 class Stats(ctypes.Structure):
-    _fields_ = [("tasks_per_level", ctypes.c_uint64 * 6), ("window_shifts", ctypes.c_uint64),
+    _fields_ = [("tasks_started", ctypes.c_uint64 * 6), ("tasks_finished", ctypes.c_uint64 * 6),
+                ("cells_per_level", ctypes.c_uint64 * 6), ("window_shifts", ctypes.c_uint64),
                 ("cells_total", ctypes.c_uint64)]
 
 

@@ -49,11 +49,17 @@ def make_workspace(n_pairs: int, max_ext_len: int, device=None) -> Workspace:
     return Workspace(t[off:off + max(nb, 256)], n_pairs, max_ext_len)
 
 
-def _opts(first_level: int | None):
-    if not first_level:
+def _opts(first_level: int | None, timing_events=None):
+    """Options struct; ``timing_events`` = list of 2*N_STAGES torch.cuda.Event."""
+    if not first_level and timing_events is None:
         return None
     o = _lib.Options()
-    o.first_level = int(first_level)
+    o.first_level = int(first_level or 0)
+    if timing_events is not None:
+        assert len(timing_events) == 2 * _lib.N_STAGES
+        arr = (ctypes.c_void_p * (2 * _lib.N_STAGES))(*[int(e.cuda_event) for e in timing_events])
+        o.timing_events = ctypes.cast(arr, ctypes.c_void_p)
+        o._keep = arr  # keep the array alive for the call
     return ctypes.pointer(o)
 
 
@@ -94,7 +100,7 @@ def to_device(batch, fmt: int = _lib.LOGAN_SEQ_2BIT, device=None) -> DeviceBatch
 
 def xdrop_batch(db: DeviceBatch, match: int, mismatch: int, gap: int, xdrop: int,
                 workspace: Workspace | None = None, out=None, cells=None, stats=None,
-                first_level: int | None = None, stream=None):
+                first_level: int | None = None, stream=None, timing_events=None):
     """Run the whole hot path on ``db``'s device, asynchronously on ``stream``
     (default: torch's current stream).  Returns ``(out int32[n,5], cells int64[n])``
     device tensors (cells holds uint64 bit patterns)."""
@@ -114,7 +120,7 @@ def xdrop_batch(db: DeviceBatch, match: int, mismatch: int, gap: int, xdrop: int
     st = lib.logan_xdrop_batch(
         db.pool.data_ptr(), db.fmt, db.pool_len, db.q_off.data_ptr(), db.q_len.data_ptr(),
         db.t_off.data_ptr(), db.t_len.data_ptr(), db.q_seed.data_ptr(), db.t_seed.data_ptr(),
-        n, db.k, sc, _opts(first_level), out.data_ptr(), cells.data_ptr(),
+        n, db.k, sc, _opts(first_level, timing_events), out.data_ptr(), cells.data_ptr(),
         stats.data_ptr() if stats is not None else None,
         workspace.ptr(), workspace.nbytes, stream.cuda_stream)
     _lib.check(st)
@@ -123,12 +129,13 @@ def xdrop_batch(db: DeviceBatch, match: int, mismatch: int, gap: int, xdrop: int
 
 def new_stats(device=None):
     torch = _require_cuda()
-    return torch.zeros(8, dtype=torch.int64, device=device or "cuda")
+    return torch.zeros(ctypes.sizeof(_lib.Stats) // 8, dtype=torch.int64, device=device or "cuda")
 
 
 def stats_dict(stats_tensor) -> dict:
     v = [int(x) for x in stats_tensor.cpu().tolist()]
-    return {"tasks_per_level": v[:6], "window_shifts": v[6], "cells_total": v[7]}
+    return {"tasks_started": v[0:6], "tasks_finished": v[6:12], "cells_per_level": v[12:18],
+            "window_shifts": v[18], "cells_total": v[19]}
 
 
 class HostArena:

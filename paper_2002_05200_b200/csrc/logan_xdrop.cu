@@ -145,7 +145,7 @@ __global__ void k_combine(const Params P, const TaskRes *tres, logan_result_t *o
          p += (int64_t)gridDim.x * blockDim.x) {
         const TaskRes L = tres[2 * p], R = tres[2 * p + 1];
         logan_result_t r;
-        if (L.flags & 1) {
+        if ((L.flags | R.flags) & 3) {  // invalid pair, or wide scratch too small (max_ext_len)
             r = {INT32_MIN, -1, -1, -1, -1};
             if (cells) cells[p] = 0;
         } else {
@@ -221,6 +221,11 @@ static int run_batch(const Params &P, const logan_options_t *opt, logan_result_t
     if (cudaMemsetAsync(ctr, 0, sizeof(uint32_t) * 32, s) != cudaSuccess) return LOGAN_ECUDA;
     if (stats && cudaMemsetAsync(stats, 0, sizeof(logan_stats_t), s) != cudaSuccess) return LOGAN_ECUDA;
 
+    cudaEvent_t const *ev = (opt && opt->timing_events) ? (cudaEvent_t const *)opt->timing_events : nullptr;
+    auto mark = [&](int stage, int which) -> bool {
+        return !ev || cudaEventRecord(ev[2 * stage + which], s) == cudaSuccess;
+    };
+    if (!mark(0, 0)) return LOGAN_ECUDA;
     const int64_t per_block = SETUP_THREADS;
     int grid = (int)((P.n_pairs + per_block - 1) / per_block);
     if (grid > sms * 8) grid = sms * 8;
@@ -232,6 +237,7 @@ static int run_batch(const Params &P, const logan_options_t *opt, logan_result_t
     if (grid2 < 1) grid2 = 1;
     k_scatter<<<grid2, SETUP_THREADS, 0, s>>>(L.ntask, tbucket, cursor_b, queue);
     if (cudaGetLastError() != cudaSuccess) return LOGAN_ECUDA;
+    if (!mark(0, 1)) return LOGAN_ECUDA;
 
     int first = (opt && opt->first_level > 0) ? opt->first_level - 1 : auto_first_level(P.xdrop);
     if (first < 0 || first > 5) return LOGAN_EINVAL;
@@ -249,6 +255,7 @@ static int run_batch(const Params &P, const logan_options_t *opt, logan_result_t
         io.level = lv;
         io.tres = tres;
         cudaError_t e;
+        if (!mark(1 + lv, 0)) return LOGAN_ECUDA;
         if (lv < 5) {
             e = launch_level<FMT>(lv, P, io, sms, s);
         } else {
@@ -256,6 +263,7 @@ static int run_batch(const Params &P, const logan_options_t *opt, logan_result_t
             e = cudaGetLastError();
         }
         if (e != cudaSuccess) return LOGAN_ECUDA;
+        if (!mark(1 + lv, 1)) return LOGAN_ECUDA;
         in_list = lists[out_sel];
         in_count = &ctr[8 + lv];
         out_sel ^= 1;
@@ -263,8 +271,10 @@ static int run_batch(const Params &P, const logan_options_t *opt, logan_result_t
     int grid3 = (int)((P.n_pairs + per_block - 1) / per_block);
     if (grid3 > sms * 8) grid3 = sms * 8;
     if (grid3 < 1) grid3 = 1;
+    if (!mark(7, 0)) return LOGAN_ECUDA;
     k_combine<FMT><<<grid3, SETUP_THREADS, 0, s>>>(P, tres, out, cells);
     if (cudaGetLastError() != cudaSuccess) return LOGAN_ECUDA;
+    if (!mark(7, 1)) return LOGAN_ECUDA;
     return LOGAN_OK;
 }
 

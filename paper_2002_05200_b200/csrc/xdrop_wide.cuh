@@ -45,6 +45,14 @@ __global__ void __launch_bounds__(WIDE_THREADS) k_wide(const Params P, const Lev
         if (task == NO_TASK) return;
         const TaskDesc td = task_desc(P, task);
         const int32_t m = td.a.len, n = td.b.len;
+        if ((int64_t)m + 2 > stride) {  // caller's max_ext_len bound was too small
+            if (tid == 0) {
+                TaskRes tr;
+                tr.best = 0; tr.i = 0; tr.j = 0; tr.flags = 2; tr.cells = 0;
+                io.tres[task] = tr;
+            }
+            continue;
+        }
 
         // per-antidiagonal bookkeeping (uniform across the block)
         int32_t vis_lo[3] = {0, 0, 0}, vis_hi[3] = {-1, -1, -1};
@@ -147,7 +155,9 @@ __global__ void __launch_bounds__(WIDE_THREADS) k_wide(const Params P, const Lev
             tr.cells = cells;
             io.tres[task] = tr;
             if (io.stats) {
-                atomicAdd((unsigned long long *)&io.stats->tasks_per_level[io.level], 1ull);
+                atomicAdd((unsigned long long *)&io.stats->tasks_started[io.level], 1ull);
+                atomicAdd((unsigned long long *)&io.stats->tasks_finished[io.level], 1ull);
+                atomicAdd((unsigned long long *)&io.stats->cells_per_level[io.level], (unsigned long long)cells);
                 atomicAdd((unsigned long long *)&io.stats->cells_total, (unsigned long long)cells);
             }
         }

@@ -437,9 +437,14 @@ __global__ void __launch_bounds__(128) k_window(const Params P, const LevelIO io
                     io.out_list[o] = task;
                 }
                 if (io.stats) {
-                    atomicAdd((unsigned long long *)&io.stats->tasks_per_level[io.level], 1ull);
+                    atomicAdd((unsigned long long *)&io.stats->tasks_started[io.level], 1ull);
                     atomicAdd((unsigned long long *)&io.stats->window_shifts, (unsigned long long)w.st.shifts);
-                    if (rc == 1) atomicAdd((unsigned long long *)&io.stats->cells_total, (unsigned long long)w.st.cells);
+                    if (rc == 1) {
+                        atomicAdd((unsigned long long *)&io.stats->tasks_finished[io.level], 1ull);
+                        atomicAdd((unsigned long long *)&io.stats->cells_per_level[io.level],
+                                  (unsigned long long)w.st.cells);
+                        atomicAdd((unsigned long long *)&io.stats->cells_total, (unsigned long long)w.st.cells);
+                    }
                 }
             }
             task = fetch();
