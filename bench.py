@@ -245,6 +245,9 @@ def main():
     ev = [[torch.cuda.Event(enable_timing=True) for _ in range(2 * nst)] for _ in range(args.steps)]
     e0 = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
     e1 = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
+    for e in [x for row in ev for x in row] + e0 + e1:
+        e.record(stream)  # torch creates the CUDA event lazily on its first record()
+    torch.cuda.synchronize()
     props = torch.cuda.get_device_properties(dev)
     uuid = getattr(props, "uuid", None)
     sampler = ClockSampler(f"GPU-{uuid}" if uuid is not None and not str(uuid).startswith("GPU-") else

@@ -41,7 +41,7 @@ extern "C" {
 
 /* Linear scoring scheme (eq. P:85, read with signed addends, c-amb-2).
  * Requirements: 0 < match <= 127, -127 <= mismatch < 0, -127 <= gap < 0,
- * 0 <= xdrop <= 2^20 (X >= (m+n)*127 disables pruning: "X = infinity"). */
+ * 0 <= xdrop <= 2^19 (X >= (m+n)*127 disables pruning: "X = infinity"). */
 typedef struct {
     int32_t match;
     int32_t mismatch;

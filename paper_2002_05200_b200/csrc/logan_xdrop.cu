@@ -35,8 +35,13 @@ __device__ __forceinline__ uint32_t cost_bucket(uint32_t c) {
 }
 
 // Workspace layout (each region 256-byte aligned).
+constexpr int NWIDTH = 5;  // register-window widths 32, 64, 128, 256, 1024
+static const int kWidth[NWIDTH] = {32, 64, 128, 256, 1024};
+
 struct Layout {
-    size_t tres, tbucket, queue, listA, listB, hist, cursor_b, counters, wide, total;
+    size_t tres, tbucket, queue, listA, listB, recsA, recsB, hist, cursor_b, counters, wide, total;
+    size_t pool[NWIDTH - 1];     // hand-over records written by width level w (w < 4)
+    uint32_t pool_cap[NWIDTH - 1];
     int64_t ntask, wide_stride;
 };
 
@@ -54,9 +59,21 @@ static Layout make_layout(int64_t n_pairs, int64_t max_ext_len) {
     L.queue = o;    o += align256(sizeof(uint32_t) * (size_t)nt);
     L.listA = o;    o += align256(sizeof(uint32_t) * (size_t)nt);
     L.listB = o;    o += align256(sizeof(uint32_t) * (size_t)nt);
+    L.recsA = o;    o += align256(sizeof(uint32_t) * (size_t)nt);
+    L.recsB = o;    o += align256(sizeof(uint32_t) * (size_t)nt);
+    for (int w = 0; w < NWIDTH - 1; ++w) {
+        // at most 128 MiB of records per level; tasks beyond that restart
+        const int64_t rec_bytes = (int64_t)sizeof(int32_t) * rec_ints(kWidth[w]);
+        int64_t cap = ((int64_t)128 << 20) / rec_bytes;
+        if (cap > nt) cap = nt;
+        L.pool_cap[w] = (uint32_t)cap;
+        L.pool[w] = o;
+        o += align256((size_t)(rec_bytes * cap));
+    }
     L.hist = o;     o += align256(sizeof(uint32_t) * NBUCKET);
     L.cursor_b = o; o += align256(sizeof(uint32_t) * NBUCKET);
-    // counters: [0] queue count, [1..NLEVEL] level cursors, [8..8+NLEVEL] out counts
+    // counters: [0] queue count, [1..NLEVEL] level cursors, [8..8+NLEVEL] out counts,
+    // [16..16+NWIDTH-1] record pool fill
     L.counters = o; o += align256(sizeof(uint32_t) * 32);
     L.wide_stride = max_ext_len + 2;
     L.wide = o;     o += align256(sizeof(int32_t) * 3 * (size_t)L.wide_stride * WIDE_CTAS);
@@ -167,28 +184,39 @@ __global__ void k_combine(const Params P, const TaskRes *tres, logan_result_t *o
 }
 
 // ---------------------------------------------------------------------------
-// Level table: window shapes (G lanes x R slots).
-template <int FMT>
-static cudaError_t launch_level(int level, const Params &P, const LevelIO &io, int sms, cudaStream_t s) {
+// Level table: register windows of W = 32, 64, 128, 256, 1024 diagonal slots.
+// Throughput shape: G = W/32 lanes x R = 32 slots (many tasks in flight).
+// Latency shape: one warp per task, R = W/32 slots per lane (few tasks left:
+// the step's critical path is short). Level 5 is the unbounded CTA path.
+template <int G, int R, int FMT>
+static cudaError_t launch_win(const Params &P, const LevelIO &io, int sms, cudaStream_t s) {
+    const size_t smem = 128 * sizeof(int32_t) * Window<G, R, FMT>::SB_STRIDE;
+    cudaError_t e = cudaFuncSetAttribute(k_window<G, R, FMT>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e != cudaSuccess) return e;
     int occ = 0;
-    cudaError_t e = cudaSuccess;
-#define LOGAN_LAUNCH_WIN(G_, R_)                                                                   \
-    do {                                                                                           \
-        e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_window<G_, R_, FMT>, 128, 0);    \
-        if (e != cudaSuccess) return e;                                                            \
-        if (occ < 1) occ = 1;                                                                      \
-        k_window<G_, R_, FMT><<<sms * occ, 128, 0, s>>>(P, io);                                    \
-    } while (0)
-    switch (level) {
-        case 0: LOGAN_LAUNCH_WIN(1, 32); break;
-        case 1: LOGAN_LAUNCH_WIN(2, 32); break;
-        case 2: LOGAN_LAUNCH_WIN(4, 32); break;
-        case 3: LOGAN_LAUNCH_WIN(8, 32); break;
-        case 4: LOGAN_LAUNCH_WIN(32, 32); break;
+    e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_window<G, R, FMT>, 128, smem);
+    if (e != cudaSuccess) return e;
+    if (occ < 1) occ = 1;
+    k_window<G, R, FMT><<<sms * occ, 128, smem, s>>>(P, io);
+    return cudaGetLastError();
+}
+
+template <int FMT>
+static cudaError_t launch_width(int wi, bool latency, const Params &P, const LevelIO &io, int sms,
+                                cudaStream_t s) {
+    switch (wi * 2 + (latency ? 1 : 0)) {
+        case 0: return launch_win<1, 32, FMT>(P, io, sms, s);
+        case 1: return launch_win<32, 1, FMT>(P, io, sms, s);
+        case 2: return launch_win<2, 32, FMT>(P, io, sms, s);
+        case 3: return launch_win<32, 2, FMT>(P, io, sms, s);
+        case 4: return launch_win<4, 32, FMT>(P, io, sms, s);
+        case 5: return launch_win<32, 4, FMT>(P, io, sms, s);
+        case 6: return launch_win<8, 32, FMT>(P, io, sms, s);
+        case 7: return launch_win<32, 8, FMT>(P, io, sms, s);
+        case 8:
+        case 9: return launch_win<32, 32, FMT>(P, io, sms, s);
         default: return cudaErrorInvalidValue;
     }
-#undef LOGAN_LAUNCH_WIN
-    return cudaGetLastError();
 }
 
 static int auto_first_level(int32_t xdrop) {
@@ -241,30 +269,66 @@ static int run_batch(const Params &P, const logan_options_t *opt, logan_result_t
 
     int first = (opt && opt->first_level > 0) ? opt->first_level - 1 : auto_first_level(P.xdrop);
     if (first < 0 || first > 5) return LOGAN_EINVAL;
+    uint32_t *recs[2] = {(uint32_t *)(ws + L.recsA), (uint32_t *)(ws + L.recsB)};
     const uint32_t *in_list = queue;
+    const uint32_t *in_recs = nullptr;
+    const int32_t *rec_in = nullptr;
+    int64_t rec_in_stride = 0;
     const uint32_t *in_count = &ctr[0];
     int out_sel = 0;
+    // below this many tasks a level runs in its latency shape (one warp per task)
+    const uint32_t latency_below = (uint32_t)sms * 16u;
     for (int lv = first; lv < NLEVEL; ++lv) {
-        LevelIO io;
+        LevelIO io{};
         io.list = in_list;
         io.count = in_count;
-        io.cursor = &ctr[1 + lv];
         io.out_list = lists[out_sel];
         io.out_count = &ctr[8 + lv];
         io.stats = stats;
         io.level = lv;
         io.tres = tres;
-        cudaError_t e;
+        io.in_recs = in_recs;
+        io.rec_in = rec_in;
+        io.rec_in_stride = rec_in_stride;
+        if (lv < NWIDTH - 1) {
+            io.out_recs = recs[out_sel];
+            io.rec_out = (int32_t *)(ws + L.pool[lv]);
+            io.rec_out_stride = rec_ints(kWidth[lv]);
+            io.rec_out_cap = L.pool_cap[lv];
+            io.rec_out_count = &ctr[16 + lv];
+        }
+        cudaError_t e = cudaSuccess;
         if (!mark(1 + lv, 0)) return LOGAN_ECUDA;
-        if (lv < 5) {
-            e = launch_level<FMT>(lv, P, io, sms, s);
+        if (lv < NWIDTH) {
+            if (lv == first) {
+                io.cursor = &ctr[1 + lv];
+                io.min_count = 0;
+                io.max_count = 0xffffffffu;
+                e = launch_width<FMT>(lv, false, P, io, sms, s);
+            } else {
+                io.cursor = &ctr[1 + lv];
+                io.min_count = 0;
+                io.max_count = latency_below;
+                e = launch_width<FMT>(lv, true, P, io, sms, s);
+                if (e == cudaSuccess) {
+                    io.min_count = latency_below;
+                    io.max_count = 0xffffffffu;
+                    e = launch_width<FMT>(lv, false, P, io, sms, s);
+                }
+            }
         } else {
+            io.cursor = &ctr[1 + lv];
+            io.min_count = 0;
+            io.max_count = 0xffffffffu;
             k_wide<FMT><<<WIDE_CTAS, WIDE_THREADS, 0, s>>>(P, io, wide, L.wide_stride);
             e = cudaGetLastError();
         }
         if (e != cudaSuccess) return LOGAN_ECUDA;
         if (!mark(1 + lv, 1)) return LOGAN_ECUDA;
         in_list = lists[out_sel];
+        in_recs = (lv < NWIDTH - 1) ? recs[out_sel] : nullptr;
+        rec_in = (lv < NWIDTH - 1) ? (const int32_t *)(ws + L.pool[lv]) : nullptr;
+        rec_in_stride = (lv < NWIDTH - 1) ? rec_ints(kWidth[lv]) : 0;
         in_count = &ctr[8 + lv];
         out_sel ^= 1;
     }
@@ -309,7 +373,7 @@ static int check_args(const uint8_t *seq_pool, int32_t seq_fmt, int64_t pool_len
     if (seq_fmt != LOGAN_SEQ_U8 && seq_fmt != LOGAN_SEQ_2BIT) return LOGAN_EINVAL;
     if (k < 0 || pool_len < 0) return LOGAN_EINVAL;
     if (sc.match <= 0 || sc.match > 127 || sc.mismatch >= 0 || sc.mismatch < -127 || sc.gap >= 0 ||
-        sc.gap < -127 || sc.xdrop < 0 || sc.xdrop > (1 << 20))
+        sc.gap < -127 || sc.xdrop < 0 || sc.xdrop > (1 << 19))
         return LOGAN_EINVAL;
     if (opt && (opt->first_level < 0 || opt->first_level > 6)) return LOGAN_EINVAL;
     if (n_pairs == 0) return LOGAN_OK;

@@ -48,6 +48,17 @@ struct LevelIO {
     logan_stats_t *stats;
     int32_t level;
     TaskRes *tres;
+    // launch-shape dispatch: run only if min_count <= *count < max_count
+    uint32_t min_count, max_count;
+    // hand-over records (NULL = restart tasks from scratch)
+    const uint32_t *in_recs;     // per list entry: record index or NO_REC
+    const int32_t *rec_in;
+    int64_t rec_in_stride;       // ints per record
+    uint32_t *out_recs;
+    int32_t *rec_out;
+    int64_t rec_out_stride;
+    uint32_t rec_out_cap;
+    uint32_t *rec_out_count;
 };
 
 constexpr uint32_t NO_TASK = 0xffffffffu;
@@ -132,49 +143,50 @@ __device__ __forceinline__ uint32_t seq_at(const Params &P, const SeqRef &s, int
     return pool_base<FMT>(P, s.base + (int64_t)s.dir * (idx - 1));
 }
 
-// A forward stream over one extension sequence with a one-word prefetch in
-// the direction of travel: consuming index i+1 after i costs a shift and, once
-// per word, a load whose latency is hidden until the following word boundary.
+// A sequential reader over one extension sequence: next() returns the code of
+// index `idx` (a sentinel outside 1..len) and moves to idx + 1. The word holding
+// the next base and the word after it are kept in registers; crossing a word
+// boundary shifts them down and issues the load of the following word, whose
+// latency is hidden until the next boundary (16 bases later for 2-bit).
+// seek() repositions the reader anywhere (blocking loads; rare: task start
+// and window shifts).
+template <int FMT>
 struct Stream {
+    using F = PoolFmt<FMT>;
+    static constexpr int CPW = 1 << F::LOG_CPW;
     SeqRef s;
-    int64_t w0;    // word index held in `cur`
-    uint32_t cur;  // word w0
-    uint32_t nxt;  // word w0 + dir (prefetched)
-};
+    int64_t wi;    // word index of `cur` (position of index max(idx,1))
+    uint32_t cur;  // word holding the base at index max(idx, 1)
+    uint32_t nxt;  // the next word in the direction of travel
+    int32_t idx;   // extension index returned by the next next()
+    int32_t sh;    // bit offset of that base inside cur
 
-template <int FMT>
-__device__ __forceinline__ void stream_seek(const Params &P, Stream &st, int32_t idx) {
-    using F = PoolFmt<FMT>;
-    int32_t c = idx < 1 ? 1 : (idx > st.s.len ? st.s.len : idx);
-    if (st.s.len <= 0) c = 1;
-    const int64_t pos = st.s.base + (int64_t)st.s.dir * (c - 1);
-    st.w0 = pos >> F::LOG_CPW;
-    st.cur = pool_word(P, st.w0);
-    st.nxt = pool_word(P, st.w0 + st.s.dir);
-}
-
-template <int FMT>
-__device__ __forceinline__ uint32_t stream_get(const Params &P, Stream &st, int32_t idx, uint32_t sent) {
-    using F = PoolFmt<FMT>;
-    if (idx < 1 || idx > st.s.len) return sent;
-    const int64_t pos = st.s.base + (int64_t)st.s.dir * (idx - 1);
-    const int64_t wi = pos >> F::LOG_CPW;
-    uint32_t w;
-    if (wi == st.w0) {
-        w = st.cur;
-    } else if (wi == st.w0 + st.s.dir) {
-        st.w0 = wi;
-        st.cur = st.nxt;
-        st.nxt = pool_word(P, wi + st.s.dir);  // prefetch; consumed a word later
-        w = st.cur;
-    } else {
-        st.w0 = wi;
-        st.cur = pool_word(P, wi);
-        st.nxt = pool_word(P, wi + st.s.dir);
-        w = st.cur;
+    __device__ __forceinline__ void seek(const Params &P, int32_t i) {
+        idx = i;
+        const int32_t c = (i < 1 || s.len <= 0) ? 1 : (i > s.len ? s.len : i);
+        const int64_t pos = s.base + (int64_t)s.dir * (c - 1);
+        wi = pos >> F::LOG_CPW;
+        sh = F::BITS * (int32_t)(pos & (CPW - 1));
+        cur = pool_word(P, wi);
+        nxt = pool_word(P, wi + s.dir);
     }
-    return (w >> (F::BITS * (uint32_t)(pos & ((1 << F::LOG_CPW) - 1)))) & F::MASK;
-}
+
+    __device__ __forceinline__ uint32_t next(const Params &P, uint32_t sent) {
+        const int32_t i = idx++;
+        if (i < 1 || i > s.len) return sent;  // before the start: parked at index 1
+        const uint32_t c = (cur >> sh) & F::MASK;
+        if (i < s.len) {  // advance to index i + 1
+            sh += s.dir * F::BITS;
+            if ((uint32_t)sh >= 32u) {  // crossed a word boundary
+                sh -= s.dir * 32;
+                wi += s.dir;
+                cur = nxt;
+                nxt = pool_word(P, wi + s.dir);  // prefetch
+            }
+        }
+        return c;
+    }
+};
 
 __device__ __forceinline__ int32_t ceil_half(int32_t d) { return (d + 1) >> 1; }
 __device__ __forceinline__ int32_t floor_half(int32_t d) { return d >> 1; }

@@ -34,6 +34,7 @@ __global__ void __launch_bounds__(WIDE_THREADS) k_wide(const Params P, const Lev
                      scratch + (int64_t)blockIdx.x * 3 * stride + stride,
                      scratch + (int64_t)blockIdx.x * 3 * stride + 2 * stride};
     const uint32_t count = *io.count;
+    if (count < io.min_count || count >= io.max_count) return;
     for (;;) {
         if (tid == 0) {
             const uint32_t pos = atomicAdd(io.cursor, 1u);
@@ -156,7 +157,7 @@ __global__ void __launch_bounds__(WIDE_THREADS) k_wide(const Params P, const Lev
             io.tres[task] = tr;
             if (io.stats) {
                 atomicAdd((unsigned long long *)&io.stats->tasks_started[io.level], 1ull);
-                atomicAdd((unsigned long long *)&io.stats->tasks_finished[io.level], 1ull);
+                atomicAdd((unsigned long long *)&io.stats->tasks_finished[io.level], 1ull);  // restarted here
                 atomicAdd((unsigned long long *)&io.stats->cells_per_level[io.level], (unsigned long long)cells);
                 atomicAdd((unsigned long long *)&io.stats->cells_total, (unsigned long long)cells);
             }

@@ -24,18 +24,18 @@
 //    u = S - T_d, live <=> u >= 0. The per-step rebase folds into the two
 //    scoring constants (gap' = gap - (T_d - T_{d-1}), s' = s - (T_d - T_{d-2}))
 //    so the cell is three DPX VIADDMNMX plus one VIMNMX.U32:
-//        t1 = max(left + gap', DEAD); t2 = max(up + gap', t1);
-//        u  = max(diag + s', t2);     u  = min_u32(u, DEAD)
-//    which maps every negative u to exactly DEAD = -2^21 (an exact, absorbing
-//    kill: a dead value can never climb back within 2^21 / match steps, far
-//    more than any task's antidiagonal count at the ABI's limits).
+//        u = max(max(up, left, DEAD - gap') + gap', diag + s');  u = min_u32(u, DEAD)
+//    (VIMNMX3, an add, VIADDMNMX, VIMNMX.U32), which maps every negative u to
+//    exactly DEAD = -2^20 (an exact, absorbing kill: a dead value can never
+//    climb back within 2^20 / match steps, far more than any task's
+//    antidiagonal count at the ABI's limits).
 //  * Bases sit in registers, 4-bit fields (2-bit pool) or 16-bit fields (u8
 //    pool), one per slot; positions past an extension's end hold sentinels
 //    that match nothing, so cells outside the matrix (i > m or j > n) can only
 //    hold values below an earlier best and are excluded from the band
 //    bookkeeping by a per-lane validity mask -- no per-cell masking.
 //  * Per antidiagonal the max and its slot come from one packed key
-//    (u << 10 | 1023 - slot) reduced with VIMNMX3 inside the lane and SHFL
+//    (u * 1027 + 1023 - slot, an IMAD) reduced with VIMNMX3 inside the lane and SHFL
 //    butterflies across the G lanes; the live extremes from a funnel-shifted
 //    sign mask + FLO. Ties go to the smallest slot = smallest i (c-amb-9).
 //  * The window re-centres by one slot when the band touches an edge; if the
@@ -46,8 +46,13 @@
 
 namespace logan {
 
-constexpr int32_t DEAD = -(1 << 21);
-constexpr uint32_t DEADU = 0xFFE00000u;  // (uint32_t)DEAD
+constexpr int32_t DEAD = -(1 << 20);
+constexpr uint32_t DEADU = 0xFFF00000u;  // (uint32_t)DEAD
+// Argmax key of a cell: u * KEYMUL + (1023 - slot). KEYMUL > 1023 keeps the
+// order (value, then smallest slot); it is not a power of two so the key is
+// one IMAD on the FMA pipe (the ALU pipe is the kernel's bottleneck).
+// |DEAD| * KEYMUL < 2^31 and (X + 2*127) * KEYMUL < 2^31 for X <= 2^19.
+constexpr int32_t KEYMUL = 1027;
 
 template <int FMT> struct RegFmt;
 template <> struct RegFmt<LOGAN_SEQ_2BIT> {
@@ -60,11 +65,13 @@ template <> struct RegFmt<LOGAN_SEQ_U8> {
 };
 
 // Group-uniform state of one task (replicated in each lane of the group).
+template <int FMT>
 struct WinState {
+    // sa feeds the top slot (read by lane G-1; sa.idx = S0 + W + ceil(d/2)),
+    // sb feeds the bottom slot (read by lane 0; sb.idx = floor(d/2) - S0 + 1)
+    Stream<FMT> sa, sb;
     uint32_t task;
     int32_t m, n;
-    Stream sa, sb;         // A stream (used by the top lane), B stream (lane 0)
-    int32_t a_next, b_next;
     int32_t d;             // last antidiagonal computed
     int32_t S0;            // slot of the window's first register
     int32_t best, arg_i, arg_j;
@@ -72,8 +79,14 @@ struct WinState {
     int32_t sF1, sL1, sF2, sL2;  // live slot extremes of d and d-1
     bool h1, h2;           // d and d-1 hold a (valid) live cell
     uint64_t cells;
+    uint64_t cells_entry;  // cells already counted when the task entered this level
     uint32_t shifts;
 };
+
+// Hand-over record between levels: REC_HDR ints of scalars, then E[W], O[W].
+constexpr int REC_HDR = 32;
+__host__ __device__ constexpr int rec_ints(int W) { return REC_HDR + 2 * W; }
+constexpr uint32_t NO_REC = 0xffffffffu;
 
 template <int G>
 __device__ __forceinline__ int32_t grp_max(int32_t v, unsigned gmask) {
@@ -92,33 +105,62 @@ template <int G, int R, int FMT>
 struct Window {
     using RF = RegFmt<FMT>;
     static constexpr int CB = RF::CB;
-    static constexpr int FPW = 32 / CB;     // fields per word
-    static constexpr int NW = R / FPW;      // words per lane per sequence
+    static constexpr int FPW = 32 / CB;             // fields per word
+    static constexpr int NW = (R + FPW - 1) / FPW;  // words per lane per sequence
+    static constexpr int RL = R - (NW - 1) * FPW;   // fields in the last word
     static constexpr int W = G * R;
     static constexpr uint32_t FM = (1u << CB) - 1u;
-    static_assert(R % FPW == 0 && R <= 32 && W <= 1024, "window shape");
+    static_assert(R >= 1 && R <= 32 && W <= 1024 && (G & (G - 1)) == 0, "window shape");
 
     int32_t E[R], O[R];
     uint32_t Aw[NW], Bw[NW];
-    WinState st;
+    WinState<FMT> st;
     int gl;            // lane within group
     unsigned gmask;
+
+    // One cell (eq. P:85 + the drop rule P:89) on threshold-relative values:
+    //   u = max(max(up, left, fg) + gap', diag + s'), then the exact kill
+    //   min_u32(u, DEAD): every negative u becomes DEAD, live values stay.
+    // VIMNMX3 + VIADDMNMX + VIMNMX.U32 on the ALU pipe, diag + s' an add.
+    __device__ __forceinline__ static int32_t cell(int32_t up, int32_t left, int32_t diag, bool mis,
+                                                   int32_t gp, int32_t fg, int32_t sma, int32_t smi) {
+        const int32_t t0 = __vimax3_s32(up, left, fg);
+        const int32_t dps = diag + (mis ? smi : sma);
+        const int32_t u = __viaddmax_s32(t0, gp, dps);
+        return (int32_t)min((uint32_t)u, DEADU);
+    }
+
+    // per-thread shared-memory slice used only by the (rare) window shifts
+    static constexpr int SB_STRIDE = 2 * R + 1;  // odd stride: conflict-free
+    int32_t *sbase;
+    __device__ __forceinline__ volatile int32_t *sbuf() const { return sbase; }
+    __device__ __forceinline__ void spill(const int32_t (&e)[R], const int32_t (&o)[R]) const {
+        volatile int32_t *b = sbase;
+#pragma unroll
+        for (int r = 0; r < R; ++r) { b[r] = e[r]; b[R + r] = o[r]; }
+    }
 
     // ---- field helpers ------------------------------------------------------
     __device__ __forceinline__ uint32_t field(const uint32_t (&w)[NW], int r) const {
         return (w[r / FPW] >> (CB * (r % FPW))) & FM;
     }
-    // fields r <- r+1, new value into the top field
+    // the top field (slot R-1) of a lane's word array
+    __device__ __forceinline__ static uint32_t top_field(const uint32_t (&w)[NW]) {
+        return (w[NW - 1] >> (CB * (RL - 1))) & FM;
+    }
+    // fields r <- r+1, new value into the top field (bits above it stay zero)
     __device__ __forceinline__ static void shift_down(uint32_t (&w)[NW], uint32_t in) {
 #pragma unroll
         for (int q = 0; q < NW - 1; ++q) w[q] = __funnelshift_r(w[q], w[q + 1], CB);
-        w[NW - 1] = __funnelshift_r(w[NW - 1], in, CB);
+        if (RL == FPW) w[NW - 1] = __funnelshift_r(w[NW - 1], in, CB);
+        else w[NW - 1] = (w[NW - 1] >> CB) | (in << (CB * (RL - 1)));
     }
     // fields r <- r-1, new value into field 0
     __device__ __forceinline__ static void shift_up(uint32_t (&w)[NW], uint32_t in) {
 #pragma unroll
         for (int q = NW - 1; q > 0; --q) w[q] = __funnelshift_l(w[q - 1], w[q], CB);
-        w[0] = (w[0] << CB) | in;
+        w[0] = (NW == 1 ? (w[0] << CB) : (w[0] << CB)) | in;
+        if (RL < FPW) w[NW - 1] &= (1u << (CB * RL)) - 1u;
     }
 
     // ---- task start -----------------------------------------------------------
@@ -147,29 +189,83 @@ struct Window {
             E[r] = (s0 + r == 0) ? P.xdrop : DEAD;
             O[r] = DEAD;
         }
-        // bases at d = 0: slot s holds a_s and b_{-s}
-        Stream ta{td.a, 0, 0, 0}, tb{td.b, 0, 0, 0};
-        stream_seek<FMT>(P, ta, s0);
-        stream_seek<FMT>(P, tb, -(s0 + R - 1));
+        st.sa.s = td.a;
+        st.sb.s = td.b;
+        st.cells_entry = 0;
+        load_bases(P);
+    }
+
+    // bases of the window at antidiagonal st.d: slot s holds a_{s + ceil(d/2)}
+    // and b_{floor(d/2) - s}; positions the top / bottom streams (rolled loops:
+    // runs once per task start or resume)
+    __device__ __forceinline__ void load_bases(const Params &P) {
+        const int32_t s0 = st.S0 + gl * R;
+        const int32_t ch = ceil_half(st.d), fh = floor_half(st.d);
 #pragma unroll
         for (int q = 0; q < NW; ++q) { Aw[q] = 0; Bw[q] = 0; }
+        st.sa.seek(P, s0 + ch);
+#pragma unroll 1
+        for (int r = 0; r < R; ++r) shift_down(Aw, st.sa.next(P, RF::SA));       // field r = a_{s0+r+ch}
+        st.sb.seek(P, fh - (s0 + R - 1));
+#pragma unroll 1
+        for (int r = R - 1; r >= 0; --r) shift_up(Bw, st.sb.next(P, RF::SB));   // field r = b_{fh-(s0+r)}
+        if (gl == G - 1) st.sa.seek(P, st.S0 + W + ch);  // sa.idx = S0 + W + ceil(d/2)
+        if (gl == 0) st.sb.seek(P, fh - st.S0 + 1);      // sb.idx = floor(d/2) - S0 + 1
+    }
+
+    // ---- exact hand-over between levels ---------------------------------------
+    // A task whose band outgrows this window is written out after antidiagonal
+    // d (values of d and d-1 plus every scalar) and the next, wider level
+    // continues it from d + 1: cells outside the old window are dead (the band
+    // invariant), so the continuation is exact.
+    __device__ __forceinline__ void save(int32_t *rec) const {
 #pragma unroll
         for (int r = 0; r < R; ++r) {
-            const uint32_t a = stream_get<FMT>(P, ta, s0 + r, RF::SA);
-            Aw[r / FPW] |= a << (CB * (r % FPW));
+            rec[REC_HDR + gl * R + r] = E[r];
+            rec[REC_HDR + W + gl * R + r] = O[r];
         }
+        if (gl == 0) {
+            rec[0] = (int32_t)st.task; rec[1] = st.d; rec[2] = st.S0; rec[3] = st.best;
+            rec[4] = st.arg_i; rec[5] = st.arg_j; rec[6] = st.Tn; rec[7] = st.Td; rec[8] = st.Tp;
+            rec[9] = st.sF1; rec[10] = st.sL1; rec[11] = st.sF2; rec[12] = st.sL2;
+            rec[13] = (st.h1 ? 1 : 0) | (st.h2 ? 2 : 0);
+            rec[14] = (int32_t)st.shifts; rec[15] = W;
+            rec[16] = (int32_t)(uint32_t)st.cells; rec[17] = (int32_t)(uint32_t)(st.cells >> 32);
+        }
+    }
+
+    __device__ __forceinline__ void resume(const Params &P, const int32_t *rec) {
+        st.task = (uint32_t)rec[0];
+        const TaskDesc td = task_desc(P, st.task);
+        st.m = td.a.len;
+        st.n = td.b.len;
+        st.sa.s = td.a;
+        st.sb.s = td.b;
+        st.d = rec[1];
+        const int32_t S0src = rec[2];
+        st.best = rec[3]; st.arg_i = rec[4]; st.arg_j = rec[5];
+        st.Tn = rec[6]; st.Td = rec[7]; st.Tp = rec[8];
+        st.sF1 = rec[9]; st.sL1 = rec[10]; st.sF2 = rec[11]; st.sL2 = rec[12];
+        st.h1 = rec[13] & 1; st.h2 = (rec[13] >> 1) & 1;
+        st.shifts = (uint32_t)rec[14];
+        const int32_t Wsrc = rec[15];
+        st.cells = (uint64_t)(uint32_t)rec[16] | ((uint64_t)(uint32_t)rec[17] << 32);
+        st.cells_entry = st.cells;
+        // centre the wider window on the live band of d and d-1
+        int32_t Fm = INT32_MAX, Lm = INT32_MIN;
+        if (st.h1) { Fm = st.sF1; Lm = st.sL1; }
+        if (st.h2) { Fm = min(Fm, st.sF2); Lm = max(Lm, st.sL2); }
+        if (Fm > Lm) { Fm = S0src; Lm = S0src + Wsrc - 1; }
+        st.S0 = ((Fm + Lm) >> 1) - W / 2;
+        const int32_t s0 = st.S0 + gl * R;
 #pragma unroll
-        for (int r = R - 1; r >= 0; --r) {
-            const uint32_t b = stream_get<FMT>(P, tb, -(s0 + r), RF::SB);
-            Bw[r / FPW] |= b << (CB * (r % FPW));
+        for (int r = 0; r < R; ++r) {
+            const int32_t q = s0 + r - S0src;
+            const bool in = q >= 0 && q < Wsrc;
+            E[r] = in ? rec[REC_HDR + q] : DEAD;
+            O[r] = in ? rec[REC_HDR + Wsrc + q] : DEAD;
         }
-        // streams: A feeds the top slot, B the bottom slot
-        st.a_next = st.S0 + W;      // = S0 + W + ceil(d/2) at d = 0
-        st.b_next = 1 - st.S0;      // = floor(d/2) - S0 + 1 at d = 0
-        st.sa = {td.a, 0, 0, 0};
-        st.sb = {td.b, 0, 0, 0};
-        if (gl == G - 1) stream_seek<FMT>(P, st.sa, st.a_next);
-        if (gl == 0) stream_seek<FMT>(P, st.sb, st.b_next);
+        load_bases(P);
     }
 
     // ---- one antidiagonal d = st.d + 1 of parity PAR ---------------------------
@@ -203,14 +299,12 @@ struct Window {
         if (PAR == 1) {  // i advances: A fields move down one slot
             uint32_t in = 0;
             if (G > 1) in = __shfl_down_sync(gmask, Aw[0], 1, G) & FM;
-            if (gl == G - 1) in = stream_get<FMT>(P, st.sa, st.a_next, RF::SA);
-            ++st.a_next;
+            if (gl == G - 1) in = st.sa.next(P, RF::SA);
             shift_down(Aw, in);
         } else {         // j advances: B fields move up one slot
             uint32_t in = 0;
-            if (G > 1) in = __shfl_up_sync(gmask, Bw[NW - 1], 1, G) >> (32 - CB);
-            if (gl == 0) in = stream_get<FMT>(P, st.sb, st.b_next, RF::SB);
-            ++st.b_next;
+            if (G > 1) in = __shfl_up_sync(gmask, top_field(Bw), 1, G);
+            if (gl == 0) in = st.sb.next(P, RF::SB);
             shift_up(Bw, in);
         }
 
@@ -219,6 +313,7 @@ struct Window {
         const int32_t gp = P.gap - (Tc - st.Td);
         const int32_t sma = P.match - (Tc - st.Tp);
         const int32_t smi = P.mismatch - (Tc - st.Tp);
+        const int32_t fg = DEAD - gp;  // max(up, left, fg) + gp >= DEAD: the floor
 
         uint32_t X[NW];
 #pragma unroll
@@ -237,15 +332,8 @@ struct Window {
 #pragma unroll
             for (int r = 0; r < R; ++r) {
                 const int32_t up = (r < R - 1) ? E[r + 1] : nb;
-                const int32_t left = E[r];
-                const int32_t diag = O[r];
                 const bool mis = ((X[r / FPW] >> (CB * (r % FPW))) & FM) != 0;
-                const int32_t s = mis ? smi : sma;
-                int32_t t = __viaddmax_s32(left, gp, DEAD);
-                t = __viaddmax_s32(up, gp, t);
-                t = __viaddmax_s32(diag, s, t);
-                t = (int32_t)min((uint32_t)t, DEADU);
-                O[r] = t;
+                O[r] = cell(up, E[r], O[r], mis, gp, fg, sma, smi);
             }
         } else {
             int32_t nb = DEAD;  // O[-1] of this lane = O[R-1] of the previous lane
@@ -255,25 +343,17 @@ struct Window {
             }
 #pragma unroll
             for (int r = 0; r < R; ++r) {
-                const int32_t up = O[r];
                 const int32_t left = (r > 0) ? O[r - 1] : nb;
-                const int32_t diag = E[r];
                 const bool mis = ((X[r / FPW] >> (CB * (r % FPW))) & FM) != 0;
-                const int32_t s = mis ? smi : sma;
-                int32_t t = __viaddmax_s32(left, gp, DEAD);
-                t = __viaddmax_s32(up, gp, t);
-                t = __viaddmax_s32(diag, s, t);
-                t = (int32_t)min((uint32_t)t, DEADU);
-                E[r] = t;
+                E[r] = cell(O[r], left, E[r], mis, gp, fg, sma, smi);
             }
         }
-        // keys (u << 10) + 1023 - r (dead u = -2^21 gives -2^31 + 1023 - r: no
-        // wrap) and sign chains over the new antidiagonal
+        // keys u * KEYMUL + 1023 - r and sign chains over the new antidiagonal
 #pragma unroll
         for (int r = R - 1; r >= 0; --r) {
             const int32_t u = PAR ? O[r] : E[r];
             const int c = r / RQ;
-            kq[c] = max(kq[c], (int32_t)(((uint32_t)u << 10) + (uint32_t)(1023 - r)));
+            kq[c] = max(kq[c], u * KEYMUL + (1023 - r));
             dq[c] = __funnelshift_l((uint32_t)u, dq[c], 1);  // appends sign(u): bit (r - c*RQ)
         }
         int32_t kmax = max(max(kq[0], kq[1]), max(kq[2], kq[3]));
@@ -291,7 +371,7 @@ struct Window {
         const uint32_t live = ~dead & vmask;
         int32_t lf = live ? gl * R + __ffs(live) - 1 : INT32_MAX;
         int32_t ll = live ? gl * R + 31 - __clz(live) : INT32_MIN;
-        kmax = kmax - gl * R;  // key = u*1024 + 1023 - (gl*R + r), never wraps for W <= 1024
+        kmax = kmax - gl * R;  // key = u*KEYMUL + 1023 - (gl*R + r)
         if (G > 1) {
             kmax = grp_max<G>(kmax, gmask);
             lf = grp_min<G>(lf, gmask);
@@ -301,10 +381,11 @@ struct Window {
 
         // (6) best after the complete antidiagonal; argmax on strict increase
         if (kmax >= 0) {
-            const int32_t V = (kmax >> 10) + Tc;
+            const int32_t ku = kmax / KEYMUL;
+            const int32_t V = ku + Tc;
             if (V > st.best) {
                 st.best = V;
-                const int32_t slot = st.S0 + (1023 - (kmax & 1023));
+                const int32_t slot = st.S0 + (1023 - (kmax - ku * KEYMUL));
                 st.arg_i = slot + ch;
                 st.arg_j = d - st.arg_i;
             }
@@ -353,17 +434,20 @@ struct Window {
         if (gl == G - 1) {
             eIn = DEAD;
             oIn = DEAD;
-            aIn = stream_get<FMT>(P, st.sa, st.a_next, RF::SA);  // a_{S1 + W - 1 + ceil(d/2)}
+            aIn = st.sa.next(P, RF::SA);  // a_{S1 + W - 1 + ceil(d/2)}
             bIn = seq_at<FMT>(P, st.sb.s, floor_half(d) - S1 - (W - 1), RF::SB);
         }
+        if (gl == 0) st.sb.seek(P, st.sb.idx - 1);  // b stream steps back one base
+        // rotate E/O through this thread's shared-memory slice: the reloads land in
+        // the registers the arrays already occupy, so the common (no-shift) path
+        // carries no register copies
+        spill(E, O);
 #pragma unroll
-        for (int r = 0; r < R - 1; ++r) { E[r] = E[r + 1]; O[r] = O[r + 1]; }
+        for (int r = 0; r < R - 1; ++r) { E[r] = sbuf()[r + 1]; O[r] = sbuf()[R + r + 1]; }
         E[R - 1] = eIn;
         O[R - 1] = oIn;
         shift_down(Aw, aIn);
         shift_down(Bw, bIn);
-        ++st.a_next;
-        --st.b_next;
         st.S0 = S1;
         ++st.shifts;
     }
@@ -375,54 +459,74 @@ struct Window {
         if (G > 1) {
             eIn = __shfl_up_sync(gmask, E[R - 1], 1, G);
             oIn = __shfl_up_sync(gmask, O[R - 1], 1, G);
-            aIn = __shfl_up_sync(gmask, Aw[NW - 1], 1, G) >> (32 - CB);
-            bIn = __shfl_up_sync(gmask, Bw[NW - 1], 1, G) >> (32 - CB);
+            aIn = __shfl_up_sync(gmask, top_field(Aw), 1, G);
+            bIn = __shfl_up_sync(gmask, top_field(Bw), 1, G);
         }
         const int32_t S1 = st.S0 - 1;
         if (gl == 0) {
             eIn = DEAD;
             oIn = DEAD;
             aIn = seq_at<FMT>(P, st.sa.s, S1 + ceil_half(d), RF::SA);
-            bIn = stream_get<FMT>(P, st.sb, st.b_next, RF::SB);  // b_{floor(d/2) - S1}
+            bIn = st.sb.next(P, RF::SB);  // b_{floor(d/2) - S1}
         }
+        if (gl == G - 1) st.sa.seek(P, st.sa.idx - 1);  // a stream steps back one base
+        spill(E, O);
 #pragma unroll
-        for (int r = R - 1; r > 0; --r) { E[r] = E[r - 1]; O[r] = O[r - 1]; }
+        for (int r = 1; r < R; ++r) { E[r] = sbuf()[r - 1]; O[r] = sbuf()[R + r - 1]; }
         E[0] = eIn;
         O[0] = oIn;
         shift_up(Aw, aIn);
         shift_up(Bw, bIn);
-        --st.a_next;
-        ++st.b_next;
         st.S0 = S1;
         ++st.shifts;
     }
 };
 
 // Persistent kernel: each group of G lanes pulls tasks from the level's list.
+// A level may exist in two shapes (throughput: G small, R = 32; latency: one
+// warp per task); the launch whose [min_count, max_count) holds the list length
+// runs, the other exits at once (no host synchronisation).
 template <int G, int R, int FMT>
 __global__ void __launch_bounds__(128) k_window(const Params P, const LevelIO io) {
+    const uint32_t count = *io.count;
+    if (count < io.min_count || count >= io.max_count) return;
     Window<G, R, FMT> w;
+    extern __shared__ int32_t win_smem[];
+    w.sbase = win_smem + threadIdx.x * Window<G, R, FMT>::SB_STRIDE;
     const int lane = threadIdx.x & 31;
     w.gl = lane % G;
     w.gmask = (G == 32) ? 0xffffffffu : (((1u << G) - 1u) << (lane - w.gl));
-    const uint32_t count = *io.count;
+    const int leader = lane - w.gl;
 
-    auto fetch = [&]() -> uint32_t {
-        uint32_t t = NO_TASK;
-        if (w.gl == 0) {
-            const uint32_t pos = atomicAdd(io.cursor, 1u);
-            if (pos < count) t = io.list[pos];
-        }
-        if (G > 1) t = __shfl_sync(w.gmask, t, lane - w.gl);
-        return t;
+    // take the next list entry; start or resume it
+    auto next_task = [&]() -> bool {
+        uint32_t pos = 0xffffffffu;
+        if (w.gl == 0) pos = atomicAdd(io.cursor, 1u);
+        if (G > 1) pos = __shfl_sync(w.gmask, pos, leader);
+        if (pos >= count) return false;
+        const uint32_t task = io.list[pos];
+        const uint32_t rec = io.in_recs ? io.in_recs[pos] : NO_REC;
+        if (rec != NO_REC) w.resume(P, io.rec_in + (size_t)rec * io.rec_in_stride);
+        else w.init(P, task);
+        if (io.stats && w.gl == 0)
+            atomicAdd((unsigned long long *)&io.stats->tasks_started[io.level], 1ull);
+        return true;
     };
 
-    uint32_t task = fetch();
-    if (task != NO_TASK) w.init(P, task);
-    while (task != NO_TASK) {
+    bool active = next_task();
+    while (active) {
         int rc = w.template step<1>(P);
         if (rc == 0) rc = w.template step<0>(P);
         if (rc != 0) {
+            uint32_t rec = NO_REC;
+            if (rc == 2 && io.rec_out) {  // hand the exact state to the next level
+                if (w.gl == 0) {
+                    rec = atomicAdd(io.rec_out_count, 1u);
+                    if (rec >= io.rec_out_cap) rec = NO_REC;  // pool full: the next level restarts it
+                }
+                if (G > 1) rec = __shfl_sync(w.gmask, rec, leader);
+                if (rec != NO_REC) w.save(io.rec_out + (size_t)rec * io.rec_out_stride);
+            }
             if (w.gl == 0) {
                 if (rc == 1) {
                     TaskRes tr;
@@ -431,24 +535,25 @@ __global__ void __launch_bounds__(128) k_window(const Params P, const LevelIO io
                     tr.j = w.st.arg_j;
                     tr.flags = 0;
                     tr.cells = w.st.cells;
-                    io.tres[task] = tr;
+                    io.tres[w.st.task] = tr;
                 } else {
                     const uint32_t o = atomicAdd(io.out_count, 1u);
-                    io.out_list[o] = task;
+                    io.out_list[o] = w.st.task;
+                    if (io.out_recs) io.out_recs[o] = rec;
                 }
                 if (io.stats) {
-                    atomicAdd((unsigned long long *)&io.stats->tasks_started[io.level], 1ull);
                     atomicAdd((unsigned long long *)&io.stats->window_shifts, (unsigned long long)w.st.shifts);
-                    if (rc == 1) {
+                    if (rc == 1)
                         atomicAdd((unsigned long long *)&io.stats->tasks_finished[io.level], 1ull);
+                    if (rc == 1 || rec != NO_REC) {
                         atomicAdd((unsigned long long *)&io.stats->cells_per_level[io.level],
-                                  (unsigned long long)w.st.cells);
-                        atomicAdd((unsigned long long *)&io.stats->cells_total, (unsigned long long)w.st.cells);
+                                  (unsigned long long)(w.st.cells - w.st.cells_entry));
                     }
+                    if (rc == 1) atomicAdd((unsigned long long *)&io.stats->cells_total, (unsigned long long)w.st.cells);
                 }
             }
-            task = fetch();
-            if (task != NO_TASK) w.init(P, task);
+            if (rc == 2) w.st.shifts = 0;
+            active = next_task();
         }
     }
 }

@@ -1,0 +1,66 @@
+"""Multi-process host logic at world size 2 on CPU (gloo): partition + gather.
+
+The per-rank compute is injected (the oracle stands in for the GPU here, as
+the tests may use it); the CUDA path is the default compute on GPU boxes.
+"""
+import os
+import socket
+
+import numpy as np
+import torch.multiprocessing as mp
+
+import datagen
+from paper_2002_05200_b200 import multi
+
+
+def _free_port():
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    p = s.getsockname()[1]
+    s.close()
+    return p
+
+
+def test_partition_is_a_balanced_permutation():
+    w = datagen.CONFIGS[4]
+    b = datagen.generate(w, n_pairs=3000, u8=False)
+    costs = multi.pair_costs(b.q_len, b.t_len, b.q_seed, b.t_seed, w.k)
+    for g in (1, 2, 4, 8):
+        parts = multi.partition_lpt(costs, g)
+        allidx = np.sort(np.concatenate(parts))
+        assert (allidx == np.arange(b.n_pairs)).all()
+        loads = np.array([costs[p].sum() for p in parts])
+        assert loads.max() - loads.min() <= costs.max()  # LPT bound
+        assert multi.partition_lpt(costs, g)[0].tolist() == parts[0].tolist()  # deterministic
+
+
+def _oracle_compute(sub, w):
+    import oracle
+    return oracle.pairs(sub.pool_u8, 0, sub.q_off, sub.q_len, sub.t_off, sub.t_len, sub.q_seed,
+                        sub.t_seed, w.k, w.match, w.mismatch, w.gap, w.xdrop, pool_len=sub.pool_len,
+                        n_threads=2)
+
+
+def _worker(rank, world, port, ret):
+    import torch.distributed as dist
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    w = datagen.CONFIGS[1]
+    b = datagen.generate(w, n_pairs=120)
+    out, cells = multi.run_sharded(b, w, compute=_oracle_compute)
+    ret[rank] = (out.copy(), cells.copy())
+    dist.destroy_process_group()
+
+
+def test_sharded_gather_equals_single_process():
+    world = 2
+    mgr = mp.Manager()
+    ret = mgr.dict()
+    mp.spawn(_worker, args=(world, _free_port(), ret), nprocs=world, join=True)
+    w = datagen.CONFIGS[1]
+    b = datagen.generate(w, n_pairs=120)
+    ref = _oracle_compute(b, w)
+    for r in range(world):
+        out, cells = ret[r]
+        assert (out == ref[0]).all() and (cells == ref[1]).all()
