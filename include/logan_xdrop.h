@@ -86,13 +86,21 @@ enum {
  *                  stage the call launches: stage 0 = setup (task expansion,
  *                  LPT bucketing), stages 1..6 = levels 1..6, stage 7 =
  *                  combine. Stages not launched leave their events untouched.
+ *  flags         : bit 0 = run the first level in its latency shape (one
+ *                  warp per task) instead of its throughput shape.
+ *  handover      : test knob, 0 = off. If > 0, every task at a register
+ *                  window level is handed over to the next level every
+ *                  `handover` antidiagonals, exercising the exact hand-over.
+ *                  Results never depend on it.
  */
 #define LOGAN_N_STAGES 8
 typedef struct {
     int32_t first_level;
-    int32_t reserved0;
+    int32_t flags;
     void *const *timing_events;
-    int64_t reserved[6];
+    int32_t handover;
+    int32_t reserved1;
+    int64_t reserved[5];
 } logan_options_t;
 
 /* Per-call device-side statistics (optional output in DEVICE memory, may be

@@ -30,8 +30,9 @@ N_STAGES = 8  # LOGAN_N_STAGES: 0 setup, 1..6 levels, 7 combine
 
 
 class Options(ctypes.Structure):
-    _fields_ = [("first_level", ctypes.c_int32), ("reserved0", ctypes.c_int32),
-                ("timing_events", ctypes.c_void_p), ("reserved", ctypes.c_int64 * 6)]
+    _fields_ = [("first_level", ctypes.c_int32), ("flags", ctypes.c_int32),
+                ("timing_events", ctypes.c_void_p), ("handover", ctypes.c_int32),
+                ("reserved1", ctypes.c_int32), ("reserved", ctypes.c_int64 * 5)]
 
 
 class Result(ctypes.Structure):

@@ -288,6 +288,7 @@ static int run_batch(const Params &P, const logan_options_t *opt, logan_result_t
         io.level = lv;
         io.tres = tres;
         io.in_recs = in_recs;
+        io.handover = opt ? opt->handover : 0;
         io.rec_in = rec_in;
         io.rec_in_stride = rec_in_stride;
         if (lv < NWIDTH - 1) {
@@ -304,7 +305,7 @@ static int run_batch(const Params &P, const logan_options_t *opt, logan_result_t
                 io.cursor = &ctr[1 + lv];
                 io.min_count = 0;
                 io.max_count = 0xffffffffu;
-                e = launch_width<FMT>(lv, false, P, io, sms, s);
+                e = launch_width<FMT>(lv, opt && (opt->flags & 1), P, io, sms, s);
             } else {
                 io.cursor = &ctr[1 + lv];
                 io.min_count = 0;
@@ -413,6 +414,7 @@ int logan_xdrop_batch(const uint8_t *seq_pool, int32_t seq_fmt, int64_t pool_len
     P.n_pairs = n_pairs;
     P.k = k;
     P.match = sc.match; P.mismatch = sc.mismatch; P.gap = sc.gap; P.xdrop = sc.xdrop;
+    P.one = 1;
 
     // extension lengths beyond the wide scratch would overflow it: such pairs
     // are rejected up front by the caller-side bound (documented in the header)

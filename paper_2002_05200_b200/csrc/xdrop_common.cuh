@@ -27,6 +27,7 @@ struct Params {
     int64_t n_pairs;
     int32_t k;
     int32_t match, mismatch, gap, xdrop;
+    int32_t one;  // = 1 at run time; opaque to the compiler (see Window::cell)
 };
 
 // Result of one extension task (L or R of one pair), 24 bytes.
@@ -59,6 +60,7 @@ struct LevelIO {
     int64_t rec_out_stride;
     uint32_t rec_out_cap;
     uint32_t *rec_out_count;
+    int32_t handover;            // test knob: force a hand-over every N antidiagonals (0 = off)
 };
 
 constexpr uint32_t NO_TASK = 0xffffffffu;

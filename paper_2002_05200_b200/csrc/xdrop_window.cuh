@@ -88,14 +88,18 @@ constexpr int REC_HDR = 32;
 __host__ __device__ constexpr int rec_ints(int W) { return REC_HDR + 2 * W; }
 constexpr uint32_t NO_REC = 0xffffffffu;
 
+// Reductions over the G lanes of a group: one CREDUX for a full warp,
+// SHFL butterflies for sub-warp groups.
 template <int G>
 __device__ __forceinline__ int32_t grp_max(int32_t v, unsigned gmask) {
+    if (G == 32) return __reduce_max_sync(0xffffffffu, v);
 #pragma unroll
     for (int o = G / 2; o > 0; o >>= 1) v = max(v, __shfl_xor_sync(gmask, v, o, G));
     return v;
 }
 template <int G>
 __device__ __forceinline__ int32_t grp_min(int32_t v, unsigned gmask) {
+    if (G == 32) return __reduce_min_sync(0xffffffffu, v);
 #pragma unroll
     for (int o = G / 2; o > 0; o >>= 1) v = min(v, __shfl_xor_sync(gmask, v, o, G));
     return v;
@@ -121,11 +125,18 @@ struct Window {
     // One cell (eq. P:85 + the drop rule P:89) on threshold-relative values:
     //   u = max(max(up, left, fg) + gap', diag + s'), then the exact kill
     //   min_u32(u, DEAD): every negative u becomes DEAD, live values stay.
-    // VIMNMX3 + VIADDMNMX + VIMNMX.U32 on the ALU pipe, diag + s' an add.
+    // The kernel is bound by the ALU pipe (VIMNMX3, VIADDMNMX, VIMNMX.U32 and
+    // the mismatch test live there), so diag + s' is computed on the FMA pipe:
+    // an IMAD by an opaque run-time 1 for the match case, overwritten by a
+    // predicated IMAD for a mismatch -- no SEL, no IADD3.
     __device__ __forceinline__ static int32_t cell(int32_t up, int32_t left, int32_t diag, bool mis,
-                                                   int32_t gp, int32_t fg, int32_t sma, int32_t smi) {
+                                                   int32_t gp, int32_t fg, int32_t sma, int32_t smi,
+                                                   int32_t one) {
         const int32_t t0 = __vimax3_s32(up, left, fg);
-        const int32_t dps = diag + (mis ? smi : sma);
+        int32_t dps;
+        asm("mad.lo.s32 %0, %1, %2, %3;" : "=r"(dps) : "r"(diag), "r"(one), "r"(sma));
+        asm("{\n\t.reg .pred q;\n\tsetp.ne.u32 q, %1, 0;\n\t@q mad.lo.s32 %0, %2, %3, %4;\n\t}"
+            : "+r"(dps) : "r"((uint32_t)mis), "r"(diag), "r"(one), "r"(smi));
         const int32_t u = __viaddmax_s32(t0, gp, dps);
         return (int32_t)min((uint32_t)u, DEADU);
     }
@@ -273,12 +284,14 @@ struct Window {
     template <int PAR>
     __device__ __forceinline__ int step(const Params &P) {
         const int32_t d = st.d + 1;
-        const int32_t ch = ceil_half(d), fh = floor_half(d);
+        const int32_t ch = PAR ? (d + 1) >> 1 : d >> 1, fh = PAR ? (d - 1) >> 1 : d >> 1;
 
         // (1) band cells of antidiagonal d from the live extremes of d-1, d-2
         //     (c-amb-14: lo = max(1, d-n, min(F1, F2+1)), hi = min(m, d-1, max(L1, L2)+1))
         if (d >= 2 && (st.h1 || st.h2)) {
-            const int32_t c1 = ceil_half(d - 1), c2 = ceil_half(d - 2);
+            // columns of slots on d-1 and d-2 (PAR fixes the parity of d)
+            const int32_t c1 = PAR ? (d - 1) >> 1 : d >> 1;
+            const int32_t c2 = PAR ? (d - 1) >> 1 : (d - 2) >> 1;
             int32_t lo, hi;
             if (st.h1 && st.h2) {
                 lo = min(st.sF1 + c1, st.sF2 + c2 + 1);
@@ -333,7 +346,7 @@ struct Window {
             for (int r = 0; r < R; ++r) {
                 const int32_t up = (r < R - 1) ? E[r + 1] : nb;
                 const bool mis = ((X[r / FPW] >> (CB * (r % FPW))) & FM) != 0;
-                O[r] = cell(up, E[r], O[r], mis, gp, fg, sma, smi);
+                O[r] = cell(up, E[r], O[r], mis, gp, fg, sma, smi, P.one);
             }
         } else {
             int32_t nb = DEAD;  // O[-1] of this lane = O[R-1] of the previous lane
@@ -345,7 +358,7 @@ struct Window {
             for (int r = 0; r < R; ++r) {
                 const int32_t left = (r > 0) ? O[r - 1] : nb;
                 const bool mis = ((X[r / FPW] >> (CB * (r % FPW))) & FM) != 0;
-                E[r] = cell(O[r], left, E[r], mis, gp, fg, sma, smi);
+                E[r] = cell(O[r], left, E[r], mis, gp, fg, sma, smi, P.one);
             }
         }
         // keys u * KEYMUL + 1023 - r and sign chains over the new antidiagonal
@@ -514,9 +527,18 @@ __global__ void __launch_bounds__(128) k_window(const Params P, const LevelIO io
     };
 
     bool active = next_task();
+    int32_t since = 0;  // antidiagonals at this level (hand-over test knob)
     while (active) {
-        int rc = w.template step<1>(P);
-        if (rc == 0) rc = w.template step<0>(P);
+        // one iteration = the odd then the even antidiagonal; a task resumed
+        // after an odd antidiagonal first takes the even one alone
+        int rc;
+        if ((w.st.d & 1) == 0) {
+            rc = w.template step<1>(P);
+            if (rc == 0) rc = w.template step<0>(P);
+        } else {
+            rc = w.template step<0>(P);
+        }
+        if (io.handover > 0 && rc == 0 && io.rec_out && (since += 2) >= io.handover) rc = 2;
         if (rc != 0) {
             uint32_t rec = NO_REC;
             if (rc == 2 && io.rec_out) {  // hand the exact state to the next level
@@ -553,6 +575,7 @@ __global__ void __launch_bounds__(128) k_window(const Params P, const LevelIO io
                 }
             }
             if (rc == 2) w.st.shifts = 0;
+            since = 0;
             active = next_task();
         }
     }

@@ -234,3 +234,47 @@ def test_repeatable_and_permutation_invariant():
                        b.q_seed[perm], b.t_seed[perm], b.pool_len, b.pool_u8, b.pool_2bit)
     ap = gpu_run(bp, 50)
     assert (ap[0] == a1[0][perm]).all() and (ap[1] == a1[1][perm]).all()
+
+
+def _mixed_pairs(seed, n=300, maxlen=300):
+    rng = random.Random(seed)
+    pairs = []
+    for _ in range(n):
+        a = "".join(rng.choice("ACGT") for _ in range(rng.randint(1, maxlen)))
+        if rng.random() < 0.6:
+            b = "".join(ch if rng.random() > 0.12 else rng.choice(["", ch + rng.choice("ACGT"), rng.choice("ACGT")])
+                        for ch in a) or "A"
+        else:
+            b = "".join(rng.choice("ACGT") for _ in range(rng.randint(1, maxlen)))
+        pairs.append((a, b, rng.randint(0, len(a)), rng.randint(0, len(b))))
+    return datagen.from_strings(pairs, k=0)
+
+
+@pytest.mark.parametrize("lvl", [1, 2, 3, 4, 5])
+def test_latency_shapes_as_first_level(lvl):
+    """Every level's latency shape (one warp per task), forced as the first level."""
+    b = _mixed_pairs(lvl)
+    for X in (0, 3, 10, 30, 80):
+        ref = oracle_run(b, X)
+        for fmt in FMTS:
+            db = logan.to_device(b, fmt)
+            out, cells = logan.xdrop_batch(db, 1, -1, -1, X, first_level=lvl, latency_first=True)
+            torch.cuda.synchronize()
+            assert_same(out.cpu().numpy(), cells.cpu().numpy().view(np.uint64), *ref,
+                        what=f"latency level {lvl} X={X} fmt={fmt}")
+
+
+@pytest.mark.parametrize("period", [2, 6, 40])
+def test_forced_handover_is_exact(period):
+    """Tasks handed over between levels every `period` antidiagonals (exact resume)."""
+    b = _mixed_pairs(100 + period)
+    for X in (0, 3, 10, 30):
+        ref = oracle_run(b, X)
+        for lvl in (1, 2):
+            for lat in (False, True):
+                db = logan.to_device(b, logan.LOGAN_SEQ_2BIT)
+                out, cells = logan.xdrop_batch(db, 1, -1, -1, X, first_level=lvl, latency_first=lat,
+                                               handover=period)
+                torch.cuda.synchronize()
+                assert_same(out.cpu().numpy(), cells.cpu().numpy().view(np.uint64), *ref,
+                            what=f"handover {period} level {lvl} lat={lat} X={X}")
