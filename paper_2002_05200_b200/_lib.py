@@ -58,7 +58,7 @@ def load(path: str | None = None) -> ctypes.CDLL:
     global _lib
     if _lib is not None:
         return _lib
-    path = path or LIB_PATH
+    path = path or os.environ.get("LOGAN_LIB") or LIB_PATH
     if not os.path.exists(path):
         raise LoganError(f"{path} is missing: build it with `python -m paper_2002_05200_b200.build` "
                          "(there is no CPU fallback)")

@@ -34,11 +34,14 @@ def needs_build() -> bool:
     return any(os.path.getmtime(s) > t for s in sources())
 
 
-def build(force: bool = False, verbose: bool = False) -> str:
-    if not force and not needs_build():
+def build(force: bool = False, verbose: bool = False, out: str | None = None,
+          defines: tuple = ()) -> str:
+    """Build the library (``out`` / ``defines`` build an experimental variant)."""
+    target = out or LIB
+    if out is None and not force and not needs_build():
         return LIB
-    tmp = LIB + ".tmp"
-    cmd = [NVCC, *FLAGS, "-o", tmp, os.path.join(CSRC, "logan_xdrop.cu")]
+    tmp = target + ".tmp"
+    cmd = [NVCC, *FLAGS, *[f"-D{d}" for d in defines], "-o", tmp, os.path.join(CSRC, "logan_xdrop.cu")]
     res = subprocess.run(cmd, capture_output=True, text=True)
     if res.returncode != 0:
         sys.stderr.write(res.stdout + res.stderr)
@@ -47,8 +50,8 @@ def build(force: bool = False, verbose: bool = False) -> str:
         f.write(res.stderr)
     if verbose:
         sys.stderr.write(res.stderr)
-    os.replace(tmp, LIB)
-    return LIB
+    os.replace(tmp, target)
+    return target
 
 
 if __name__ == "__main__":

@@ -73,7 +73,7 @@ static Layout make_layout(int64_t n_pairs, int64_t max_ext_len) {
     L.hist = o;     o += align256(sizeof(uint32_t) * NBUCKET);
     L.cursor_b = o; o += align256(sizeof(uint32_t) * NBUCKET);
     // counters: [0] queue count, [1..NLEVEL] level cursors, [8..8+NLEVEL] out counts,
-    // [16..16+NWIDTH-1] record pool fill
+    // [16..16+NWIDTH-1] record pool fill, [24] producer groups done (helpers)
     L.counters = o; o += align256(sizeof(uint32_t) * 32);
     L.wide_stride = max_ext_len + 2;
     L.wide = o;     o += align256(sizeof(int32_t) * 3 * (size_t)L.wide_stride * WIDE_CTAS);
@@ -188,33 +188,55 @@ __global__ void k_combine(const Params P, const TaskRes *tres, logan_result_t *o
 // Throughput shape: G = W/32 lanes x R = 32 slots (many tasks in flight).
 // Latency shape: one warp per task, R = W/32 slots per lane (few tasks left:
 // the step's critical path is short). Level 5 is the unbounded CTA path.
-template <int G, int R, int FMT>
-static cudaError_t launch_win(const Params &P, const LevelIO &io, int sms, cudaStream_t s) {
-    const size_t smem = 128 * sizeof(int32_t) * Window<G, R, FMT>::SB_STRIDE;
-    cudaError_t e = cudaFuncSetAttribute(k_window<G, R, FMT>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+template <int G, int R, int FMT, int HR>
+static cudaError_t launch_win(const Params &P, const LevelIO &io_in, const LevelIO &hio, int sms, cudaStream_t s) {
+    constexpr int S1 = Window<G, R, FMT>::SB_STRIDE;
+    constexpr int S2 = HR > 0 ? Window<32, (HR > 0 ? HR : 1), FMT>::SB_STRIDE : 0;
+    const size_t smem = 128 * sizeof(int32_t) * (S1 > S2 ? S1 : S2);
+    auto kern = k_window<G, R, FMT, HR>;
+    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return e;
     int occ = 0;
-    e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_window<G, R, FMT>, 128, smem);
+    e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, 128, smem);
     if (e != cudaSuccess) return e;
     if (occ < 1) occ = 1;
-    k_window<G, R, FMT><<<sms * occ, 128, smem, s>>>(P, io);
+    const int grid = sms * occ;
+    LevelIO io = io_in;
+    if (HR > 0) {
+        io.helpers = grid < 32 ? grid : 32;
+        io.workers = (uint32_t)((grid * 128 - io.helpers * 32) / G);
+    } else {
+        io.helpers = 0;
+    }
+    kern<<<grid, 128, smem, s>>>(P, io, hio);
     return cudaGetLastError();
 }
 
+// wi = width index; latency = run the latency shape; helpers = first level with
+// in-kernel escalation helpers running the next width's latency shape
 template <int FMT>
-static cudaError_t launch_width(int wi, bool latency, const Params &P, const LevelIO &io, int sms,
-                                cudaStream_t s) {
+static cudaError_t launch_width(int wi, bool latency, bool helpers, const Params &P, const LevelIO &io,
+                                const LevelIO &hio, int sms, cudaStream_t s) {
+    if (helpers && !latency) {
+        switch (wi) {
+            case 0: return launch_win<1, 32, FMT, 2>(P, io, hio, sms, s);
+            case 1: return launch_win<2, 32, FMT, 4>(P, io, hio, sms, s);
+            case 2: return launch_win<4, 32, FMT, 8>(P, io, hio, sms, s);
+            case 3: return launch_win<8, 32, FMT, 32>(P, io, hio, sms, s);
+            default: break;
+        }
+    }
     switch (wi * 2 + (latency ? 1 : 0)) {
-        case 0: return launch_win<1, 32, FMT>(P, io, sms, s);
-        case 1: return launch_win<32, 1, FMT>(P, io, sms, s);
-        case 2: return launch_win<2, 32, FMT>(P, io, sms, s);
-        case 3: return launch_win<32, 2, FMT>(P, io, sms, s);
-        case 4: return launch_win<4, 32, FMT>(P, io, sms, s);
-        case 5: return launch_win<32, 4, FMT>(P, io, sms, s);
-        case 6: return launch_win<8, 32, FMT>(P, io, sms, s);
-        case 7: return launch_win<32, 8, FMT>(P, io, sms, s);
+        case 0: return launch_win<1, 32, FMT, 0>(P, io, hio, sms, s);
+        case 1: return launch_win<32, 1, FMT, 0>(P, io, hio, sms, s);
+        case 2: return launch_win<2, 32, FMT, 0>(P, io, hio, sms, s);
+        case 3: return launch_win<32, 2, FMT, 0>(P, io, hio, sms, s);
+        case 4: return launch_win<4, 32, FMT, 0>(P, io, hio, sms, s);
+        case 5: return launch_win<32, 4, FMT, 0>(P, io, hio, sms, s);
+        case 6: return launch_win<8, 32, FMT, 0>(P, io, hio, sms, s);
+        case 7: return launch_win<32, 8, FMT, 0>(P, io, hio, sms, s);
         case 8:
-        case 9: return launch_win<32, 32, FMT>(P, io, sms, s);
+        case 9: return launch_win<32, 32, FMT, 0>(P, io, hio, sms, s);
         default: return cudaErrorInvalidValue;
     }
 }
@@ -278,49 +300,62 @@ static int run_batch(const Params &P, const logan_options_t *opt, logan_result_t
     int out_sel = 0;
     // below this many tasks a level runs in its latency shape (one warp per task)
     const uint32_t latency_below = (uint32_t)sms * 16u;
-    for (int lv = first; lv < NLEVEL; ++lv) {
+    // the IO of window level lv, given its input list / records
+    auto level_io = [&](int lv, const uint32_t *lst, const uint32_t *cnt, const uint32_t *irecs,
+                        const int32_t *rin, int64_t rin_stride, int osel) {
         LevelIO io{};
-        io.list = in_list;
-        io.count = in_count;
-        io.out_list = lists[out_sel];
+        io.list = lst;
+        io.count = cnt;
+        io.cursor = &ctr[1 + lv];
+        io.out_list = lists[osel];
         io.out_count = &ctr[8 + lv];
         io.stats = stats;
         io.level = lv;
         io.tres = tres;
-        io.in_recs = in_recs;
+        io.in_recs = irecs;
+        io.rec_in = rin;
+        io.rec_in_stride = rin_stride;
         io.handover = opt ? opt->handover : 0;
-        io.rec_in = rec_in;
-        io.rec_in_stride = rec_in_stride;
+        io.min_count = 0;
+        io.max_count = 0xffffffffu;
         if (lv < NWIDTH - 1) {
-            io.out_recs = recs[out_sel];
+            io.out_recs = recs[osel];
             io.rec_out = (int32_t *)(ws + L.pool[lv]);
             io.rec_out_stride = rec_ints(kWidth[lv]);
             io.rec_out_cap = L.pool_cap[lv];
             io.rec_out_count = &ctr[16 + lv];
         }
+        return io;
+    };
+    const bool latency_first = opt && (opt->flags & 1);
+    for (int lv = first; lv < NLEVEL; ++lv) {
+        LevelIO io = level_io(lv, in_list, in_count, in_recs, rec_in, rec_in_stride, out_sel);
         cudaError_t e = cudaSuccess;
         if (!mark(1 + lv, 0)) return LOGAN_ECUDA;
         if (lv < NWIDTH) {
             if (lv == first) {
-                io.cursor = &ctr[1 + lv];
-                io.min_count = 0;
-                io.max_count = 0xffffffffu;
-                e = launch_width<FMT>(lv, opt && (opt->flags & 1), P, io, sms, s);
+                const bool helpers = !latency_first && lv + 1 < NWIDTH;
+                LevelIO hio{};
+                if (helpers) {
+                    // the next level's IO: it reads this level's hand-overs
+                    hio = level_io(lv + 1, lists[out_sel], &ctr[8 + lv], recs[out_sel],
+                                   (const int32_t *)(ws + L.pool[lv]), rec_ints(kWidth[lv]), out_sel ^ 1);
+                    io.done = &ctr[24];
+                    // entries are published by writing the task id: start from NO_TASK
+                    if (cudaMemsetAsync(lists[out_sel], 0xff, sizeof(uint32_t) * (size_t)L.ntask, s) != cudaSuccess)
+                        return LOGAN_ECUDA;
+                }
+                e = launch_width<FMT>(lv, latency_first, helpers, P, io, hio, sms, s);
             } else {
-                io.cursor = &ctr[1 + lv];
-                io.min_count = 0;
                 io.max_count = latency_below;
-                e = launch_width<FMT>(lv, true, P, io, sms, s);
+                e = launch_width<FMT>(lv, true, false, P, io, io, sms, s);
                 if (e == cudaSuccess) {
                     io.min_count = latency_below;
                     io.max_count = 0xffffffffu;
-                    e = launch_width<FMT>(lv, false, P, io, sms, s);
+                    e = launch_width<FMT>(lv, false, false, P, io, io, sms, s);
                 }
             }
         } else {
-            io.cursor = &ctr[1 + lv];
-            io.min_count = 0;
-            io.max_count = 0xffffffffu;
             k_wide<FMT><<<WIDE_CTAS, WIDE_THREADS, 0, s>>>(P, io, wide, L.wide_stride);
             e = cudaGetLastError();
         }

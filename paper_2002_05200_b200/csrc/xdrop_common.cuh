@@ -61,6 +61,10 @@ struct LevelIO {
     uint32_t rec_out_cap;
     uint32_t *rec_out_count;
     int32_t handover;            // test knob: force a hand-over every N antidiagonals (0 = off)
+    // in-kernel escalation helpers (first level only)
+    int32_t helpers;             // blocks whose last warp is a helper
+    uint32_t workers;            // producer groups (non-helper groups) in the launch
+    uint32_t *done;              // producer groups that finished
 };
 
 constexpr uint32_t NO_TASK = 0xffffffffu;

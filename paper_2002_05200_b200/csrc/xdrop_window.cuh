@@ -54,6 +54,12 @@ constexpr uint32_t DEADU = 0xFFF00000u;  // (uint32_t)DEAD
 // |DEAD| * KEYMUL < 2^31 and (X + 2*127) * KEYMUL < 2^31 for X <= 2^19.
 constexpr int32_t KEYMUL = 1027;
 
+// How many of the 4 sign-mask chains run on the FMA pipe (the rest use SHF on
+// the ALU pipe): balances the two pipes (tuned by measurement).
+#ifndef LOGAN_MASK_FMA_CHAINS
+#define LOGAN_MASK_FMA_CHAINS 0
+#endif
+
 template <int FMT> struct RegFmt;
 template <> struct RegFmt<LOGAN_SEQ_2BIT> {
     static constexpr int CB = 4;                 // bits per register field
@@ -113,6 +119,7 @@ struct Window {
     static constexpr int NW = (R + FPW - 1) / FPW;  // words per lane per sequence
     static constexpr int RL = R - (NW - 1) * FPW;   // fields in the last word
     static constexpr int W = G * R;
+    static constexpr int GG = G;
     static constexpr uint32_t FM = (1u << CB) - 1u;
     static_assert(R >= 1 && R <= 32 && W <= 1024 && (G & (G - 1)) == 0, "window shape");
 
@@ -328,6 +335,7 @@ struct Window {
         const int32_t smi = P.mismatch - (Tc - st.Tp);
         const int32_t fg = DEAD - gp;  // max(up, left, fg) + gp >= DEAD: the floor
 
+        const uint32_t two = 2u * (uint32_t)P.one;  // = 2, opaque to the compiler
         uint32_t X[NW];
 #pragma unroll
         for (int q = 0; q < NW; ++q) X[q] = Aw[q] ^ Bw[q];
@@ -367,7 +375,14 @@ struct Window {
             const int32_t u = PAR ? O[r] : E[r];
             const int c = r / RQ;
             kq[c] = max(kq[c], u * KEYMUL + (1023 - r));
-            dq[c] = __funnelshift_l((uint32_t)u, dq[c], 1);  // appends sign(u): bit (r - c*RQ)
+            // append sign(u) (1 = dead) as bit (r - c*RQ): dq = 2*dq + (u >>> 31)
+            if (LOGAN_MASK_FMA_CHAINS > c) {  // two IMADs on the FMA pipe
+                uint32_t sg;
+                asm("mul.hi.u32 %0, %1, %2;" : "=r"(sg) : "r"((uint32_t)u), "r"(two));
+                asm("mad.lo.u32 %0, %1, %2, %3;" : "=r"(dq[c]) : "r"(dq[c]), "r"(two), "r"(sg));
+            } else {  // one funnel shift on the ALU pipe
+                dq[c] = __funnelshift_l((uint32_t)u, dq[c], 1);
+            }
         }
         int32_t kmax = max(max(kq[0], kq[1]), max(kq[2], kq[3]));
         uint32_t dead = 0;
@@ -375,12 +390,17 @@ struct Window {
         for (int c = 0; c < 4; ++c)
             if (c * RQ < R) dead |= dq[c] << (c * RQ);
 
-        // (5) validity of slots (0 <= i <= m, 0 <= j <= n) for this lane
-        const int32_t vlo = max(-ch, fh - st.n), vhi = min(st.m - ch, fh);
+        // (5) validity of slots for this lane: cells with i < 0 or j < 0 are dead
+        //     by construction; cells past the matrix (i > m or j > n) are masked
+        //     out of the band bookkeeping (slot s: i <= m <=> s <= m - ch,
+        //     j <= n <=> s >= fh - n). Most steps take the all-valid path.
+        const int32_t vlo = fh - st.n, vhi = st.m - ch;
         const int32_t base = st.S0 + gl * R;
-        int32_t rlo = max(vlo - base, 0), rhi = min(vhi - base, R - 1);
-        uint32_t vmask = 0;
-        if (rlo <= rhi) vmask = (0xffffffffu >> (31 - rhi)) & ~((1u << rlo) - 1u);
+        uint32_t vmask = (R == 32) ? 0xffffffffu : ((1u << R) - 1u);
+        if (vlo > base || vhi < base + R - 1) {
+            const int32_t rlo = max(vlo - base, 0), rhi = min(vhi - base, R - 1);
+            vmask = (rlo <= rhi) ? ((0xffffffffu >> (31 - rhi)) & ~((1u << rlo) - 1u)) : 0u;
+        }
         const uint32_t live = ~dead & vmask;
         int32_t lf = live ? gl * R + __ffs(live) - 1 : INT32_MAX;
         int32_t ll = live ? gl * R + 31 - __clz(live) : INT32_MIN;
@@ -495,28 +515,17 @@ struct Window {
     }
 };
 
-// Persistent kernel: each group of G lanes pulls tasks from the level's list.
-// A level may exist in two shapes (throughput: G small, R = 32; latency: one
-// warp per task); the launch whose [min_count, max_count) holds the list length
-// runs, the other exits at once (no host synchronisation).
-template <int G, int R, int FMT>
-__global__ void __launch_bounds__(128) k_window(const Params P, const LevelIO io) {
-    const uint32_t count = *io.count;
-    if (count < io.min_count || count >= io.max_count) return;
-    Window<G, R, FMT> w;
-    extern __shared__ int32_t win_smem[];
-    w.sbase = win_smem + threadIdx.x * Window<G, R, FMT>::SB_STRIDE;
+// Runs one group's task loop. `fetch(pos&)` yields the next list position (or
+// false when there is none); the loop starts or resumes that task, sweeps it to
+// completion or hand-over, and writes the result / publishes the hand-over.
+template <class Win, class Fetch>
+__device__ __forceinline__ void run_group(Win &w, const Params &P, const LevelIO &io, Fetch fetch) {
+    constexpr int G = Win::GG;
     const int lane = threadIdx.x & 31;
-    w.gl = lane % G;
-    w.gmask = (G == 32) ? 0xffffffffu : (((1u << G) - 1u) << (lane - w.gl));
     const int leader = lane - w.gl;
-
-    // take the next list entry; start or resume it
     auto next_task = [&]() -> bool {
-        uint32_t pos = 0xffffffffu;
-        if (w.gl == 0) pos = atomicAdd(io.cursor, 1u);
-        if (G > 1) pos = __shfl_sync(w.gmask, pos, leader);
-        if (pos >= count) return false;
+        uint32_t pos;
+        if (!fetch(pos)) return false;
         const uint32_t task = io.list[pos];
         const uint32_t rec = io.in_recs ? io.in_recs[pos] : NO_REC;
         if (rec != NO_REC) w.resume(P, io.rec_in + (size_t)rec * io.rec_in_stride);
@@ -548,6 +557,7 @@ __global__ void __launch_bounds__(128) k_window(const Params P, const LevelIO io
                 }
                 if (G > 1) rec = __shfl_sync(w.gmask, rec, leader);
                 if (rec != NO_REC) w.save(io.rec_out + (size_t)rec * io.rec_out_stride);
+                if (G > 1) __syncwarp(w.gmask);
             }
             if (w.gl == 0) {
                 if (rc == 1) {
@@ -559,9 +569,12 @@ __global__ void __launch_bounds__(128) k_window(const Params P, const LevelIO io
                     tr.cells = w.st.cells;
                     io.tres[w.st.task] = tr;
                 } else {
+                    // publish: record index first, then the task id (the entry's
+                    // ready flag for in-kernel consumers; lists start as NO_TASK)
                     const uint32_t o = atomicAdd(io.out_count, 1u);
-                    io.out_list[o] = w.st.task;
                     if (io.out_recs) io.out_recs[o] = rec;
+                    __threadfence();
+                    *(volatile uint32_t *)&io.out_list[o] = w.st.task;
                 }
                 if (io.stats) {
                     atomicAdd((unsigned long long *)&io.stats->window_shifts, (unsigned long long)w.st.shifts);
@@ -578,6 +591,71 @@ __global__ void __launch_bounds__(128) k_window(const Params P, const LevelIO io
             since = 0;
             active = next_task();
         }
+    }
+}
+
+// Persistent kernel: each group of G lanes pulls tasks from the level's list.
+// A level may exist in two shapes (throughput: G small, R = 32; latency: one
+// warp per task); the launch whose [min_count, max_count) holds the list length
+// runs, the other exits at once (no host synchronisation).
+//
+// With HR > 0 (first level only), the last warp of the first `io.helpers`
+// blocks runs the NEXT level in its latency shape (one warp per task, window
+// 32*HR) on the tasks this level hands over, as soon as each is published:
+// overflowing tasks then finish while this level is still running instead of
+// forming a serial tail after it. What the helpers do not take, the next
+// level's own launch does (it shares their cursor).
+template <int G, int R, int FMT, int HR>
+__global__ void __launch_bounds__(128) k_window(const Params P, const LevelIO io, const LevelIO hio) {
+    const uint32_t count = *io.count;
+    if (count < io.min_count || count >= io.max_count) return;
+    extern __shared__ int32_t win_smem[];
+    const int lane = threadIdx.x & 31;
+    const bool helper = HR > 0 && (int)blockIdx.x < io.helpers && (threadIdx.x >> 5) == (blockDim.x >> 5) - 1;
+    if (HR > 0 && helper) {
+        Window<32, (HR > 0 ? HR : 1), FMT> w;
+        w.sbase = win_smem + threadIdx.x * Window<32, (HR > 0 ? HR : 1), FMT>::SB_STRIDE;
+        w.gl = lane;
+        w.gmask = 0xffffffffu;
+        const uint32_t total = io.workers;
+        auto fetch = [&](uint32_t &pos) -> bool {
+            uint32_t p = 0;
+            if (lane == 0) p = atomicAdd(hio.cursor, 1u);
+            p = __shfl_sync(0xffffffffu, p, 0);
+            for (;;) {  // wait until entry p exists, or no producer is left
+                const uint32_t cnt = *(volatile const uint32_t *)io.out_count;
+                if (p < cnt) break;
+                if (*(volatile const uint32_t *)io.done == total) {
+                    __threadfence();
+                    if (p >= *(volatile const uint32_t *)io.out_count) return false;
+                    break;
+                }
+                __nanosleep(1000);
+            }
+            while (*(volatile const uint32_t *)&io.out_list[p] == NO_TASK) __nanosleep(64);
+            __threadfence();
+            pos = p;
+            return true;
+        };
+        run_group(w, P, hio, fetch);
+        return;
+    }
+    Window<G, R, FMT> w;
+    w.sbase = win_smem + threadIdx.x * Window<G, R, FMT>::SB_STRIDE;
+    w.gl = lane % G;
+    w.gmask = (G == 32) ? 0xffffffffu : (((1u << G) - 1u) << (lane - w.gl));
+    const int leader = lane - w.gl;
+    auto fetch = [&](uint32_t &pos) -> bool {
+        uint32_t p = 0xffffffffu;
+        if (w.gl == 0) p = atomicAdd(io.cursor, 1u);
+        if (G > 1) p = __shfl_sync(w.gmask, p, leader);
+        pos = p;
+        return p < count;
+    };
+    run_group(w, P, io, fetch);
+    if (HR > 0 && w.gl == 0) {  // this group will publish no more hand-overs
+        __threadfence();
+        atomicAdd(io.done, 1u);
     }
 }
 
