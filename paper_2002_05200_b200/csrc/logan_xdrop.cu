@@ -35,8 +35,12 @@ __device__ __forceinline__ uint32_t cost_bucket(uint32_t c) {
 }
 
 // Workspace layout (each region 256-byte aligned).
-constexpr int NWIDTH = 5;  // register-window widths 32, 64, 128, 256, 1024
-static const int kWidth[NWIDTH] = {32, 64, 128, 256, 1024};
+// First-level window (G = 1 lane x LOGAN_L0_R slots); tuned by measurement.
+#ifndef LOGAN_L0_R
+#define LOGAN_L0_R 32
+#endif
+constexpr int NWIDTH = 5;  // register-window widths L0, 64, 128, 256, 1024
+static const int kWidth[NWIDTH] = {LOGAN_L0_R, 64, 128, 256, 1024};
 
 struct Layout {
     size_t tres, tbucket, queue, listA, listB, recsA, recsB, hist, cursor_b, counters, wide, total;
@@ -219,7 +223,7 @@ static cudaError_t launch_width(int wi, bool latency, bool helpers, const Params
                                 const LevelIO &hio, int sms, cudaStream_t s) {
     if (helpers && !latency) {
         switch (wi) {
-            case 0: return launch_win<1, 32, FMT, 2>(P, io, hio, sms, s);
+            case 0: return launch_win<1, LOGAN_L0_R, FMT, 2>(P, io, hio, sms, s);
             case 1: return launch_win<2, 32, FMT, 4>(P, io, hio, sms, s);
             case 2: return launch_win<4, 32, FMT, 8>(P, io, hio, sms, s);
             case 3: return launch_win<8, 32, FMT, 32>(P, io, hio, sms, s);
@@ -227,8 +231,9 @@ static cudaError_t launch_width(int wi, bool latency, bool helpers, const Params
         }
     }
     switch (wi * 2 + (latency ? 1 : 0)) {
-        case 0: return launch_win<1, 32, FMT, 0>(P, io, hio, sms, s);
-        case 1: return launch_win<32, 1, FMT, 0>(P, io, hio, sms, s);
+        case 0: return launch_win<1, LOGAN_L0_R, FMT, 0>(P, io, hio, sms, s);
+        case 1: return LOGAN_L0_R == 32 ? launch_win<32, 1, FMT, 0>(P, io, hio, sms, s)
+                                        : launch_win<1, LOGAN_L0_R, FMT, 0>(P, io, hio, sms, s);
         case 2: return launch_win<2, 32, FMT, 0>(P, io, hio, sms, s);
         case 3: return launch_win<32, 2, FMT, 0>(P, io, hio, sms, s);
         case 4: return launch_win<4, 32, FMT, 0>(P, io, hio, sms, s);

@@ -34,7 +34,6 @@ __global__ void __launch_bounds__(WIDE_THREADS) k_wide(const Params P, const Lev
                      scratch + (int64_t)blockIdx.x * 3 * stride + stride,
                      scratch + (int64_t)blockIdx.x * 3 * stride + 2 * stride};
     const uint32_t count = *io.count;
-    if (count < io.min_count || count >= io.max_count) return;
     for (;;) {
         if (tid == 0) {
             const uint32_t pos = atomicAdd(io.cursor, 1u);

@@ -82,8 +82,10 @@ struct WinState {
     int32_t S0;            // slot of the window's first register
     int32_t best, arg_i, arg_j;
     int32_t Tn, Td, Tp;    // T_{d+1}, T_d, T_{d-1}
-    int32_t sF1, sL1, sF2, sL2;  // live slot extremes of d and d-1
-    bool h1, h2;           // d and d-1 hold a (valid) live cell
+    // live slot extremes of d and d-1; an antidiagonal without a (valid) live
+    // cell has sF = EMPTY_F, sL = EMPTY_L, which makes every min / max below
+    // ignore it without a branch
+    int32_t sF1, sL1, sF2, sL2;
     uint64_t cells;
     uint64_t cells_entry;  // cells already counted when the task entered this level
     uint32_t shifts;
@@ -93,6 +95,7 @@ struct WinState {
 constexpr int REC_HDR = 32;
 __host__ __device__ constexpr int rec_ints(int W) { return REC_HDR + 2 * W; }
 constexpr uint32_t NO_REC = 0xffffffffu;
+constexpr int32_t EMPTY_F = 1 << 29, EMPTY_L = -(1 << 29);
 
 // Reductions over the G lanes of a group: one CREDUX for a full warp,
 // SHFL butterflies for sub-warp groups.
@@ -195,9 +198,8 @@ struct Window {
         st.Tp = -P.xdrop;
         st.Tn = -P.xdrop;  // T_1 = best_0 - X
         st.sF1 = st.sL1 = 0;  // antidiagonal 0: the origin (slot 0)
-        st.h1 = true;
-        st.h2 = false;
-        st.sF2 = st.sL2 = 0;
+        st.sF2 = EMPTY_F;     // antidiagonal -1: empty
+        st.sL2 = EMPTY_L;
         st.cells = 0;
         st.shifts = 0;
         // values: origin S(0,0) = 0 -> u = 0 - T_0 = X; everything else dead
@@ -246,7 +248,7 @@ struct Window {
             rec[0] = (int32_t)st.task; rec[1] = st.d; rec[2] = st.S0; rec[3] = st.best;
             rec[4] = st.arg_i; rec[5] = st.arg_j; rec[6] = st.Tn; rec[7] = st.Td; rec[8] = st.Tp;
             rec[9] = st.sF1; rec[10] = st.sL1; rec[11] = st.sF2; rec[12] = st.sL2;
-            rec[13] = (st.h1 ? 1 : 0) | (st.h2 ? 2 : 0);
+            rec[13] = 0;
             rec[14] = (int32_t)st.shifts; rec[15] = W;
             rec[16] = (int32_t)(uint32_t)st.cells; rec[17] = (int32_t)(uint32_t)(st.cells >> 32);
         }
@@ -264,15 +266,12 @@ struct Window {
         st.best = rec[3]; st.arg_i = rec[4]; st.arg_j = rec[5];
         st.Tn = rec[6]; st.Td = rec[7]; st.Tp = rec[8];
         st.sF1 = rec[9]; st.sL1 = rec[10]; st.sF2 = rec[11]; st.sL2 = rec[12];
-        st.h1 = rec[13] & 1; st.h2 = (rec[13] >> 1) & 1;
         st.shifts = (uint32_t)rec[14];
         const int32_t Wsrc = rec[15];
         st.cells = (uint64_t)(uint32_t)rec[16] | ((uint64_t)(uint32_t)rec[17] << 32);
         st.cells_entry = st.cells;
         // centre the wider window on the live band of d and d-1
-        int32_t Fm = INT32_MAX, Lm = INT32_MIN;
-        if (st.h1) { Fm = st.sF1; Lm = st.sL1; }
-        if (st.h2) { Fm = min(Fm, st.sF2); Lm = max(Lm, st.sL2); }
+        int32_t Fm = min(st.sF1, st.sF2), Lm = max(st.sL1, st.sL2);
         if (Fm > Lm) { Fm = S0src; Lm = S0src + Wsrc - 1; }
         st.S0 = ((Fm + Lm) >> 1) - W / 2;
         const int32_t s0 = st.S0 + gl * R;
@@ -295,24 +294,15 @@ struct Window {
 
         // (1) band cells of antidiagonal d from the live extremes of d-1, d-2
         //     (c-amb-14: lo = max(1, d-n, min(F1, F2+1)), hi = min(m, d-1, max(L1, L2)+1))
-        if (d >= 2 && (st.h1 || st.h2)) {
+        //     Empty antidiagonals carry EMPTY_F / EMPTY_L and drop out of the
+        //     min / max; d = 1 clips to an empty band by itself.
+        {
             // columns of slots on d-1 and d-2 (PAR fixes the parity of d)
             const int32_t c1 = PAR ? (d - 1) >> 1 : d >> 1;
             const int32_t c2 = PAR ? (d - 1) >> 1 : (d - 2) >> 1;
-            int32_t lo, hi;
-            if (st.h1 && st.h2) {
-                lo = min(st.sF1 + c1, st.sF2 + c2 + 1);
-                hi = max(st.sL1 + c1, st.sL2 + c2) + 1;
-            } else if (st.h1) {
-                lo = st.sF1 + c1;
-                hi = st.sL1 + c1 + 1;
-            } else {
-                lo = st.sF2 + c2 + 1;
-                hi = st.sL2 + c2 + 1;
-            }
-            lo = max(lo, max(1, d - st.n));
-            hi = min(hi, min(st.m, d - 1));
-            if (hi >= lo) st.cells += (uint64_t)(hi - lo + 1);
+            const int32_t lo = max(min(st.sF1 + c1, st.sF2 + c2 + 1), max(1, d - st.n));
+            const int32_t hi = min(max(st.sL1 + c1, st.sL2 + c2) + 1, min(st.m, d - 1));
+            st.cells += (uint32_t)max(hi - lo + 1, 0);
         }
 
         // (2) bases for antidiagonal d
@@ -429,16 +419,14 @@ struct Window {
         st.d = d;
 
         // (7) termination: antidiagonals d and d-1 both empty (c-amb-7)
-        if (!h && !st.h1) return 1;
-        st.h2 = st.h1; st.sF2 = st.sF1; st.sL2 = st.sL1;
-        st.h1 = h;
-        st.sF1 = st.S0 + lf;
-        st.sL1 = st.S0 + ll;
+        if (!h && st.sF1 == EMPTY_F) return 1;
+        st.sF2 = st.sF1;
+        st.sL2 = st.sL1;
+        st.sF1 = h ? st.S0 + lf : EMPTY_F;
+        st.sL1 = h ? st.S0 + ll : EMPTY_L;
 
         // (8) keep the live band of d and d-1 inside [S0+1, S0+W-2]
-        int32_t Fm = INT32_MAX, Lm = INT32_MIN;
-        if (st.h1) { Fm = st.sF1; Lm = st.sL1; }
-        if (st.h2) { Fm = min(Fm, st.sF2); Lm = max(Lm, st.sL2); }
+        const int32_t Fm = min(st.sF1, st.sF2), Lm = max(st.sL1, st.sL2);
         const bool lowv = Fm < st.S0 + 1, highv = Lm > st.S0 + W - 2;
         if (lowv || highv) {
             if (lowv && highv) return 2;
@@ -608,7 +596,9 @@ __device__ __forceinline__ void run_group(Win &w, const Params &P, const LevelIO
 template <int G, int R, int FMT, int HR>
 __global__ void __launch_bounds__(128) k_window(const Params P, const LevelIO io, const LevelIO hio) {
     const uint32_t count = *io.count;
-    if (count < io.min_count || count >= io.max_count) return;
+    const uint32_t taken = *io.cursor;  // entries already taken (by in-kernel helpers)
+    const uint32_t remaining = count - (taken < count ? taken : count);
+    if (remaining < io.min_count || remaining >= io.max_count) return;
     extern __shared__ int32_t win_smem[];
     const int lane = threadIdx.x & 31;
     const bool helper = HR > 0 && (int)blockIdx.x < io.helpers && (threadIdx.x >> 5) == (blockDim.x >> 5) - 1;
@@ -618,19 +608,27 @@ __global__ void __launch_bounds__(128) k_window(const Params P, const LevelIO io
         w.gl = lane;
         w.gmask = 0xffffffffu;
         const uint32_t total = io.workers;
+        // Helpers only work while producers are still sweeping: once every
+        // producer group is done they stop taking entries, and whatever is left
+        // goes to the next level's own launch (throughput shape if many).
         auto fetch = [&](uint32_t &pos) -> bool {
+            for (;;) {  // take a new entry only while producers are running
+                if (*(volatile const uint32_t *)io.done == total) return false;
+                if (*(volatile const uint32_t *)hio.cursor < *(volatile const uint32_t *)io.out_count) break;
+                __nanosleep(1000);
+            }
             uint32_t p = 0;
             if (lane == 0) p = atomicAdd(hio.cursor, 1u);
             p = __shfl_sync(0xffffffffu, p, 0);
-            for (;;) {  // wait until entry p exists, or no producer is left
-                const uint32_t cnt = *(volatile const uint32_t *)io.out_count;
-                if (p < cnt) break;
+            // a claimed position is either processed here or proven not to exist
+            for (;;) {
+                if (p < *(volatile const uint32_t *)io.out_count) break;
                 if (*(volatile const uint32_t *)io.done == total) {
                     __threadfence();
                     if (p >= *(volatile const uint32_t *)io.out_count) return false;
                     break;
                 }
-                __nanosleep(1000);
+                __nanosleep(500);
             }
             while (*(volatile const uint32_t *)&io.out_list[p] == NO_TASK) __nanosleep(64);
             __threadfence();
