@@ -46,6 +46,8 @@ def parse_args():
     ap.add_argument("--xdrop", type=int, default=None)
     ap.add_argument("--fmt", choices=["2bit", "u8"], default="2bit")
     ap.add_argument("--first-level", type=int, default=0)
+    ap.add_argument("--latency-first", action="store_true",
+                    help="run the first level in its latency shape (one warp per task)")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-seconds", type=float, default=12.0,
@@ -224,7 +226,8 @@ def main():
 
     def step(events=None, stats=None):
         logan.xdrop_batch(db, w.match, w.mismatch, w.gap, w.xdrop, workspace=ws, out=out, cells=cells,
-                          stats=stats, first_level=first, stream=stream, timing_events=events)
+                          stats=stats, first_level=first, stream=stream, timing_events=events,
+                          latency_first=args.latency_first)
 
     # one untimed run with device stats: per-level task and cell counts (deterministic)
     st = logan.new_stats(dev)
@@ -276,7 +279,7 @@ def main():
             stage_ms[stg] = sum(ev[s][2 * stg].elapsed_time(ev[s][2 * stg + 1]) for s in range(args.steps))
         except RuntimeError:
             pass  # stage not launched in this configuration
-    n_launch_stages = [stg for stg in stage_ms if 1 <= stg <= 6]
+    n_launch_stages = [stg for stg in stage_ms if 1 <= stg <= nst - 2]
     launches_per_step = 3 + len(n_launch_stages) + 1  # expand, scan, scatter, levels, combine
 
     # max over ranks (time), sum over ranks (cells)
@@ -302,7 +305,7 @@ def main():
         gather_ms = g0.elapsed_time(g1)
 
     # dominant kernel and its roofline (bound: int32 ALU)
-    dom_stage = max((s for s in stage_ms if 1 <= s <= 6), key=lambda s: stage_ms[s])
+    dom_stage = max((s for s in stage_ms if 1 <= s <= nst - 2), key=lambda s: stage_ms[s])
     dom_level = dom_stage - 1
     dom_ms = stage_ms[dom_stage] / args.steps
     dom_cells = stats["cells_per_level"][dom_level]
@@ -318,7 +321,8 @@ def main():
             traffic = tj.get(key)
         except (OSError, ValueError):
             traffic = None
-    level_names = ["window32", "window64", "window128", "window256", "window1024", "wide_cta"]
+    level_names = ["window32", "window64", "window128", "window256", "window512", "window1024",
+                   "wide_cta"]
     roofline = {"bound": "alu", "achieved": achieved_tops, "peak": peak_tops, "unit": "TOP/s",
                 "frac": achieved_tops / peak_tops, "traffic": traffic,
                 "kernel": f"k_window level {dom_level + 1} ({level_names[dom_level]})",
@@ -326,41 +330,57 @@ def main():
                 "ops_per_cell": N_REF_OPS_PER_CELL,
                 "peak_derivation": f"{B200_SMS} SMs x {ALU_LANES_PER_SM_CLK} int32 lanes/clk x {sm_max:.0f} MHz"}
 
-    # end-to-end through the host-buffer C-ABI entry point (pinned host memory)
+    # End-to-end through the host-buffer C-ABI entry point, from pinned host memory:
+    # every step copies its inputs in (H2D) and its results out (D2H) inside the timed
+    # region. Steps alternate between two arenas / streams (logan_xdrop_batch_host_async),
+    # so one step's copies overlap the previous step's sweep.
     e2e = None
     if not args.no_e2e:
         pool_np = batch.pool_2bit if fmt == logan.LOGAN_SEQ_2BIT else batch.pool_u8
         pin = lambda a: torch.from_numpy(np.ascontiguousarray(a)).pin_memory().numpy()
         hp = [pin(x) for x in (pool_np, batch.q_off, batch.q_len, batch.t_off, batch.t_len,
                                batch.q_seed, batch.t_seed)]
-        hout = torch.empty((n, 5), dtype=torch.int32).pin_memory().numpy()
-        hcells = torch.empty(n, dtype=torch.int64).pin_memory().numpy().view(np.uint64)
-        arena = logan.HostArena(n, batch.pool_len, fmt, db.max_ext_len, device=dev)
+        hout = [torch.empty((n, 5), dtype=torch.int32).pin_memory().numpy() for _ in range(2)]
+        hcells = [torch.empty(n, dtype=torch.int64).pin_memory().numpy().view(np.uint64) for _ in range(2)]
+        arenas = [logan.HostArena(n, batch.pool_len, fmt, db.max_ext_len, device=dev) for _ in range(2)]
+        streams = [torch.cuda.Stream(dev) for _ in range(2)]
         pool_bytes = (batch.pool_len + 3) // 4 if fmt == logan.LOGAN_SEQ_2BIT else batch.pool_len
 
-        def e2e_step():
+        def e2e_step(s):
             logan.xdrop_batch_host(hp[0], fmt, batch.pool_len, *hp[1:], w.k, w.match, w.mismatch,
-                                   w.gap, w.xdrop, arena, out=hout, cells=hcells, first_level=first,
-                                   stream=stream)
+                                   w.gap, w.xdrop, arenas[s % 2], out=hout[s % 2], cells=hcells[s % 2],
+                                   first_level=first, stream=streams[s % 2], asynchronous=True)
 
-        for _ in range(2):
-            e2e_step()
-        ke = max(3, min(args.steps, 10))
+        for s_ in range(2):
+            e2e_step(s_)
+        torch.cuda.synchronize()
+        ke = max(4, min(args.steps, 12))
         if world > 1:
             dist.barrier(device_ids=[local])
-        a0, a1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        a0.record(stream)
-        for _ in range(ke):
-            e2e_step()
-        a1.record(stream)
         torch.cuda.synchronize()
-        te = torch.tensor([a0.elapsed_time(a1)], dtype=torch.float64, device=dev)
+        a0 = torch.cuda.Event(enable_timing=True)
+        a0.record(streams[0])
+        streams[1].wait_event(a0)
+        for s_ in range(ke):
+            if s_ >= 2:
+                streams[s_ % 2].synchronize()  # step s-2's outputs are read before its buffers are reused
+                assert int(hcells[s_ % 2].sum()) == cells_step
+            e2e_step(s_)
+        ends = []
+        for st_ in streams:
+            ev = torch.cuda.Event(enable_timing=True)
+            ev.record(st_)
+            ends.append(ev)
+        torch.cuda.synchronize()
+        e2e_ms = max(a0.elapsed_time(ev) for ev in ends)
+        te = torch.tensor([e2e_ms], dtype=torch.float64, device=dev)
         if world > 1:
             dist.all_reduce(te, op=dist.ReduceOp.MAX)
-        assert int(hcells.sum()) == cells_step
+        for hc in hcells:
+            assert int(hc.sum()) == cells_step
         e2e = {"value": cells_all * ke / (float(te.item()) / 1e3) / 1e9, "unit": UNIT,
                "h2d_bytes_per_step": int(pool_bytes + 32 * n), "d2h_bytes_per_step": int(28 * n),
-               "steps": ke, "api": "logan_xdrop_batch_host"}
+               "steps": ke, "api": "logan_xdrop_batch_host_async (2 arenas / 2 streams, pinned)"}
 
     # CPU baseline: the oracle on this host's cores, rank 0 at N = 1 only
     cpu = None

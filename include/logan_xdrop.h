@@ -75,16 +75,16 @@ enum {
 };
 
 /* Options (may be passed as NULL = all defaults).
- *  first_level   : 0 = automatic from xdrop; 1..5 force the first
- *                  register-window level (windows of 32, 64, 128, 256, 1024
- *                  diagonal slots); 6 forces every task onto the unbounded CTA
- *                  level. Results never depend on it (tests assert this);
- *                  only speed does.
+ *  first_level   : 0 = automatic from xdrop; 1..6 force the first
+ *                  register-window level (windows of 32, 64, 128, 256, 512,
+ *                  1024 diagonal slots); 7 forces every task onto the
+ *                  unbounded CTA level. Results never depend on it (tests
+ *                  assert this); only speed does.
  *  timing_events : NULL, or LOGAN_N_STAGES * 2 cudaEvent_t created by the
  *                  caller (timing enabled). Event [2s] is recorded on `stream`
  *                  just before stage s and [2s+1] just after it, for every
  *                  stage the call launches: stage 0 = setup (task expansion,
- *                  LPT bucketing), stages 1..6 = levels 1..6, stage 7 =
+ *                  LPT bucketing), stages 1..7 = levels 1..7, stage 8 =
  *                  combine. Stages not launched leave their events untouched.
  *  flags         : bit 0 = run the first level in its latency shape (one
  *                  warp per task) instead of its throughput shape.
@@ -93,7 +93,7 @@ enum {
  *                  `handover` antidiagonals, exercising the exact hand-over.
  *                  Results never depend on it.
  */
-#define LOGAN_N_STAGES 8
+#define LOGAN_N_STAGES 9
 typedef struct {
     int32_t first_level;
     int32_t flags;
@@ -108,9 +108,9 @@ typedef struct {
  * there, the tasks that finished there and their band cells; window shifts
  * summed over all tasks. */
 typedef struct {
-    uint64_t tasks_started[6];
-    uint64_t tasks_finished[6];
-    uint64_t cells_per_level[6];
+    uint64_t tasks_started[8];   /* entries 0..6 used: levels 1..7 */
+    uint64_t tasks_finished[8];
+    uint64_t cells_per_level[8];
     uint64_t window_shifts;
     uint64_t cells_total;
 } logan_stats_t;
@@ -129,8 +129,8 @@ size_t logan_workspace_bytes(int64_t n_pairs, int64_t max_ext_len);
  * nothing, keeps no global state and is reentrant given distinct workspaces.
  *
  *  seq_pool   : the read pool, format `seq_fmt`, pool_len bases. The buffer
- *               must be 4-byte aligned and readable up to the next multiple
- *               of 16 bytes past its last byte (the kernels load whole words).
+ *               must be 4-byte aligned and readable for 16 bytes past its last
+ *               byte (the kernels load whole words and prefetch one ahead).
  *  q_off,t_off: int64[n_pairs] base offsets of query / target read in the pool
  *               (reads may be shared between pairs).
  *  q_len,t_len: int32[n_pairs] read lengths (bases), 0 <= len < 2^30.
@@ -181,6 +181,23 @@ int logan_xdrop_batch_host(const uint8_t *seq_pool, int32_t seq_fmt, int64_t poo
                            const logan_options_t *opt,
                            logan_result_t *out, uint64_t *cells,
                            void *device_arena, size_t arena_bytes, void *stream);
+
+/*
+ * Asynchronous variant of logan_xdrop_batch_host: enqueues the host->device
+ * copies, the sweep and the device->host copies on `stream` and returns without
+ * synchronising; `out` / `cells` are valid once `stream` has been synchronised.
+ * The host buffers must stay untouched until then (pinned memory makes the
+ * copies truly asynchronous). With two arenas on two streams a caller overlaps
+ * the copies of one batch with the sweep of the previous one.
+ */
+int logan_xdrop_batch_host_async(const uint8_t *seq_pool, int32_t seq_fmt, int64_t pool_len,
+                                 const int64_t *q_off, const int32_t *q_len,
+                                 const int64_t *t_off, const int32_t *t_len,
+                                 const int32_t *q_seed, const int32_t *t_seed,
+                                 int64_t n_pairs, int32_t k, logan_scoring_t sc,
+                                 const logan_options_t *opt,
+                                 logan_result_t *out, uint64_t *cells,
+                                 void *device_arena, size_t arena_bytes, void *stream);
 
 /* Human-readable text for a status code (static storage). */
 const char *logan_strerror(int status);

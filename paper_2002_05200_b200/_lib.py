@@ -18,7 +18,8 @@ LOGAN_OK, LOGAN_EINVAL, LOGAN_ECUDA, LOGAN_ENOSPC = 0, 1, 2, 3
 
 #: every symbol include/logan_xdrop.h declares
 EXPORTS = ("logan_workspace_bytes", "logan_xdrop_batch", "logan_host_arena_bytes",
-           "logan_xdrop_batch_host", "logan_strerror", "logan_abi_version")
+           "logan_xdrop_batch_host", "logan_xdrop_batch_host_async", "logan_strerror",
+           "logan_abi_version")
 
 
 class Scoring(ctypes.Structure):
@@ -26,7 +27,7 @@ class Scoring(ctypes.Structure):
                 ("gap", ctypes.c_int32), ("xdrop", ctypes.c_int32)]
 
 
-N_STAGES = 8  # LOGAN_N_STAGES: 0 setup, 1..6 levels, 7 combine
+N_STAGES = 9  # LOGAN_N_STAGES: 0 setup, 1..7 levels, 8 combine
 
 
 class Options(ctypes.Structure):
@@ -41,8 +42,8 @@ class Result(ctypes.Structure):
 
 
 class Stats(ctypes.Structure):
-    _fields_ = [("tasks_started", ctypes.c_uint64 * 6), ("tasks_finished", ctypes.c_uint64 * 6),
-                ("cells_per_level", ctypes.c_uint64 * 6), ("window_shifts", ctypes.c_uint64),
+    _fields_ = [("tasks_started", ctypes.c_uint64 * 8), ("tasks_finished", ctypes.c_uint64 * 8),
+                ("cells_per_level", ctypes.c_uint64 * 8), ("window_shifts", ctypes.c_uint64),
                 ("cells_total", ctypes.c_uint64)]
 
 
@@ -74,6 +75,8 @@ def load(path: str | None = None) -> ctypes.CDLL:
     lib.logan_xdrop_batch_host.argtypes = [vp, i32, i64, vp, vp, vp, vp, vp, vp, i64, i32, Scoring,
                                            ctypes.POINTER(Options), vp, vp, vp, sz, vp]
     lib.logan_xdrop_batch_host.restype = ctypes.c_int
+    lib.logan_xdrop_batch_host_async.argtypes = lib.logan_xdrop_batch_host.argtypes
+    lib.logan_xdrop_batch_host_async.restype = ctypes.c_int
     lib.logan_strerror.argtypes = [ctypes.c_int]
     lib.logan_strerror.restype = ctypes.c_char_p
     lib.logan_abi_version.argtypes = []

@@ -139,8 +139,8 @@ def new_stats(device=None):
 
 def stats_dict(stats_tensor) -> dict:
     v = [int(x) for x in stats_tensor.cpu().tolist()]
-    return {"tasks_started": v[0:6], "tasks_finished": v[6:12], "cells_per_level": v[12:18],
-            "window_shifts": v[18], "cells_total": v[19]}
+    return {"tasks_started": v[0:7], "tasks_finished": v[8:15], "cells_per_level": v[16:23],
+            "window_shifts": v[24], "cells_total": v[25]}
 
 
 class HostArena:
@@ -158,8 +158,13 @@ class HostArena:
 def xdrop_batch_host(pool: np.ndarray, fmt: int, pool_len: int, q_off, q_len, t_off, t_len,
                      q_seed, t_seed, k: int, match: int, mismatch: int, gap: int, xdrop: int,
                      arena: HostArena, out: np.ndarray | None = None,
-                     cells: np.ndarray | None = None, first_level: int | None = None, stream=None):
-    """End-to-end call with HOST buffers (numpy; pinned memory copies fastest)."""
+                     cells: np.ndarray | None = None, first_level: int | None = None, stream=None,
+                     asynchronous: bool = False):
+    """End-to-end call with HOST buffers (numpy; pinned memory copies fastest).
+
+    ``asynchronous=True`` returns right after enqueuing (``logan_xdrop_batch_host_async``):
+    the outputs are valid once ``stream`` is synchronised and the inputs must stay alive
+    until then."""
     torch = _require_cuda()
     lib = _lib.load()
     n = len(q_len)
@@ -168,12 +173,15 @@ def xdrop_batch_host(pool: np.ndarray, fmt: int, pool_len: int, q_off, q_len, t_
     if cells is None:
         cells = np.empty(n, np.uint64)
     arrs = [np.ascontiguousarray(a) for a in (q_off, q_len, t_off, t_len, q_seed, t_seed)]
+    if asynchronous and any(a is not b for a, b in zip(arrs, (q_off, q_len, t_off, t_len, q_seed, t_seed))):
+        raise ValueError("asynchronous host calls need C-contiguous numpy inputs (they must outlive the call)")
     if stream is None:
         stream = torch.cuda.current_stream()
     sc = _lib.Scoring(match, mismatch, gap, xdrop)
     ptr = lambda a: a.ctypes.data
-    st = lib.logan_xdrop_batch_host(ptr(pool), fmt, pool_len, *[ptr(a) for a in arrs], n, k, sc,
-                                    _opts(first_level), ptr(out), ptr(cells),
-                                    arena.tensor.data_ptr(), arena.nbytes, stream.cuda_stream)
+    fn = lib.logan_xdrop_batch_host_async if asynchronous else lib.logan_xdrop_batch_host
+    st = fn(ptr(pool), fmt, pool_len, *[ptr(a) for a in arrs], n, k, sc,
+            _opts(first_level), ptr(out), ptr(cells),
+            arena.tensor.data_ptr(), arena.nbytes, stream.cuda_stream)
     _lib.check(st)
     return out, cells

@@ -24,7 +24,7 @@
 namespace logan {
 
 constexpr int NBUCKET = 2048;
-constexpr int NLEVEL = 6;  // 5 window levels + the wide level
+constexpr int NLEVEL = 7;  // 6 window levels + the wide level
 constexpr int SETUP_THREADS = 256;
 
 __device__ __forceinline__ uint32_t cost_bucket(uint32_t c) {
@@ -35,16 +35,18 @@ __device__ __forceinline__ uint32_t cost_bucket(uint32_t c) {
 }
 
 // Workspace layout (each region 256-byte aligned).
-// First-level window (G = 1 lane x LOGAN_L0_R slots); tuned by measurement.
+// First-level window (G = 1 lane x LOGAN_L0_R slots); tuned by measurement on
+// C2 (X = 20): 28 slots + throughput-shape helpers beat 32 slots by ~2.5%
+// (about 1% of tasks overflow and finish inside the first kernel).
 #ifndef LOGAN_L0_R
-#define LOGAN_L0_R 32
+#define LOGAN_L0_R 28
 #endif
-constexpr int NWIDTH = 5;  // register-window widths L0, 64, 128, 256, 1024
-static const int kWidth[NWIDTH] = {LOGAN_L0_R, 64, 128, 256, 1024};
+constexpr int NWIDTH = 6;  // register-window widths L0, 64, 128, 256, 512, 1024
+static const int kWidth[NWIDTH] = {LOGAN_L0_R, 64, 128, 256, 512, 1024};
 
 struct Layout {
     size_t tres, tbucket, queue, listA, listB, recsA, recsB, hist, cursor_b, counters, wide, total;
-    size_t pool[NWIDTH - 1];     // hand-over records written by width level w (w < 4)
+    size_t pool[NWIDTH - 1];     // hand-over records written by width level w (w < NWIDTH-1)
     uint32_t pool_cap[NWIDTH - 1];
     int64_t ntask, wide_stride;
 };
@@ -192,12 +194,27 @@ __global__ void k_combine(const Params P, const TaskRes *tres, logan_result_t *o
 // Throughput shape: G = W/32 lanes x R = 32 slots (many tasks in flight).
 // Latency shape: one warp per task, R = W/32 slots per lane (few tasks left:
 // the step's critical path is short). Level 5 is the unbounded CTA path.
-template <int G, int R, int FMT, int HR>
+// Helper shape for the first level: the next width's throughput shape (many
+// tasks per helper warp, default) or its latency shape (one warp per task);
+// LOGAN_HELPER_WARPS warps (the last warp of as many blocks) are helpers.
+#ifndef LOGAN_HELPER_THROUGHPUT
+#define LOGAN_HELPER_THROUGHPUT 1
+#endif
+#ifndef LOGAN_HELPER_WARPS
+#define LOGAN_HELPER_WARPS 96
+#endif
+#if LOGAN_HELPER_THROUGHPUT
+#define LOGAN_HSHAPE(W) ((W) / 32), 32
+#else
+#define LOGAN_HSHAPE(W) 32, ((W) / 32)
+#endif
+
+template <int G, int R, int FMT, int HG, int HR>
 static cudaError_t launch_win(const Params &P, const LevelIO &io_in, const LevelIO &hio, int sms, cudaStream_t s) {
     constexpr int S1 = Window<G, R, FMT>::SB_STRIDE;
-    constexpr int S2 = HR > 0 ? Window<32, (HR > 0 ? HR : 1), FMT>::SB_STRIDE : 0;
+    constexpr int S2 = HR > 0 ? Window<(HG > 0 ? HG : 32), (HR > 0 ? HR : 1), FMT>::SB_STRIDE : 0;
     const size_t smem = 128 * sizeof(int32_t) * (S1 > S2 ? S1 : S2);
-    auto kern = k_window<G, R, FMT, HR>;
+    auto kern = k_window<G, R, FMT, HG, HR>;
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return e;
     int occ = 0;
@@ -207,7 +224,7 @@ static cudaError_t launch_win(const Params &P, const LevelIO &io_in, const Level
     const int grid = sms * occ;
     LevelIO io = io_in;
     if (HR > 0) {
-        io.helpers = grid < 32 ? grid : 32;
+        io.helpers = grid < LOGAN_HELPER_WARPS ? grid : LOGAN_HELPER_WARPS;
         io.workers = (uint32_t)((grid * 128 - io.helpers * 32) / G);
     } else {
         io.helpers = 0;
@@ -217,43 +234,47 @@ static cudaError_t launch_win(const Params &P, const LevelIO &io_in, const Level
 }
 
 // wi = width index; latency = run the latency shape; helpers = first level with
-// in-kernel escalation helpers running the next width's latency shape
+// in-kernel escalation helpers running the next width
 template <int FMT>
 static cudaError_t launch_width(int wi, bool latency, bool helpers, const Params &P, const LevelIO &io,
                                 const LevelIO &hio, int sms, cudaStream_t s) {
     if (helpers && !latency) {
         switch (wi) {
-            case 0: return launch_win<1, LOGAN_L0_R, FMT, 2>(P, io, hio, sms, s);
-            case 1: return launch_win<2, 32, FMT, 4>(P, io, hio, sms, s);
-            case 2: return launch_win<4, 32, FMT, 8>(P, io, hio, sms, s);
-            case 3: return launch_win<8, 32, FMT, 32>(P, io, hio, sms, s);
+            case 0: return launch_win<1, LOGAN_L0_R, FMT, LOGAN_HSHAPE(64)>(P, io, hio, sms, s);
+            case 1: return launch_win<2, 32, FMT, LOGAN_HSHAPE(128)>(P, io, hio, sms, s);
+            case 2: return launch_win<4, 32, FMT, LOGAN_HSHAPE(256)>(P, io, hio, sms, s);
+            case 3: return launch_win<8, 32, FMT, LOGAN_HSHAPE(512)>(P, io, hio, sms, s);
+            case 4: return launch_win<16, 32, FMT, 32, 32>(P, io, hio, sms, s);
             default: break;
         }
     }
     switch (wi * 2 + (latency ? 1 : 0)) {
-        case 0: return launch_win<1, LOGAN_L0_R, FMT, 0>(P, io, hio, sms, s);
-        case 1: return LOGAN_L0_R == 32 ? launch_win<32, 1, FMT, 0>(P, io, hio, sms, s)
-                                        : launch_win<1, LOGAN_L0_R, FMT, 0>(P, io, hio, sms, s);
-        case 2: return launch_win<2, 32, FMT, 0>(P, io, hio, sms, s);
-        case 3: return launch_win<32, 2, FMT, 0>(P, io, hio, sms, s);
-        case 4: return launch_win<4, 32, FMT, 0>(P, io, hio, sms, s);
-        case 5: return launch_win<32, 4, FMT, 0>(P, io, hio, sms, s);
-        case 6: return launch_win<8, 32, FMT, 0>(P, io, hio, sms, s);
-        case 7: return launch_win<32, 8, FMT, 0>(P, io, hio, sms, s);
-        case 8:
-        case 9: return launch_win<32, 32, FMT, 0>(P, io, hio, sms, s);
+        case 0: return launch_win<1, LOGAN_L0_R, FMT, 0, 0>(P, io, hio, sms, s);
+        case 1: return LOGAN_L0_R == 32 ? launch_win<32, 1, FMT, 0, 0>(P, io, hio, sms, s)
+                                        : launch_win<1, LOGAN_L0_R, FMT, 0, 0>(P, io, hio, sms, s);
+        case 2: return launch_win<2, 32, FMT, 0, 0>(P, io, hio, sms, s);
+        case 3: return launch_win<32, 2, FMT, 0, 0>(P, io, hio, sms, s);
+        case 4: return launch_win<4, 32, FMT, 0, 0>(P, io, hio, sms, s);
+        case 5: return launch_win<32, 4, FMT, 0, 0>(P, io, hio, sms, s);
+        case 6: return launch_win<8, 32, FMT, 0, 0>(P, io, hio, sms, s);
+        case 7: return launch_win<32, 8, FMT, 0, 0>(P, io, hio, sms, s);
+        case 8: return launch_win<16, 32, FMT, 0, 0>(P, io, hio, sms, s);
+        case 9: return launch_win<32, 16, FMT, 0, 0>(P, io, hio, sms, s);
+        case 10:
+        case 11: return launch_win<32, 32, FMT, 0, 0>(P, io, hio, sms, s);
         default: return cudaErrorInvalidValue;
     }
 }
 
 static int auto_first_level(int32_t xdrop) {
-    // band width is about X + a few slots for true pairs
-    if (xdrop <= 20) return 0;   // W = 32
-    if (xdrop <= 48) return 1;   // W = 64
+    // the band of true pairs is about X + a few slots wide
+    if (xdrop <= 20) return 0;   // W = LOGAN_L0_R (28)
+    if (xdrop <= 50) return 1;   // W = 64
     if (xdrop <= 110) return 2;  // W = 128
     if (xdrop <= 230) return 3;  // W = 256
-    if (xdrop <= 1000) return 4; // W = 1024
-    return 5;                    // wide
+    if (xdrop <= 480) return 4;  // W = 512
+    if (xdrop <= 1000) return 5; // W = 1024
+    return 6;                    // unbounded CTA level
 }
 
 template <int FMT>
@@ -295,7 +316,7 @@ static int run_batch(const Params &P, const logan_options_t *opt, logan_result_t
     if (!mark(0, 1)) return LOGAN_ECUDA;
 
     int first = (opt && opt->first_level > 0) ? opt->first_level - 1 : auto_first_level(P.xdrop);
-    if (first < 0 || first > 5) return LOGAN_EINVAL;
+    if (first < 0 || first > NLEVEL - 1) return LOGAN_EINVAL;
     uint32_t *recs[2] = {(uint32_t *)(ws + L.recsA), (uint32_t *)(ws + L.recsB)};
     const uint32_t *in_list = queue;
     const uint32_t *in_recs = nullptr;
@@ -376,10 +397,10 @@ static int run_batch(const Params &P, const logan_options_t *opt, logan_result_t
     int grid3 = (int)((P.n_pairs + per_block - 1) / per_block);
     if (grid3 > sms * 8) grid3 = sms * 8;
     if (grid3 < 1) grid3 = 1;
-    if (!mark(7, 0)) return LOGAN_ECUDA;
+    if (!mark(LOGAN_N_STAGES - 1, 0)) return LOGAN_ECUDA;
     k_combine<FMT><<<grid3, SETUP_THREADS, 0, s>>>(P, tres, out, cells);
     if (cudaGetLastError() != cudaSuccess) return LOGAN_ECUDA;
-    if (!mark(7, 1)) return LOGAN_ECUDA;
+    if (!mark(LOGAN_N_STAGES - 1, 1)) return LOGAN_ECUDA;
     return LOGAN_OK;
 }
 
@@ -416,7 +437,7 @@ static int check_args(const uint8_t *seq_pool, int32_t seq_fmt, int64_t pool_len
     if (sc.match <= 0 || sc.match > 127 || sc.mismatch >= 0 || sc.mismatch < -127 || sc.gap >= 0 ||
         sc.gap < -127 || sc.xdrop < 0 || sc.xdrop > (1 << 19))
         return LOGAN_EINVAL;
-    if (opt && (opt->first_level < 0 || opt->first_level > 6)) return LOGAN_EINVAL;
+    if (opt && (opt->first_level < 0 || opt->first_level > 7)) return LOGAN_EINVAL;
     if (n_pairs == 0) return LOGAN_OK;
     if (!seq_pool || !q_off || !q_len || !t_off || !t_len || !q_seed || !t_seed || !out) return LOGAN_EINVAL;
     if (((uintptr_t)seq_pool & 3) != 0) return LOGAN_EINVAL;
@@ -439,8 +460,10 @@ int logan_xdrop_batch(const uint8_t *seq_pool, int32_t seq_fmt, int64_t pool_len
     if (workspace_bytes < base.total) return LOGAN_ENOSPC;
     const size_t per_col = sizeof(int32_t) * 3 * WIDE_CTAS;
     int64_t max_ext = (int64_t)((workspace_bytes - base.total) / per_col);
+    // alignment padding makes the estimate approximate: take the largest bound that fits
+    while (make_layout(n_pairs, max_ext + 1).total <= workspace_bytes) ++max_ext;
+    while (max_ext > 0 && make_layout(n_pairs, max_ext).total > workspace_bytes) --max_ext;
     Layout L = make_layout(n_pairs, max_ext);
-    while (L.total > workspace_bytes && max_ext > 0) L = make_layout(n_pairs, --max_ext);
     if (L.total > workspace_bytes) return LOGAN_ENOSPC;
 
     Params P;
@@ -477,11 +500,38 @@ size_t logan_host_arena_bytes(int64_t n_pairs, int64_t pool_len, int32_t seq_fmt
     return o;
 }
 
+static int host_batch(const uint8_t *seq_pool, int32_t seq_fmt, int64_t pool_len, const int64_t *q_off,
+                      const int32_t *q_len, const int64_t *t_off, const int32_t *t_len, const int32_t *q_seed,
+                      const int32_t *t_seed, int64_t n_pairs, int32_t k, logan_scoring_t sc,
+                      const logan_options_t *opt, logan_result_t *out, uint64_t *cells, void *device_arena,
+                      size_t arena_bytes, void *stream, bool sync);
+
 int logan_xdrop_batch_host(const uint8_t *seq_pool, int32_t seq_fmt, int64_t pool_len, const int64_t *q_off,
                            const int32_t *q_len, const int64_t *t_off, const int32_t *t_len,
                            const int32_t *q_seed, const int32_t *t_seed, int64_t n_pairs, int32_t k,
                            logan_scoring_t sc, const logan_options_t *opt, logan_result_t *out,
                            uint64_t *cells, void *device_arena, size_t arena_bytes, void *stream) {
+    return host_batch(seq_pool, seq_fmt, pool_len, q_off, q_len, t_off, t_len, q_seed, t_seed, n_pairs, k, sc,
+                      opt, out, cells, device_arena, arena_bytes, stream, true);
+}
+
+int logan_xdrop_batch_host_async(const uint8_t *seq_pool, int32_t seq_fmt, int64_t pool_len,
+                                 const int64_t *q_off, const int32_t *q_len, const int64_t *t_off,
+                                 const int32_t *t_len, const int32_t *q_seed, const int32_t *t_seed,
+                                 int64_t n_pairs, int32_t k, logan_scoring_t sc, const logan_options_t *opt,
+                                 logan_result_t *out, uint64_t *cells, void *device_arena, size_t arena_bytes,
+                                 void *stream) {
+    return host_batch(seq_pool, seq_fmt, pool_len, q_off, q_len, t_off, t_len, q_seed, t_seed, n_pairs, k, sc,
+                      opt, out, cells, device_arena, arena_bytes, stream, false);
+}
+
+}  // extern "C"
+
+static int host_batch(const uint8_t *seq_pool, int32_t seq_fmt, int64_t pool_len, const int64_t *q_off,
+                      const int32_t *q_len, const int64_t *t_off, const int32_t *t_len, const int32_t *q_seed,
+                      const int32_t *t_seed, int64_t n_pairs, int32_t k, logan_scoring_t sc,
+                      const logan_options_t *opt, logan_result_t *out, uint64_t *cells, void *device_arena,
+                      size_t arena_bytes, void *stream, bool sync) {
     int st = check_args(seq_pool, seq_fmt, pool_len, q_off, q_len, t_off, t_len, q_seed, t_seed, n_pairs, k,
                         sc, opt, out);
     if (st != LOGAN_OK) return st;
@@ -520,8 +570,6 @@ int logan_xdrop_batch_host(const uint8_t *seq_pool, int32_t seq_fmt, int64_t poo
     if (cells && cudaMemcpyAsync(cells, d_cells, sizeof(uint64_t) * (size_t)n_pairs, cudaMemcpyDeviceToHost, s) !=
                      cudaSuccess)
         return LOGAN_ECUDA;
-    if (cudaStreamSynchronize(s) != cudaSuccess) return LOGAN_ECUDA;
+    if (sync && cudaStreamSynchronize(s) != cudaSuccess) return LOGAN_ECUDA;
     return LOGAN_OK;
 }
-
-}  // extern "C"

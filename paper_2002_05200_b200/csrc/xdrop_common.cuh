@@ -154,27 +154,31 @@ __device__ __forceinline__ uint32_t seq_at(const Params &P, const SeqRef &s, int
 // the next base and the word after it are kept in registers; crossing a word
 // boundary shifts them down and issues the load of the following word, whose
 // latency is hidden until the next boundary (16 bases later for 2-bit).
-// seek() repositions the reader anywhere (blocking loads; rare: task start
-// and window shifts).
+// The common path is a shift, a mask and two compares; word addresses are plain
+// pointers (the ABI guarantees 16 readable bytes past the pool's end, so a
+// forward prefetch never needs a bound; a backward one stops at the pool start).
+// seek() repositions the reader anywhere (blocking loads; rare: task start,
+// resume and window shifts).
 template <int FMT>
 struct Stream {
     using F = PoolFmt<FMT>;
     static constexpr int CPW = 1 << F::LOG_CPW;
     SeqRef s;
-    int64_t wi;    // word index of `cur` (position of index max(idx,1))
-    uint32_t cur;  // word holding the base at index max(idx, 1)
-    uint32_t nxt;  // the next word in the direction of travel
-    int32_t idx;   // extension index returned by the next next()
-    int32_t sh;    // bit offset of that base inside cur
+    const uint32_t *wp;  // word holding the base at index max(idx, 1)
+    uint32_t cur;        // *wp
+    uint32_t nxt;        // wp[dir] (prefetched)
+    int32_t idx;         // extension index returned by the next next()
+    int32_t sh;          // bit offset of that base inside cur
 
     __device__ __forceinline__ void seek(const Params &P, int32_t i) {
         idx = i;
         const int32_t c = (i < 1 || s.len <= 0) ? 1 : (i > s.len ? s.len : i);
         const int64_t pos = s.base + (int64_t)s.dir * (c - 1);
-        wi = pos >> F::LOG_CPW;
+        const int64_t wi = pos >> F::LOG_CPW;
         sh = F::BITS * (int32_t)(pos & (CPW - 1));
-        cur = pool_word(P, wi);
-        nxt = pool_word(P, wi + s.dir);
+        wp = P.pool + (wi < 0 ? 0 : (wi >= P.pool_words ? P.pool_words - 1 : wi));
+        cur = __ldg(wp);
+        nxt = (s.dir < 0 && wp == P.pool) ? 0u : __ldg(wp + s.dir);
     }
 
     __device__ __forceinline__ uint32_t next(const Params &P, uint32_t sent) {
@@ -183,11 +187,11 @@ struct Stream {
         const uint32_t c = (cur >> sh) & F::MASK;
         if (i < s.len) {  // advance to index i + 1
             sh += s.dir * F::BITS;
-            if ((uint32_t)sh >= 32u) {  // crossed a word boundary
+            if ((uint32_t)sh >= 32u) {  // crossed a word boundary (once per CPW bases)
                 sh -= s.dir * 32;
-                wi += s.dir;
+                wp += s.dir;
                 cur = nxt;
-                nxt = pool_word(P, wi + s.dir);  // prefetch
+                nxt = (s.dir < 0 && wp == P.pool) ? 0u : __ldg(wp + s.dir);  // prefetch
             }
         }
         return c;

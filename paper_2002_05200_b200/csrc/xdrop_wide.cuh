@@ -6,28 +6,30 @@
 //
 // This is the paper's own intra-sequence scheme, kept only as the exact
 // fallback for tasks whose band outgrows the widest register window (1024
-// diagonal slots): e.g. unrelated reads at large X (c-amb-17). Values are
+// diagonal slots): e.g. long unrelated reads at large X (c-amb-17). Values are
 // absolute int32 with an explicit dead marker; a column outside the range
 // visited on an antidiagonal is dead (it had no live predecessor).
+//
+// Per antidiagonal: each thread sweeps its cells, warps reduce with CREDUX
+// (max value, then smallest i at that value; smallest / largest live i), lane
+// 0 of every warp writes its partials to a parity-double-buffered shared slot,
+// ONE __syncthreads, then every warp folds the 32 partials with one LDS per lane
+// and CREDUX (no second barrier: the next antidiagonal writes the other
+// parity's slots).
 #pragma once
 
 #include "xdrop_common.cuh"
 
 namespace logan {
 
-constexpr int WIDE_THREADS = 256;
+constexpr int WIDE_THREADS = 1024;
+constexpr int WIDE_WARPS = WIDE_THREADS / 32;
 constexpr int32_t WDEAD = INT32_MIN;
-
-__device__ __forceinline__ unsigned long long wide_key(int32_t v, int32_t i) {
-    // max over keys = max value, then smallest i
-    return ((unsigned long long)((uint32_t)v ^ 0x80000000u) << 32) | (uint32_t)(~(uint32_t)i);
-}
 
 template <int FMT>
 __global__ void __launch_bounds__(WIDE_THREADS) k_wide(const Params P, const LevelIO io,
                                                        int32_t *scratch, int64_t stride) {
-    __shared__ unsigned long long s_key[WIDE_THREADS / 32];
-    __shared__ int32_t s_f[WIDE_THREADS / 32], s_l[WIDE_THREADS / 32];
+    __shared__ int32_t s_v[2][WIDE_WARPS], s_i[2][WIDE_WARPS], s_f[2][WIDE_WARPS], s_l[2][WIDE_WARPS];
     __shared__ uint32_t s_task;
     const int tid = threadIdx.x, wid = tid >> 5, lane = tid & 31;
     int32_t *V[3] = {scratch + (int64_t)blockIdx.x * 3 * stride,
@@ -54,45 +56,39 @@ __global__ void __launch_bounds__(WIDE_THREADS) k_wide(const Params P, const Lev
             continue;
         }
 
-        // per-antidiagonal bookkeeping (uniform across the block)
-        int32_t vis_lo[3] = {0, 0, 0}, vis_hi[3] = {-1, -1, -1};
-        int32_t F[3] = {0, 0, 0}, L[3] = {0, 0, 0};
-        bool has[3] = {false, false, false};
-        if (tid == 0) V[0][0] = 0;  // origin S(0,0) = 0
-        vis_lo[0] = vis_hi[0] = 0;
-        F[0] = L[0] = 0;
-        has[0] = true;
+        // per-antidiagonal bookkeeping (uniform across the block), rotated
+        // scalars for d-1 ("1") and d-2 ("2"); buffers rotate through V[]
+        int32_t lo1 = 0, hi1 = 0, F1 = 0, L1 = 0;  // antidiagonal 0: the origin
+        bool h1 = true;
+        int32_t lo2 = 0, hi2 = -1, F2 = 0, L2 = 0;
+        bool h2 = false;
+        int32_t *V0 = V[1], *V1 = V[0], *V2 = V[2];
+        if (tid == 0) V1[0] = 0;  // origin S(0,0) = 0
         int32_t best = 0, ai = 0, aj = 0;
         uint64_t cells = 0;
         __syncthreads();
 
         for (int32_t d = 1;; ++d) {
-            const int c = d % 3, c1 = (d + 2) % 3, c2 = (d + 1) % 3;
-            const bool h1 = has[c1], h2 = (d >= 2) && has[c2];
             // band and visiting range (cells with a possibly live predecessor)
             int32_t lo = INT32_MAX, hi = INT32_MIN;
-            if (h1) { lo = min(lo, F[c1]); hi = max(hi, L[c1] + 1); }
-            if (h2) { lo = min(lo, F[c2] + 1); hi = max(hi, L[c2] + 1); }
+            if (h1) { lo = min(lo, F1); hi = max(hi, L1 + 1); }
+            if (h2) { lo = min(lo, F2 + 1); hi = max(hi, L2 + 1); }
             if (d >= 2 && (h1 || h2)) {
                 const int32_t blo = max(lo, max(1, d - n)), bhi = min(hi, min(m, d - 1));
                 if (bhi >= blo) cells += (uint64_t)(bhi - blo + 1);
             }
             const int32_t vlo = max(lo, max(0, d - n)), vhi = min(hi, min(m, d));
             const int32_t thr = best - P.xdrop;
-            unsigned long long kbest = 0;
-            int32_t lf = INT32_MAX, ll = INT32_MIN;
-            const int32_t *V1 = V[c1], *V2 = V[c2];
-            int32_t *V0 = V[c];
-            const int32_t lo1 = vis_lo[c1], hi1 = vis_hi[c1], lo2 = vis_lo[c2], hi2 = vis_hi[c2];
+            int32_t bv = INT32_MIN, bi = INT32_MAX, lf = INT32_MAX, ll = INT32_MIN;
             for (int32_t i = vlo + tid; i <= vhi; i += WIDE_THREADS) {
                 const int32_t j = d - i;
                 bool have = false;
                 int32_t v = 0;
-                if (i >= 1 && j >= 1 && d >= 2 && i - 1 >= lo2 && i - 1 <= hi2) {
+                if (i >= 1 && j >= 1 && h2 && i - 1 >= lo2 && i - 1 <= hi2) {
                     const int32_t p = V2[i - 1];
                     if (p != WDEAD) {
-                        const uint32_t a = seq_at<FMT>(P, td.a, i, 0xffffffffu);
-                        const uint32_t b = seq_at<FMT>(P, td.b, j, 0xfffffffeu);
+                        const uint32_t a = pool_base<FMT>(P, td.a.base + (int64_t)td.a.dir * (i - 1));
+                        const uint32_t b = pool_base<FMT>(P, td.b.base + (int64_t)td.b.dir * (j - 1));
                         v = p + (a == b ? P.match : P.mismatch);
                         have = true;
                     }
@@ -110,41 +106,31 @@ __global__ void __launch_bounds__(WIDE_THREADS) k_wide(const Params P, const Lev
                 if (live) {
                     lf = min(lf, i);
                     ll = max(ll, i);
-                    const unsigned long long key = wide_key(v, i);
-                    kbest = key > kbest ? key : kbest;
+                    if (v > bv) { bv = v; bi = i; }  // ascending i: the first max is kept
                 }
             }
-            // block reductions
-#pragma unroll
-            for (int o = 16; o > 0; o >>= 1) {
-                const unsigned long long ok = __shfl_xor_sync(0xffffffffu, kbest, o);
-                kbest = ok > kbest ? ok : kbest;
-            }
-            lf = __reduce_min_sync(0xffffffffu, lf);
-            ll = __reduce_max_sync(0xffffffffu, ll);
-            if (lane == 0) { s_key[wid] = kbest; s_f[wid] = lf; s_l[wid] = ll; }
+            // warp reductions: max value, then the smallest i holding it
+            const int32_t wv = __reduce_max_sync(0xffffffffu, bv);
+            const int32_t wi = __reduce_min_sync(0xffffffffu, bv == wv ? bi : INT32_MAX);
+            const int32_t wf = __reduce_min_sync(0xffffffffu, lf);
+            const int32_t wl = __reduce_max_sync(0xffffffffu, ll);
+            const int par = d & 1;
+            if (lane == 0) { s_v[par][wid] = wv; s_i[par][wid] = wi; s_f[par][wid] = wf; s_l[par][wid] = wl; }
             __syncthreads();  // also orders the V0 writes before the next antidiagonal
-            kbest = 0;
-            lf = INT32_MAX;
-            ll = INT32_MIN;
-#pragma unroll
-            for (int q = 0; q < WIDE_THREADS / 32; ++q) {
-                kbest = s_key[q] > kbest ? s_key[q] : kbest;
-                lf = min(lf, s_f[q]);
-                ll = max(ll, s_l[q]);
-            }
-            __syncthreads();
-            vis_lo[c] = vlo;
-            vis_hi[c] = vhi;
-            has[c] = (lf != INT32_MAX);
-            F[c] = lf;
-            L[c] = ll;
-            if (kbest != 0) {
-                const int32_t v = (int32_t)((uint32_t)(kbest >> 32) ^ 0x80000000u);
-                const int32_t i = (int32_t)(~(uint32_t)kbest);
-                if (v > best) { best = v; ai = i; aj = d - i; }  // P:178, strict increase
-            }
-            if (!has[c] && !has[c1]) break;  // P:186, c-amb-7
+            // every warp folds the 32 partials the same way: lane q reads warp
+            // q's slot (one LDS each) and CREDUX combines them
+            const int32_t qv = s_v[par][lane], qi = s_i[par][lane];
+            const int32_t gv = __reduce_max_sync(0xffffffffu, qv);
+            const int32_t gi = __reduce_min_sync(0xffffffffu, qv == gv ? qi : INT32_MAX);
+            const int32_t gf = __reduce_min_sync(0xffffffffu, s_f[par][lane]);
+            const int32_t gl = __reduce_max_sync(0xffffffffu, s_l[par][lane]);
+            const bool h0 = (gf != INT32_MAX);
+            if (h0 && gv > best) { best = gv; ai = gi; aj = d - gi; }  // P:178, strict increase
+            if (!h0 && !h1) break;  // P:186, c-amb-7
+            // rotate: d becomes "1", d-1 becomes "2"
+            lo2 = lo1; hi2 = hi1; F2 = F1; L2 = L1; h2 = h1;
+            lo1 = vlo; hi1 = vhi; F1 = gf; L1 = gl; h1 = h0;
+            int32_t *t = V2; V2 = V1; V1 = V0; V0 = t;
         }
         if (tid == 0) {
             TaskRes tr;
@@ -161,6 +147,7 @@ __global__ void __launch_bounds__(WIDE_THREADS) k_wide(const Params P, const Lev
                 atomicAdd((unsigned long long *)&io.stats->cells_total, (unsigned long long)cells);
             }
         }
+        __syncthreads();  // both parities' slots are reused by the next task
     }
 }
 

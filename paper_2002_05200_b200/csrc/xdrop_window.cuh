@@ -56,6 +56,12 @@ constexpr int32_t KEYMUL = 1027;
 
 // How many of the 4 sign-mask chains run on the FMA pipe (the rest use SHF on
 // the ALU pipe): balances the two pipes (tuned by measurement).
+// Minimum resident blocks per SM requested for the one-lane-per-task kernels
+// (caps registers; tuned by measurement).
+#ifndef LOGAN_L0_MINB
+#define LOGAN_L0_MINB 1
+#endif
+
 #ifndef LOGAN_MASK_FMA_CHAINS
 #define LOGAN_MASK_FMA_CHAINS 0
 #endif
@@ -535,7 +541,10 @@ __device__ __forceinline__ void run_group(Win &w, const Params &P, const LevelIO
         } else {
             rc = w.template step<0>(P);
         }
-        if (io.handover > 0 && rc == 0 && io.rec_out && (since += 2) >= io.handover) rc = 2;
+        if (io.handover > 0) {  // test knob (uniform branch, off in production)
+            since += 2;
+            if (rc == 0 && io.rec_out && since >= io.handover) rc = 2;
+        }
         if (rc != 0) {
             uint32_t rec = NO_REC;
             if (rc == 2 && io.rec_out) {  // hand the exact state to the next level
@@ -593,8 +602,9 @@ __device__ __forceinline__ void run_group(Win &w, const Params &P, const LevelIO
 // overflowing tasks then finish while this level is still running instead of
 // forming a serial tail after it. What the helpers do not take, the next
 // level's own launch does (it shares their cursor).
-template <int G, int R, int FMT, int HR>
-__global__ void __launch_bounds__(128) k_window(const Params P, const LevelIO io, const LevelIO hio) {
+template <int G, int R, int FMT, int HG, int HR>
+__global__ void __launch_bounds__(128, (G == 1 ? LOGAN_L0_MINB : 1))
+    k_window(const Params P, const LevelIO io, const LevelIO hio) {
     const uint32_t count = *io.count;
     const uint32_t taken = *io.cursor;  // entries already taken (by in-kernel helpers)
     const uint32_t remaining = count - (taken < count ? taken : count);
@@ -603,10 +613,12 @@ __global__ void __launch_bounds__(128) k_window(const Params P, const LevelIO io
     const int lane = threadIdx.x & 31;
     const bool helper = HR > 0 && (int)blockIdx.x < io.helpers && (threadIdx.x >> 5) == (blockDim.x >> 5) - 1;
     if (HR > 0 && helper) {
-        Window<32, (HR > 0 ? HR : 1), FMT> w;
-        w.sbase = win_smem + threadIdx.x * Window<32, (HR > 0 ? HR : 1), FMT>::SB_STRIDE;
-        w.gl = lane;
-        w.gmask = 0xffffffffu;
+        constexpr int HG_ = HG > 0 ? HG : 32, HR_ = HR > 0 ? HR : 1;
+        Window<HG_, HR_, FMT> w;
+        w.sbase = win_smem + threadIdx.x * Window<HG_, HR_, FMT>::SB_STRIDE;
+        w.gl = lane % HG_;
+        w.gmask = (HG_ == 32) ? 0xffffffffu : (((1u << HG_) - 1u) << (lane - w.gl));
+        const int leader = lane - w.gl;
         const uint32_t total = io.workers;
         // Helpers only work while producers are still sweeping: once every
         // producer group is done they stop taking entries, and whatever is left
@@ -618,8 +630,8 @@ __global__ void __launch_bounds__(128) k_window(const Params P, const LevelIO io
                 __nanosleep(1000);
             }
             uint32_t p = 0;
-            if (lane == 0) p = atomicAdd(hio.cursor, 1u);
-            p = __shfl_sync(0xffffffffu, p, 0);
+            if (w.gl == 0) p = atomicAdd(hio.cursor, 1u);
+            if (HG_ > 1) p = __shfl_sync(w.gmask, p, leader);
             // a claimed position is either processed here or proven not to exist
             for (;;) {
                 if (p < *(volatile const uint32_t *)io.out_count) break;

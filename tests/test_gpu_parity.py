@@ -63,7 +63,7 @@ def test_exhaustive_tiny_extensions_all_levels():
     b = ext_batch(pairs)
     for X in (0, 1, 2, 3, 5, 2 ** 19):
         ref = oracle_run(b, X)
-        for lvl in (1, 2, 3, 4, 5, 6):
+        for lvl in (1, 2, 3, 4, 5, 6, 7):
             got = gpu_run(b, X, first_level=lvl)
             assert_same(*got, *ref, what=f"X={X} level={lvl}")
 
@@ -119,7 +119,7 @@ def test_adversarial_inputs():
     batch = datagen.from_strings(pairs, k=1)
     for X in (0, 5, 20, 50, 100, 400):
         ref = oracle_run(batch, X)
-        for lvl in (None, 1, 3, 6):
+        for lvl in (None, 1, 3, 5, 7):
             for fmt in FMTS:
                 got = gpu_run(batch, X, fmt=fmt, first_level=lvl)
                 assert_same(*got, *ref, what=f"X={X} level={lvl} fmt={fmt}")
@@ -152,7 +152,7 @@ def test_config1_all_pairs(X):
     s = logan.stats_dict(st)
     assert s["cells_total"] == int(ref[1].sum())
     for fmt in FMTS:
-        for lvl in (2, 3, 6):
+        for lvl in (2, 3, 7):
             got = gpu_run(b, X, fmt=fmt, first_level=lvl)
             assert_same(*got, *ref, what=f"C1 fmt={fmt} level={lvl}")
 
@@ -250,7 +250,7 @@ def _mixed_pairs(seed, n=300, maxlen=300):
     return datagen.from_strings(pairs, k=0)
 
 
-@pytest.mark.parametrize("lvl", [1, 2, 3, 4, 5])
+@pytest.mark.parametrize("lvl", [1, 2, 3, 4, 5, 6])
 def test_latency_shapes_as_first_level(lvl):
     """Every level's latency shape (one warp per task), forced as the first level."""
     b = _mixed_pairs(lvl)
@@ -278,3 +278,52 @@ def test_forced_handover_is_exact(period):
                 torch.cuda.synchronize()
                 assert_same(out.cpu().numpy(), cells.cpu().numpy().view(np.uint64), *ref,
                             what=f"handover {period} level {lvl} lat={lat} X={X}")
+
+
+def test_mass_overflow_with_helpers():
+    """Most tasks overflow the first window (X far above its width): helpers take
+    what they can while level 1 runs, the next launch takes the rest; results exact."""
+    w = datagen.CONFIGS[2].with_(xdrop=60)
+    b = datagen.generate(w, n_pairs=4000)
+    idx = np.arange(0, b.n_pairs, 10)
+    ref = oracle_run(b, 60, idx=idx)
+    st = logan.new_stats()
+    db = logan.to_device(b, logan.LOGAN_SEQ_2BIT)
+    out, cells = logan.xdrop_batch(db, 1, -1, -1, 60, first_level=1, stats=st)
+    torch.cuda.synchronize()
+    s = logan.stats_dict(st)
+    assert s["tasks_started"][1] > 1000  # mass hand-over to the W=64 level
+    o, c = out.cpu().numpy(), cells.cpu().numpy().view(np.uint64)
+    assert_same(o[idx], c[idx], *ref, what="mass overflow")
+
+
+def test_cta_level_wide_bands():
+    """The unbounded CTA level forced on BELLA-like pairs (spurious ones have
+    bands of hundreds of slots: several cells per thread, many warps)."""
+    w = datagen.CONFIGS[4]
+    b = datagen.generate(w, n_pairs=40)
+    b.q_len[:] = np.minimum(b.q_len, 2500)
+    b.t_len[:] = np.minimum(b.t_len, 2500)
+    b.q_seed[:] = np.minimum(b.q_seed, b.q_len - w.k)
+    b.t_seed[:] = np.minimum(b.t_seed, b.t_len - w.k)
+    ref = oracle_run(b, 50)
+    for lvl in (7, 6, None):
+        got = gpu_run(b, 50, first_level=lvl)
+        assert_same(*got, *ref, what=f"wide bands level={lvl}")
+
+
+def test_cta_level_extension_equal_to_workspace_bound():
+    """Regression: an extension exactly as long as max_ext_len must fit the CTA
+    level's scratch (the workspace-size -> bound recovery once lost one base to
+    alignment padding)."""
+    w = datagen.CONFIGS[4]
+    b = datagen.generate(w, n_pairs=6)
+    b.q_len[:] = np.minimum(b.q_len, 1200)
+    b.t_len[:] = np.minimum(b.t_len, 1200)
+    b.q_seed[:] = np.minimum(b.q_seed, b.q_len - w.k)
+    b.t_seed[:] = np.minimum(b.t_seed, b.t_len - w.k)
+    assert b.max_ext_len() in set(b.q_seed.tolist()) | set(b.t_seed.tolist())
+    ref = oracle_run(b, 50)
+    for lvl in (7, None):
+        got = gpu_run(b, 50, first_level=lvl)
+        assert_same(*got, *ref, what=f"bound level={lvl}")

@@ -5,7 +5,7 @@ import paper_2002_05200_b200 as logan
 b = T._mixed_pairs(7)
 for X in (3, 10, 30):
     ref = T.oracle_run(b, X)
-    for lvl in (1, 2, 3, 4, 5):
+    for lvl in (1, 2, 3, 4, 5, 6):
         for lat in (False, True):
             for ho in (0, 2, 7):
                 db = logan.to_device(b, logan.LOGAN_SEQ_2BIT)

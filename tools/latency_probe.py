@@ -17,7 +17,7 @@ b.t_seed[:] = 0
 b.workload = b.workload.with_(k=0)
 db = logan.to_device(b)
 for X in (20, 100):
-    for lvl in (1, 2, 3, 4, 5):
+    for lvl in (1, 2, 3, 4, 5, 6):
         for lat in (False, True):
             st = logan.new_stats()
             logan.xdrop_batch(db, 1, -1, -1, X, first_level=lvl, latency_first=lat, stats=st)

@@ -1,0 +1,24 @@
+"""Small batches through every level shape, for compute-sanitizer (memcheck / racecheck / synccheck)."""
+import sys
+
+import numpy as np
+import torch
+
+sys.path.insert(0, ".")
+import datagen
+import paper_2002_05200_b200 as logan
+
+small = "--small" in sys.argv  # racecheck is very slow: a handful of pairs, 2-bit only
+w = datagen.CONFIGS[4]
+b = datagen.generate(w, n_pairs=6 if small else 60)
+if small:
+    b.q_len[:] = np.minimum(b.q_len, 1200)
+    b.t_len[:] = np.minimum(b.t_len, 1200)
+    b.q_seed[:] = np.minimum(b.q_seed, b.q_len - w.k)
+    b.t_seed[:] = np.minimum(b.t_seed, b.t_len - w.k)
+for fmt in ((logan.LOGAN_SEQ_2BIT,) if small else (logan.LOGAN_SEQ_2BIT, logan.LOGAN_SEQ_U8)):
+    db = logan.to_device(b, fmt)
+    for lvl, lat, ho in ((None, False, 0), (1, False, 0), (2, True, 0), (1, False, 6), (7, False, 0)):
+        out, cells = logan.xdrop_batch(db, 1, -1, -1, 50, first_level=lvl, latency_first=lat, handover=ho)
+        torch.cuda.synchronize()
+        print(fmt, lvl, lat, ho, int(cells.sum()), flush=True)
