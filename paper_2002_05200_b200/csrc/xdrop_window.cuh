@@ -517,7 +517,12 @@ __device__ __forceinline__ void run_group(Win &w, const Params &P, const LevelIO
     constexpr int G = Win::GG;
     const int lane = threadIdx.x & 31;
     const int leader = lane - w.gl;
-    auto next_task = [&]() -> bool {
+    // start or resume the next task; a task resumed after an odd antidiagonal
+    // takes the even one here, so the hot loop below always starts at an even d
+    // (a single code path: no per-iteration register shuffling). `rc` returns
+    // the outcome of that alignment step (0 = keep sweeping).
+    auto next_task = [&](int &rc) -> bool {
+        rc = 0;
         uint32_t pos;
         if (!fetch(pos)) return false;
         const uint32_t task = io.list[pos];
@@ -526,20 +531,18 @@ __device__ __forceinline__ void run_group(Win &w, const Params &P, const LevelIO
         else w.init(P, task);
         if (io.stats && w.gl == 0)
             atomicAdd((unsigned long long *)&io.stats->tasks_started[io.level], 1ull);
+        if (w.st.d & 1) rc = w.template step<0>(P);
         return true;
     };
 
-    bool active = next_task();
+    int rc = 0;
+    bool active = next_task(rc);
     int32_t since = 0;  // antidiagonals at this level (hand-over test knob)
     while (active) {
-        // one iteration = the odd then the even antidiagonal; a task resumed
-        // after an odd antidiagonal first takes the even one alone
-        int rc;
-        if ((w.st.d & 1) == 0) {
+        // one iteration = the odd then the even antidiagonal
+        if (rc == 0) {
             rc = w.template step<1>(P);
             if (rc == 0) rc = w.template step<0>(P);
-        } else {
-            rc = w.template step<0>(P);
         }
         if (io.handover > 0) {  // test knob (uniform branch, off in production)
             since += 2;
@@ -586,7 +589,7 @@ __device__ __forceinline__ void run_group(Win &w, const Params &P, const LevelIO
             }
             if (rc == 2) w.st.shifts = 0;
             since = 0;
-            active = next_task();
+            active = next_task(rc);
         }
     }
 }
