@@ -88,6 +88,9 @@ enum {
  *                  combine. Stages not launched leave their events untouched.
  *  flags         : bit 0 = run the first level in its latency shape (one
  *                  warp per task) instead of its throughput shape.
+ *  first_slots   : 0 = automatic; 20, 24, 28 or 32 force the width of the
+ *                  first window (one lane per task) when the first level is
+ *                  level 1. Results never depend on it.
  *  handover      : test knob, 0 = off. If > 0, every task at a register
  *                  window level is handed over to the next level every
  *                  `handover` antidiagonals, exercising the exact hand-over.
@@ -99,7 +102,7 @@ typedef struct {
     int32_t flags;
     void *const *timing_events;
     int32_t handover;
-    int32_t reserved1;
+    int32_t first_slots;
     int64_t reserved[5];
 } logan_options_t;
 

@@ -33,7 +33,7 @@ N_STAGES = 9  # LOGAN_N_STAGES: 0 setup, 1..7 levels, 8 combine
 class Options(ctypes.Structure):
     _fields_ = [("first_level", ctypes.c_int32), ("flags", ctypes.c_int32),
                 ("timing_events", ctypes.c_void_p), ("handover", ctypes.c_int32),
-                ("reserved1", ctypes.c_int32), ("reserved", ctypes.c_int64 * 5)]
+                ("first_slots", ctypes.c_int32), ("reserved", ctypes.c_int64 * 5)]
 
 
 class Result(ctypes.Structure):

@@ -35,14 +35,11 @@ __device__ __forceinline__ uint32_t cost_bucket(uint32_t c) {
 }
 
 // Workspace layout (each region 256-byte aligned).
-// First-level window (G = 1 lane x LOGAN_L0_R slots); tuned by measurement on
-// C2 (X = 20): 28 slots + throughput-shape helpers beat 32 slots by ~2.5%
-// (about 1% of tasks overflow and finish inside the first kernel).
-#ifndef LOGAN_L0_R
-#define LOGAN_L0_R 28
-#endif
-constexpr int NWIDTH = 6;  // register-window widths L0, 64, 128, 256, 512, 1024
-static const int kWidth[NWIDTH] = {LOGAN_L0_R, 64, 128, 256, 512, 1024};
+// First-level window: one lane per task x w0 slots, w0 in {20, 24, 28, 32}
+// chosen at run time from X and the read lengths (auto_first_slots), or forced
+// by options.first_slots. LOGAN_L0_R (build knob) restricts it to one value.
+constexpr int NWIDTH = 6;  // register-window widths w0, 64, 128, 256, 512, 1024
+static const int kWidth[NWIDTH] = {32, 64, 128, 256, 512, 1024};  // [0]: the largest w0 (pool sizing)
 
 struct Layout {
     size_t tres, tbucket, queue, listA, listB, recsA, recsB, hist, cursor_b, counters, wide, total;
@@ -236,11 +233,29 @@ static cudaError_t launch_win(const Params &P, const LevelIO &io_in, const Level
 // wi = width index; latency = run the latency shape; helpers = first level with
 // in-kernel escalation helpers running the next width
 template <int FMT>
+static cudaError_t launch_first(int w0, bool helpers, const Params &P, const LevelIO &io, const LevelIO &hio,
+                                int sms, cudaStream_t s) {
+#ifdef LOGAN_L0_R
+    w0 = LOGAN_L0_R;
+#endif
+    switch (w0) {
+        case 20: return helpers ? launch_win<1, 20, FMT, LOGAN_HSHAPE(64)>(P, io, hio, sms, s)
+                                : launch_win<1, 20, FMT, 0, 0>(P, io, hio, sms, s);
+        case 24: return helpers ? launch_win<1, 24, FMT, LOGAN_HSHAPE(64)>(P, io, hio, sms, s)
+                                : launch_win<1, 24, FMT, 0, 0>(P, io, hio, sms, s);
+        case 28: return helpers ? launch_win<1, 28, FMT, LOGAN_HSHAPE(64)>(P, io, hio, sms, s)
+                                : launch_win<1, 28, FMT, 0, 0>(P, io, hio, sms, s);
+        default: return helpers ? launch_win<1, 32, FMT, LOGAN_HSHAPE(64)>(P, io, hio, sms, s)
+                                : launch_win<1, 32, FMT, 0, 0>(P, io, hio, sms, s);
+    }
+}
+
+template <int FMT>
 static cudaError_t launch_width(int wi, bool latency, bool helpers, const Params &P, const LevelIO &io,
-                                const LevelIO &hio, int sms, cudaStream_t s) {
+                                const LevelIO &hio, int sms, cudaStream_t s, int w0) {
+    if (wi == 0 && !(latency && w0 == 32)) return launch_first<FMT>(w0, helpers && !latency, P, io, hio, sms, s);
     if (helpers && !latency) {
         switch (wi) {
-            case 0: return launch_win<1, LOGAN_L0_R, FMT, LOGAN_HSHAPE(64)>(P, io, hio, sms, s);
             case 1: return launch_win<2, 32, FMT, LOGAN_HSHAPE(128)>(P, io, hio, sms, s);
             case 2: return launch_win<4, 32, FMT, LOGAN_HSHAPE(256)>(P, io, hio, sms, s);
             case 3: return launch_win<8, 32, FMT, LOGAN_HSHAPE(512)>(P, io, hio, sms, s);
@@ -249,9 +264,7 @@ static cudaError_t launch_width(int wi, bool latency, bool helpers, const Params
         }
     }
     switch (wi * 2 + (latency ? 1 : 0)) {
-        case 0: return launch_win<1, LOGAN_L0_R, FMT, 0, 0>(P, io, hio, sms, s);
-        case 1: return LOGAN_L0_R == 32 ? launch_win<32, 1, FMT, 0, 0>(P, io, hio, sms, s)
-                                        : launch_win<1, LOGAN_L0_R, FMT, 0, 0>(P, io, hio, sms, s);
+        case 1: return launch_win<32, 1, FMT, 0, 0>(P, io, hio, sms, s);
         case 2: return launch_win<2, 32, FMT, 0, 0>(P, io, hio, sms, s);
         case 3: return launch_win<32, 2, FMT, 0, 0>(P, io, hio, sms, s);
         case 4: return launch_win<4, 32, FMT, 0, 0>(P, io, hio, sms, s);
@@ -268,13 +281,22 @@ static cudaError_t launch_width(int wi, bool latency, bool helpers, const Params
 
 static int auto_first_level(int32_t xdrop) {
     // the band of true pairs is about X + a few slots wide
-    if (xdrop <= 20) return 0;   // W = LOGAN_L0_R (28)
+    if (xdrop <= 20) return 0;   // W = w0 (auto_first_slots)
     if (xdrop <= 50) return 1;   // W = 64
     if (xdrop <= 110) return 2;  // W = 128
     if (xdrop <= 230) return 3;  // W = 256
     if (xdrop <= 480) return 4;  // W = 512
     if (xdrop <= 1000) return 5; // W = 1024
     return 6;                    // unbounded CTA level
+}
+
+// Slots of the first window: the band of true pairs is about X + 8 slots wide at
+// its widest, and long reads drift more between re-centrings.
+static int auto_first_slots(int32_t xdrop, int64_t max_ext) {
+    if (xdrop <= 12) return 20;
+    if (xdrop <= 16) return 24;
+    if (xdrop <= 20) return max_ext > 6000 ? 32 : 28;
+    return 32;
 }
 
 template <int FMT>
@@ -318,6 +340,8 @@ static int run_batch(const Params &P, const logan_options_t *opt, logan_result_t
     int first = (opt && opt->first_level > 0) ? opt->first_level - 1 : auto_first_level(P.xdrop);
     if (first < 0 || first > NLEVEL - 1) return LOGAN_EINVAL;
     uint32_t *recs[2] = {(uint32_t *)(ws + L.recsA), (uint32_t *)(ws + L.recsB)};
+    const int w0 = (opt && opt->first_slots > 0) ? opt->first_slots : auto_first_slots(P.xdrop, L.wide_stride - 2);
+    auto width_of = [&](int lv) { return lv == 0 ? w0 : kWidth[lv]; };
     const uint32_t *in_list = queue;
     const uint32_t *in_recs = nullptr;
     const int32_t *rec_in = nullptr;
@@ -347,7 +371,7 @@ static int run_batch(const Params &P, const logan_options_t *opt, logan_result_t
         if (lv < NWIDTH - 1) {
             io.out_recs = recs[osel];
             io.rec_out = (int32_t *)(ws + L.pool[lv]);
-            io.rec_out_stride = rec_ints(kWidth[lv]);
+            io.rec_out_stride = rec_ints(width_of(lv));
             io.rec_out_cap = L.pool_cap[lv];
             io.rec_out_count = &ctr[16 + lv];
         }
@@ -357,7 +381,7 @@ static int run_batch(const Params &P, const logan_options_t *opt, logan_result_t
     // would leave SMs with too few warps to hide the per-antidiagonal latency,
     // so the first level runs one warp per task instead (measured on C5 with
     // 2,500 pairs: 260 vs 158 GCUPS).
-    const int64_t groups_needed = L.ntask * (first < NWIDTH ? kWidth[first] / 32 : 1) / 32;  // warps
+    const int64_t groups_needed = L.ntask * (first < NWIDTH ? width_of(first) / 32 : 1) / 32;  // warps
     const bool few_tasks = first > 0 && first < NWIDTH && groups_needed < (int64_t)sms * 16;
     const bool latency_first = (opt && (opt->flags & 1)) || few_tasks;
     for (int lv = first; lv < NLEVEL; ++lv) {
@@ -371,20 +395,20 @@ static int run_batch(const Params &P, const logan_options_t *opt, logan_result_t
                 if (helpers) {
                     // the next level's IO: it reads this level's hand-overs
                     hio = level_io(lv + 1, lists[out_sel], &ctr[8 + lv], recs[out_sel],
-                                   (const int32_t *)(ws + L.pool[lv]), rec_ints(kWidth[lv]), out_sel ^ 1);
+                                   (const int32_t *)(ws + L.pool[lv]), rec_ints(width_of(lv)), out_sel ^ 1);
                     io.done = &ctr[24];
                     // entries are published by writing the task id: start from NO_TASK
                     if (cudaMemsetAsync(lists[out_sel], 0xff, sizeof(uint32_t) * (size_t)L.ntask, s) != cudaSuccess)
                         return LOGAN_ECUDA;
                 }
-                e = launch_width<FMT>(lv, latency_first, helpers, P, io, hio, sms, s);
+                e = launch_width<FMT>(lv, latency_first, helpers, P, io, hio, sms, s, w0);
             } else {
                 io.max_count = latency_below;
-                e = launch_width<FMT>(lv, true, false, P, io, io, sms, s);
+                e = launch_width<FMT>(lv, true, false, P, io, io, sms, s, w0);
                 if (e == cudaSuccess) {
                     io.min_count = latency_below;
                     io.max_count = 0xffffffffu;
-                    e = launch_width<FMT>(lv, false, false, P, io, io, sms, s);
+                    e = launch_width<FMT>(lv, false, false, P, io, io, sms, s, w0);
                 }
             }
         } else {
@@ -396,7 +420,7 @@ static int run_batch(const Params &P, const logan_options_t *opt, logan_result_t
         in_list = lists[out_sel];
         in_recs = (lv < NWIDTH - 1) ? recs[out_sel] : nullptr;
         rec_in = (lv < NWIDTH - 1) ? (const int32_t *)(ws + L.pool[lv]) : nullptr;
-        rec_in_stride = (lv < NWIDTH - 1) ? rec_ints(kWidth[lv]) : 0;
+        rec_in_stride = (lv < NWIDTH - 1) ? rec_ints(width_of(lv)) : 0;
         in_count = &ctr[8 + lv];
         out_sel ^= 1;
     }
@@ -444,6 +468,9 @@ static int check_args(const uint8_t *seq_pool, int32_t seq_fmt, int64_t pool_len
         sc.gap < -127 || sc.xdrop < 0 || sc.xdrop > (1 << 19))
         return LOGAN_EINVAL;
     if (opt && (opt->first_level < 0 || opt->first_level > 7)) return LOGAN_EINVAL;
+    if (opt && opt->first_slots != 0 && opt->first_slots != 20 && opt->first_slots != 24 &&
+        opt->first_slots != 28 && opt->first_slots != 32)
+        return LOGAN_EINVAL;
     if (n_pairs == 0) return LOGAN_OK;
     if (!seq_pool || !q_off || !q_len || !t_off || !t_len || !q_seed || !t_seed || !out) return LOGAN_EINVAL;
     if (((uintptr_t)seq_pool & 3) != 0) return LOGAN_EINVAL;

@@ -178,22 +178,27 @@ struct Stream {
         sh = F::BITS * (int32_t)(pos & (CPW - 1));
         wp = P.pool + (wi < 0 ? 0 : (wi >= P.pool_words ? P.pool_words - 1 : wi));
         cur = __ldg(wp);
-        nxt = (s.dir < 0 && wp == P.pool) ? 0u : __ldg(wp + s.dir);
+        nxt = (s.dir < 0 && wp <= P.pool) ? 0u : __ldg(wp + s.dir);
+    }
+
+    // word boundary crossed: shift the prefetched word in, prefetch the next one
+    __device__ __forceinline__ void refill(const Params &P) {
+        sh -= s.dir * 32;
+        wp += s.dir;
+        cur = nxt;
+        // going backwards, one crossing past the last base can put wp on the word
+        // before the pool: never prefetch below the pool start
+        nxt = (s.dir < 0 && wp <= P.pool) ? 0u : __ldg(wp + s.dir);
     }
 
     __device__ __forceinline__ uint32_t next(const Params &P, uint32_t sent) {
         const int32_t i = idx++;
         if (i < 1 || i > s.len) return sent;  // before the start: parked at index 1
         const uint32_t c = (cur >> sh) & F::MASK;
-        if (i < s.len) {  // advance to index i + 1
-            sh += s.dir * F::BITS;
-            if ((uint32_t)sh >= 32u) {  // crossed a word boundary (once per CPW bases)
-                sh -= s.dir * 32;
-                wp += s.dir;
-                cur = nxt;
-                nxt = (s.dir < 0 && wp == P.pool) ? 0u : __ldg(wp + s.dir);  // prefetch
-            }
-        }
+        // advance (also past index len: at most one extra word, inside the pool's
+        // 16-byte padding going forward, bounded by the pool start going back)
+        sh += s.dir * F::BITS;
+        if (__builtin_expect((uint32_t)sh >= 32u, 0)) refill(P);  // once per CPW bases
         return c;
     }
 };

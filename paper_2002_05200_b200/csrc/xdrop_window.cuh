@@ -87,11 +87,15 @@ struct WinState {
     int32_t d;             // last antidiagonal computed
     int32_t S0;            // slot of the window's first register
     int32_t best, arg_i, arg_j;
-    int32_t Tn, Td, Tp;    // T_{d+1}, T_d, T_{d-1}
-    // live slot extremes of d and d-1; an antidiagonal without a (valid) live
-    // cell has sF = EMPTY_F, sL = EMPTY_L, which makes every min / max below
-    // ignore it without a branch
-    int32_t sF1, sL1, sF2, sL2;
+    // thresholds: Tn = T_{d+1}; Tq[p] = the last T_e with e of parity p
+    // (after antidiagonal d: Tq[d&1] = T_d, Tq[(d-1)&1] = T_{d-1}). Indexing by
+    // parity (a compile-time constant inside a step) means nothing rotates.
+    int32_t Tn, Tq[2];
+    // live slot extremes of the last antidiagonal of each parity (sF[d&1] is
+    // antidiagonal d, sF[(d-1)&1] is d-1); an antidiagonal without a (valid)
+    // live cell has sF = EMPTY_F, sL = EMPTY_L, which makes every min / max
+    // below ignore it without a branch
+    int32_t sF[2], sL[2];
     uint64_t cells;
     uint64_t cells_entry;  // cells already counted when the task entered this level
     uint32_t shifts;
@@ -200,12 +204,12 @@ struct Window {
         st.S0 = -(W / 2);
         st.best = 0;
         st.arg_i = st.arg_j = 0;
-        st.Td = -P.xdrop;  // T_0 = best_{-1} - X with best_{-1} := 0
-        st.Tp = -P.xdrop;
-        st.Tn = -P.xdrop;  // T_1 = best_0 - X
-        st.sF1 = st.sL1 = 0;  // antidiagonal 0: the origin (slot 0)
-        st.sF2 = EMPTY_F;     // antidiagonal -1: empty
-        st.sL2 = EMPTY_L;
+        st.Tq[0] = -P.xdrop;  // T_0 = best_{-1} - X with best_{-1} := 0
+        st.Tq[1] = -P.xdrop;  // T_{-1}
+        st.Tn = -P.xdrop;     // T_1 = best_0 - X
+        st.sF[0] = st.sL[0] = 0;  // antidiagonal 0: the origin (slot 0)
+        st.sF[1] = EMPTY_F;       // antidiagonal -1: empty
+        st.sL[1] = EMPTY_L;
         st.cells = 0;
         st.shifts = 0;
         // values: origin S(0,0) = 0 -> u = 0 - T_0 = X; everything else dead
@@ -252,8 +256,14 @@ struct Window {
         }
         if (gl == 0) {
             rec[0] = (int32_t)st.task; rec[1] = st.d; rec[2] = st.S0; rec[3] = st.best;
-            rec[4] = st.arg_i; rec[5] = st.arg_j; rec[6] = st.Tn; rec[7] = st.Td; rec[8] = st.Tp;
-            rec[9] = st.sF1; rec[10] = st.sL1; rec[11] = st.sF2; rec[12] = st.sL2;
+            const bool odd = st.d & 1;  // record order: d, then d-1
+            rec[4] = st.arg_i; rec[5] = st.arg_j; rec[6] = st.Tn;
+            rec[7] = odd ? st.Tq[1] : st.Tq[0];
+            rec[8] = odd ? st.Tq[0] : st.Tq[1];
+            rec[9] = odd ? st.sF[1] : st.sF[0];
+            rec[10] = odd ? st.sL[1] : st.sL[0];
+            rec[11] = odd ? st.sF[0] : st.sF[1];
+            rec[12] = odd ? st.sL[0] : st.sL[1];
             rec[13] = 0;
             rec[14] = (int32_t)st.shifts; rec[15] = W;
             rec[16] = (int32_t)(uint32_t)st.cells; rec[17] = (int32_t)(uint32_t)(st.cells >> 32);
@@ -270,14 +280,20 @@ struct Window {
         st.d = rec[1];
         const int32_t S0src = rec[2];
         st.best = rec[3]; st.arg_i = rec[4]; st.arg_j = rec[5];
-        st.Tn = rec[6]; st.Td = rec[7]; st.Tp = rec[8];
-        st.sF1 = rec[9]; st.sL1 = rec[10]; st.sF2 = rec[11]; st.sL2 = rec[12];
+        const bool odd = st.d & 1;
+        st.Tn = rec[6];
+        st.Tq[0] = odd ? rec[8] : rec[7];
+        st.Tq[1] = odd ? rec[7] : rec[8];
+        st.sF[0] = odd ? rec[11] : rec[9];
+        st.sF[1] = odd ? rec[9] : rec[11];
+        st.sL[0] = odd ? rec[12] : rec[10];
+        st.sL[1] = odd ? rec[10] : rec[12];
         st.shifts = (uint32_t)rec[14];
         const int32_t Wsrc = rec[15];
         st.cells = (uint64_t)(uint32_t)rec[16] | ((uint64_t)(uint32_t)rec[17] << 32);
         st.cells_entry = st.cells;
         // centre the wider window on the live band of d and d-1
-        int32_t Fm = min(st.sF1, st.sF2), Lm = max(st.sL1, st.sL2);
+        int32_t Fm = min(st.sF[0], st.sF[1]), Lm = max(st.sL[0], st.sL[1]);
         if (Fm > Lm) { Fm = S0src; Lm = S0src + Wsrc - 1; }
         st.S0 = ((Fm + Lm) >> 1) - W / 2;
         const int32_t s0 = st.S0 + gl * R;
@@ -306,8 +322,9 @@ struct Window {
             // columns of slots on d-1 and d-2 (PAR fixes the parity of d)
             const int32_t c1 = PAR ? (d - 1) >> 1 : d >> 1;
             const int32_t c2 = PAR ? (d - 1) >> 1 : (d - 2) >> 1;
-            const int32_t lo = max(min(st.sF1 + c1, st.sF2 + c2 + 1), max(1, d - st.n));
-            const int32_t hi = min(max(st.sL1 + c1, st.sL2 + c2) + 1, min(st.m, d - 1));
+            // d-1 has the other parity, d-2 this parity
+            const int32_t lo = max(min(st.sF[1 - PAR] + c1, st.sF[PAR] + c2 + 1), max(1, d - st.n));
+            const int32_t hi = min(max(st.sL[1 - PAR] + c1, st.sL[PAR] + c2) + 1, min(st.m, d - 1));
             st.cells += (uint32_t)max(hi - lo + 1, 0);
         }
 
@@ -324,11 +341,12 @@ struct Window {
             shift_up(Bw, in);
         }
 
-        // (3) rebased constants (T_d = st.Tn is this step's threshold)
+        // (3) rebased constants (T_d = st.Tn is this step's threshold; T_{d-1} is
+        //     the other parity's, T_{d-2} this parity's)
         const int32_t Tc = st.Tn;
-        const int32_t gp = P.gap - (Tc - st.Td);
-        const int32_t sma = P.match - (Tc - st.Tp);
-        const int32_t smi = P.mismatch - (Tc - st.Tp);
+        const int32_t gp = P.gap - (Tc - st.Tq[1 - PAR]);
+        const int32_t sma = P.match - (Tc - st.Tq[PAR]);
+        const int32_t smi = P.mismatch - (Tc - st.Tq[PAR]);
         const int32_t fg = DEAD - gp;  // max(up, left, fg) + gp >= DEAD: the floor
 
         const uint32_t two = 2u * (uint32_t)P.one;  // = 2, opaque to the compiler
@@ -419,20 +437,25 @@ struct Window {
                 st.arg_j = d - st.arg_i;
             }
         }
-        st.Tp = st.Td;
-        st.Td = Tc;
+        st.Tq[PAR] = Tc;
         st.Tn = st.best - P.xdrop;
         st.d = d;
 
+        st.sF[PAR] = h ? st.S0 + lf : EMPTY_F;
+        st.sL[PAR] = h ? st.S0 + ll : EMPTY_L;
+        // The checks below run after the even antidiagonal only. The band's
+        // right edge can grow (by one slot) only on even steps and its left
+        // edge only on odd steps, so the margin-1 invariant checked here keeps
+        // every cell outside the window dead through both steps of the next
+        // iteration. An odd antidiagonal that ends the task is followed by one
+        // extra even one whose band is empty: no cells, no best change.
+        if (PAR == 1) return 0;
+
         // (7) termination: antidiagonals d and d-1 both empty (c-amb-7)
-        if (!h && st.sF1 == EMPTY_F) return 1;
-        st.sF2 = st.sF1;
-        st.sL2 = st.sL1;
-        st.sF1 = h ? st.S0 + lf : EMPTY_F;
-        st.sL1 = h ? st.S0 + ll : EMPTY_L;
+        if (st.sF[0] == EMPTY_F && st.sF[1] == EMPTY_F) return 1;
 
         // (8) keep the live band of d and d-1 inside [S0+1, S0+W-2]
-        const int32_t Fm = min(st.sF1, st.sF2), Lm = max(st.sL1, st.sL2);
+        const int32_t Fm = min(st.sF[0], st.sF[1]), Lm = max(st.sL[0], st.sL[1]);
         const bool lowv = Fm < st.S0 + 1, highv = Lm > st.S0 + W - 2;
         if (lowv || highv) {
             if (lowv && highv) return 2;

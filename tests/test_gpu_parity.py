@@ -327,3 +327,17 @@ def test_cta_level_extension_equal_to_workspace_bound():
     for lvl in (7, None):
         got = gpu_run(b, 50, first_level=lvl)
         assert_same(*got, *ref, what=f"bound level={lvl}")
+
+
+@pytest.mark.parametrize("slots", [20, 24, 28, 32])
+def test_first_window_widths(slots):
+    """Every compiled first-window width (one lane per task) is exact, including
+    the overflow hand-over to the next level."""
+    b = _mixed_pairs(300 + slots)
+    for X in (0, 5, 12, 20):
+        ref = oracle_run(b, X)
+        db = logan.to_device(b, logan.LOGAN_SEQ_2BIT)
+        out, cells = logan.xdrop_batch(db, 1, -1, -1, X, first_level=1, first_slots=slots)
+        torch.cuda.synchronize()
+        assert_same(out.cpu().numpy(), cells.cpu().numpy().view(np.uint64), *ref,
+                    what=f"first window {slots} X={X}")
