@@ -104,6 +104,11 @@ CONFIGS = {
                 len_hi=30000, xdrop=50, seed=SEED_BASE + 4),
     5: Workload("c5_long_x100", 20_000, tlen_min=50000, tlen_max=100000, err=0.12, xdrop=100,
                 seed=SEED_BASE + 5),
+    # not a BASELINE config: the paper's own benchmark set (Tables II-III):
+    # 100K pairs of 2.5-7.5 kb reads at ~15% error, swept over X = 10 ... 5000
+    # (the wide-band mode); listed at its largest X
+    6: Workload("t2_2.5-7.5k_x5000", 100_000, tlen_min=2500, tlen_max=7500, err=0.15, xdrop=5000,
+                seed=SEED_BASE + 6),
 }
 
 

@@ -77,14 +77,17 @@ enum {
 /* Options (may be passed as NULL = all defaults).
  *  first_level   : 0 = automatic from xdrop; 1..6 force the first
  *                  register-window level (windows of 32, 64, 128, 256, 512,
- *                  1024 diagonal slots); 7 forces every task onto the
- *                  unbounded CTA level. Results never depend on it (tests
- *                  assert this); only speed does.
+ *                  1024 diagonal slots); 7 starts every task on the ring
+ *                  level (one warp per task, band in an 8192-slot shared-
+ *                  memory ring; used for X <= 30000, wider bands go on);
+ *                  8 forces every task onto the unbounded CTA level.
+ *                  Results never depend on it (tests assert this); only
+ *                  speed does.
  *  timing_events : NULL, or LOGAN_N_STAGES * 2 cudaEvent_t created by the
  *                  caller (timing enabled). Event [2s] is recorded on `stream`
  *                  just before stage s and [2s+1] just after it, for every
  *                  stage the call launches: stage 0 = setup (task expansion,
- *                  LPT bucketing), stages 1..7 = levels 1..7, stage 8 =
+ *                  LPT bucketing), stages 1..8 = levels 1..8, stage 9 =
  *                  combine. Stages not launched leave their events untouched.
  *  flags         : bit 0 = run the first level in its latency shape (one
  *                  warp per task) instead of its throughput shape.
@@ -96,7 +99,7 @@ enum {
  *                  `handover` antidiagonals, exercising the exact hand-over.
  *                  Results never depend on it.
  */
-#define LOGAN_N_STAGES 9
+#define LOGAN_N_STAGES 10
 typedef struct {
     int32_t first_level;
     int32_t flags;
@@ -111,7 +114,7 @@ typedef struct {
  * there, the tasks that finished there and their band cells; window shifts
  * summed over all tasks. */
 typedef struct {
-    uint64_t tasks_started[8];   /* entries 0..6 used: levels 1..7 */
+    uint64_t tasks_started[8];   /* entry l-1 = level l (1..8) */
     uint64_t tasks_finished[8];
     uint64_t cells_per_level[8];
     uint64_t window_shifts;

@@ -27,7 +27,7 @@ class Scoring(ctypes.Structure):
                 ("gap", ctypes.c_int32), ("xdrop", ctypes.c_int32)]
 
 
-N_STAGES = 9  # LOGAN_N_STAGES: 0 setup, 1..7 levels, 8 combine
+N_STAGES = 10  # LOGAN_N_STAGES: 0 setup, 1..8 levels, 9 combine
 
 
 class Options(ctypes.Structure):

@@ -141,7 +141,7 @@ def new_stats(device=None):
 
 def stats_dict(stats_tensor) -> dict:
     v = [int(x) for x in stats_tensor.cpu().tolist()]
-    return {"tasks_started": v[0:7], "tasks_finished": v[8:15], "cells_per_level": v[16:23],
+    return {"tasks_started": v[0:8], "tasks_finished": v[8:16], "cells_per_level": v[16:24],
             "window_shifts": v[24], "cells_total": v[25]}
 
 

@@ -8,23 +8,27 @@
 //   2. k_scan     : bucket histogram -> descending start offsets
 //   3. k_scatter  : tasks into a longest-first (LPT) work queue, the device
 //                   counterpart of the paper's host load balancing
-//   4. levels 1-5 : k_window<G, R> register-window sweeps, widening W = G*R
+//   4. levels 1-6 : k_window<G, R> register-window sweeps, widening W = G*R
 //                   from the level chosen for X; a task whose band outgrows a
-//                   window is handed to the next level (exact restart)
-//   5. level 6    : k_wide, one CTA per task, unbounded band
-//   6. k_combine  : seed score + L + R -> logan_result_t, cells (c-amb-8/10)
+//                   window is handed to the next level with its exact state
+//   5. level 7    : k_ring, one warp per task, the band in a shared-memory
+//                   ring of 8192 slots (wide bands: large X)
+//   6. level 8    : k_wide, one CTA per task, unbounded band (restart)
+//   7. k_combine  : seed score + L + R -> logan_result_t, cells (c-amb-8/10)
 #include <cstdio>
 #include <cstring>
 
 #include "logan_xdrop.h"
 #include "xdrop_common.cuh"
+#include "xdrop_ring.cuh"
 #include "xdrop_wide.cuh"
 #include "xdrop_window.cuh"
 
 namespace logan {
 
 constexpr int NBUCKET = 2048;
-constexpr int NLEVEL = 7;  // 6 window levels + the wide level
+constexpr int NLEVEL = 8;  // 6 window levels + the ring level + the CTA level
+constexpr int RING_LEVEL = 6, WIDE_LEVEL = 7;
 constexpr int SETUP_THREADS = 256;
 
 __device__ __forceinline__ uint32_t cost_bucket(uint32_t c) {
@@ -43,12 +47,14 @@ static const int kWidth[NWIDTH] = {32, 64, 128, 256, 512, 1024};  // [0]: the la
 
 struct Layout {
     size_t tres, tbucket, queue, listA, listB, recsA, recsB, hist, cursor_b, counters, wide, total;
-    size_t pool[NWIDTH - 1];     // hand-over records written by width level w (w < NWIDTH-1)
-    uint32_t pool_cap[NWIDTH - 1];
+    size_t pool[NWIDTH];         // hand-over records written by window level w
+    uint32_t pool_cap[NWIDTH];
     int64_t ntask, wide_stride;
 };
 
 constexpr int WIDE_CTAS = 296;  // 2 per SM on B200
+constexpr int NCTR = 64;
+constexpr int CTR_OUT = 16, CTR_FILL = 32, CTR_DONE = 48;
 
 static size_t align256(size_t x) { return (x + 255) & ~(size_t)255; }
 
@@ -64,7 +70,7 @@ static Layout make_layout(int64_t n_pairs, int64_t max_ext_len) {
     L.listB = o;    o += align256(sizeof(uint32_t) * (size_t)nt);
     L.recsA = o;    o += align256(sizeof(uint32_t) * (size_t)nt);
     L.recsB = o;    o += align256(sizeof(uint32_t) * (size_t)nt);
-    for (int w = 0; w < NWIDTH - 1; ++w) {
+    for (int w = 0; w < NWIDTH; ++w) {
         // at most 128 MiB of records per level; tasks beyond that restart
         const int64_t rec_bytes = (int64_t)sizeof(int32_t) * rec_ints(kWidth[w]);
         int64_t cap = ((int64_t)128 << 20) / rec_bytes;
@@ -75,9 +81,9 @@ static Layout make_layout(int64_t n_pairs, int64_t max_ext_len) {
     }
     L.hist = o;     o += align256(sizeof(uint32_t) * NBUCKET);
     L.cursor_b = o; o += align256(sizeof(uint32_t) * NBUCKET);
-    // counters: [0] queue count, [1..NLEVEL] level cursors, [8..8+NLEVEL] out counts,
-    // [16..16+NWIDTH-1] record pool fill, [24] producer groups done (helpers)
-    L.counters = o; o += align256(sizeof(uint32_t) * 32);
+    // counters: [0] queue count, [1 + lv] level cursors, [16 + lv] out counts,
+    // [32 + lv] record pool fill, [48] producer groups done (helpers)
+    L.counters = o; o += align256(sizeof(uint32_t) * NCTR);
     L.wide_stride = max_ext_len + 2;
     L.wide = o;     o += align256(sizeof(int32_t) * 3 * (size_t)L.wide_stride * WIDE_CTAS);
     L.total = o;
@@ -287,7 +293,8 @@ static int auto_first_level(int32_t xdrop) {
     if (xdrop <= 230) return 3;  // W = 256
     if (xdrop <= 480) return 4;  // W = 512
     if (xdrop <= 1000) return 5; // W = 1024
-    return 6;                    // unbounded CTA level
+    if (xdrop <= RING_XMAX) return RING_LEVEL;  // the band follows the alignment's width
+    return WIDE_LEVEL;           // unbounded CTA level
 }
 
 // Slots of the first window: the band of true pairs is about X + 8 slots wide at
@@ -316,7 +323,7 @@ static int run_batch(const Params &P, const logan_options_t *opt, logan_result_t
     if (cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess) return LOGAN_ECUDA;
 
     if (cudaMemsetAsync(hist, 0, sizeof(uint32_t) * NBUCKET, s) != cudaSuccess) return LOGAN_ECUDA;
-    if (cudaMemsetAsync(ctr, 0, sizeof(uint32_t) * 32, s) != cudaSuccess) return LOGAN_ECUDA;
+    if (cudaMemsetAsync(ctr, 0, sizeof(uint32_t) * NCTR, s) != cudaSuccess) return LOGAN_ECUDA;
     if (stats && cudaMemsetAsync(stats, 0, sizeof(logan_stats_t), s) != cudaSuccess) return LOGAN_ECUDA;
 
     cudaEvent_t const *ev = (opt && opt->timing_events) ? (cudaEvent_t const *)opt->timing_events : nullptr;
@@ -358,7 +365,7 @@ static int run_batch(const Params &P, const logan_options_t *opt, logan_result_t
         io.count = cnt;
         io.cursor = &ctr[1 + lv];
         io.out_list = lists[osel];
-        io.out_count = &ctr[8 + lv];
+        io.out_count = &ctr[CTR_OUT + lv];
         io.stats = stats;
         io.level = lv;
         io.tres = tres;
@@ -368,12 +375,12 @@ static int run_batch(const Params &P, const logan_options_t *opt, logan_result_t
         io.handover = opt ? opt->handover : 0;
         io.min_count = 0;
         io.max_count = 0xffffffffu;
-        if (lv < NWIDTH - 1) {
+        if (lv < NWIDTH) {
             io.out_recs = recs[osel];
             io.rec_out = (int32_t *)(ws + L.pool[lv]);
             io.rec_out_stride = rec_ints(width_of(lv));
             io.rec_out_cap = L.pool_cap[lv];
-            io.rec_out_count = &ctr[16 + lv];
+            io.rec_out_count = &ctr[CTR_FILL + lv];
         }
         return io;
     };
@@ -394,9 +401,9 @@ static int run_batch(const Params &P, const logan_options_t *opt, logan_result_t
                 LevelIO hio{};
                 if (helpers) {
                     // the next level's IO: it reads this level's hand-overs
-                    hio = level_io(lv + 1, lists[out_sel], &ctr[8 + lv], recs[out_sel],
+                    hio = level_io(lv + 1, lists[out_sel], &ctr[CTR_OUT + lv], recs[out_sel],
                                    (const int32_t *)(ws + L.pool[lv]), rec_ints(width_of(lv)), out_sel ^ 1);
-                    io.done = &ctr[24];
+                    io.done = &ctr[CTR_DONE];
                     // entries are published by writing the task id: start from NO_TASK
                     if (cudaMemsetAsync(lists[out_sel], 0xff, sizeof(uint32_t) * (size_t)L.ntask, s) != cudaSuccess)
                         return LOGAN_ECUDA;
@@ -411,6 +418,12 @@ static int run_batch(const Params &P, const logan_options_t *opt, logan_result_t
                     e = launch_width<FMT>(lv, false, false, P, io, io, sms, s, w0);
                 }
             }
+        } else if (lv == RING_LEVEL) {
+            e = cudaFuncSetAttribute(k_ring<FMT>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)RING_SMEM);
+            if (e == cudaSuccess) {
+                k_ring<FMT><<<sms, RING_WARPS * 32, RING_SMEM, s>>>(P, io);
+                e = cudaGetLastError();
+            }
         } else {
             k_wide<FMT><<<WIDE_CTAS, WIDE_THREADS, 0, s>>>(P, io, wide, L.wide_stride);
             e = cudaGetLastError();
@@ -418,10 +431,10 @@ static int run_batch(const Params &P, const logan_options_t *opt, logan_result_t
         if (e != cudaSuccess) return LOGAN_ECUDA;
         if (!mark(1 + lv, 1)) return LOGAN_ECUDA;
         in_list = lists[out_sel];
-        in_recs = (lv < NWIDTH - 1) ? recs[out_sel] : nullptr;
-        rec_in = (lv < NWIDTH - 1) ? (const int32_t *)(ws + L.pool[lv]) : nullptr;
-        rec_in_stride = (lv < NWIDTH - 1) ? rec_ints(width_of(lv)) : 0;
-        in_count = &ctr[8 + lv];
+        in_recs = (lv < NWIDTH) ? recs[out_sel] : nullptr;
+        rec_in = (lv < NWIDTH) ? (const int32_t *)(ws + L.pool[lv]) : nullptr;
+        rec_in_stride = (lv < NWIDTH) ? rec_ints(width_of(lv)) : 0;
+        in_count = &ctr[CTR_OUT + lv];
         out_sel ^= 1;
     }
     int grid3 = (int)((P.n_pairs + per_block - 1) / per_block);
@@ -467,7 +480,7 @@ static int check_args(const uint8_t *seq_pool, int32_t seq_fmt, int64_t pool_len
     if (sc.match <= 0 || sc.match > 127 || sc.mismatch >= 0 || sc.mismatch < -127 || sc.gap >= 0 ||
         sc.gap < -127 || sc.xdrop < 0 || sc.xdrop > (1 << 19))
         return LOGAN_EINVAL;
-    if (opt && (opt->first_level < 0 || opt->first_level > 7)) return LOGAN_EINVAL;
+    if (opt && (opt->first_level < 0 || opt->first_level > NLEVEL)) return LOGAN_EINVAL;
     if (opt && opt->first_slots != 0 && opt->first_slots != 20 && opt->first_slots != 24 &&
         opt->first_slots != 28 && opt->first_slots != 32)
         return LOGAN_EINVAL;

@@ -63,7 +63,7 @@ def test_exhaustive_tiny_extensions_all_levels():
     b = ext_batch(pairs)
     for X in (0, 1, 2, 3, 5, 2 ** 19):
         ref = oracle_run(b, X)
-        for lvl in (1, 2, 3, 4, 5, 6, 7):
+        for lvl in (1, 2, 3, 4, 5, 6, 7, 8):
             got = gpu_run(b, X, first_level=lvl)
             assert_same(*got, *ref, what=f"X={X} level={lvl}")
 
@@ -119,7 +119,7 @@ def test_adversarial_inputs():
     batch = datagen.from_strings(pairs, k=1)
     for X in (0, 5, 20, 50, 100, 400):
         ref = oracle_run(batch, X)
-        for lvl in (None, 1, 3, 5, 7):
+        for lvl in (None, 1, 3, 5, 7, 8):
             for fmt in FMTS:
                 got = gpu_run(batch, X, fmt=fmt, first_level=lvl)
                 assert_same(*got, *ref, what=f"X={X} level={lvl} fmt={fmt}")
@@ -152,7 +152,7 @@ def test_config1_all_pairs(X):
     s = logan.stats_dict(st)
     assert s["cells_total"] == int(ref[1].sum())
     for fmt in FMTS:
-        for lvl in (2, 3, 7):
+        for lvl in (2, 3, 7, 8):
             got = gpu_run(b, X, fmt=fmt, first_level=lvl)
             assert_same(*got, *ref, what=f"C1 fmt={fmt} level={lvl}")
 
@@ -307,7 +307,7 @@ def test_cta_level_wide_bands():
     b.q_seed[:] = np.minimum(b.q_seed, b.q_len - w.k)
     b.t_seed[:] = np.minimum(b.t_seed, b.t_len - w.k)
     ref = oracle_run(b, 50)
-    for lvl in (7, 6, None):
+    for lvl in (8, 7, 6, None):
         got = gpu_run(b, 50, first_level=lvl)
         assert_same(*got, *ref, what=f"wide bands level={lvl}")
 
@@ -324,7 +324,7 @@ def test_cta_level_extension_equal_to_workspace_bound():
     b.t_seed[:] = np.minimum(b.t_seed, b.t_len - w.k)
     assert b.max_ext_len() in set(b.q_seed.tolist()) | set(b.t_seed.tolist())
     ref = oracle_run(b, 50)
-    for lvl in (7, None):
+    for lvl in (8, None):
         got = gpu_run(b, 50, first_level=lvl)
         assert_same(*got, *ref, what=f"bound level={lvl}")
 
@@ -341,3 +341,74 @@ def test_first_window_widths(slots):
         torch.cuda.synchronize()
         assert_same(out.cpu().numpy(), cells.cpu().numpy().view(np.uint64), *ref,
                     what=f"first window {slots} X={X}")
+
+
+# --------------------------------------------------------------------------
+# Ring level (level 7): one warp per task, the band in a shared-memory ring.
+
+def _t2_pairs(n, cap, seed_off=0):
+    """The paper's benchmark set (config 6: 2.5-7.5 kb reads, ~15% error),
+    reads capped at `cap` bases so the oracle's full-band DP stays fast."""
+    w = datagen.CONFIGS[6]
+    b = datagen.generate(w, n_pairs=n, pair_base=seed_off)
+    b.q_len[:] = np.minimum(b.q_len, cap)
+    b.t_len[:] = np.minimum(b.t_len, cap)
+    b.q_seed[:] = np.minimum(b.q_seed, b.q_len - w.k)
+    b.t_seed[:] = np.minimum(b.t_seed, b.t_len - w.k)
+    return b
+
+
+@pytest.mark.parametrize("X", [150, 1000, 5000])
+def test_ring_level_wide_x(X):
+    """Large X (the paper's X sweep): bands of hundreds to thousands
+    of slots, swept by the ring level; forced and automatic level choice, both
+    pool formats, and the per-level statistics."""
+    b = _t2_pairs(24, 3000)
+    ref = oracle_run(b, X)
+    for fmt in FMTS:
+        for lvl in (7, None):
+            st = logan.new_stats()
+            got = gpu_run(b, X, fmt=fmt, first_level=lvl, stats=st)
+            assert_same(*got, *ref, what=f"ring X={X} fmt={fmt} level={lvl}")
+            s = logan.stats_dict(st)
+            assert s["cells_total"] == int(ref[1].sum())
+            if lvl == 7:
+                assert s["tasks_finished"][6] == s["tasks_started"][6] > 0
+
+
+def test_ring_level_resumes_window_records():
+    """Tasks handed over by the widest register window (W = 1024) continue in
+    the ring from the exact record: forced hand-overs after 2, 7 and 300
+    antidiagonals, starting at level 6 (and at level 1, cascading through every
+    window)."""
+    b = _t2_pairs(16, 1500)
+    for X in (60, 400, 3000):
+        ref = oracle_run(b, X)
+        for lvl, period in ((6, 2), (6, 7), (6, 300), (1, 2)):
+            db = logan.to_device(b, logan.LOGAN_SEQ_2BIT)
+            st = logan.new_stats()
+            out, cells = logan.xdrop_batch(db, 1, -1, -1, X, first_level=lvl, handover=period, stats=st)
+            torch.cuda.synchronize()
+            assert_same(out.cpu().numpy(), cells.cpu().numpy().view(np.uint64), *ref,
+                        what=f"ring resume X={X} level={lvl} period={period}")
+            assert logan.stats_dict(st)["tasks_started"][6] > 0
+
+
+def test_ring_overflow_and_large_x_go_to_cta_level():
+    """A band wider than the ring (two 9 kb near-identical reads at a huge X)
+    and X above the ring's int16 limit both end on the CTA level, exactly."""
+    rng = np.random.default_rng(7)
+    base = "".join(rng.choice(list("ACGT"), 9000))
+    mut = list(base)
+    for p in rng.choice(9000, 300, replace=False):
+        mut[p] = "ACGT"[("ACGT".index(mut[p]) + 1) % 4]
+    pairs = [(base, "".join(mut), 0, 0), (base[:3000], "".join(mut)[:3000], 1500, 1500)]
+    b = datagen.from_strings(pairs, k=5)
+    for X in (20000, 40000):
+        ref = oracle_run(b, X)
+        for lvl in (7, None):
+            st = logan.new_stats()
+            got = gpu_run(b, X, first_level=lvl, stats=st)
+            assert_same(*got, *ref, what=f"ring overflow X={X} level={lvl}")
+            s = logan.stats_dict(st)
+            assert s["tasks_finished"][7] >= 1  # the 9 kb extension finished on the CTA level
