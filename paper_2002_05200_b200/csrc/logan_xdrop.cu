@@ -11,8 +11,8 @@
 //   4. levels 1-6 : k_window<G, R> register-window sweeps, widening W = G*R
 //                   from the level chosen for X; a task whose band outgrows a
 //                   window is handed to the next level with its exact state
-//   5. level 7    : k_ring, one warp per task, the band in a shared-memory
-//                   ring of 8192 slots (wide bands: large X)
+//   5. level 7    : k_band, one CTA per task, the band as int16 pairs in a
+//                   shared-memory ring of 8192 slots (wide bands: large X)
 //   6. level 8    : k_wide, one CTA per task, unbounded band (restart)
 //   7. k_combine  : seed score + L + R -> logan_result_t, cells (c-amb-8/10)
 #include <cstdio>
@@ -20,15 +20,15 @@
 
 #include "logan_xdrop.h"
 #include "xdrop_common.cuh"
-#include "xdrop_ring.cuh"
+#include "xdrop_band.cuh"
 #include "xdrop_wide.cuh"
 #include "xdrop_window.cuh"
 
 namespace logan {
 
 constexpr int NBUCKET = 2048;
-constexpr int NLEVEL = 8;  // 6 window levels + the ring level + the CTA level
-constexpr int RING_LEVEL = 6, WIDE_LEVEL = 7;
+constexpr int NLEVEL = 8;  // 6 window levels + the band level + the CTA level
+constexpr int BAND_LEVEL = 6, WIDE_LEVEL = 7;
 constexpr int SETUP_THREADS = 256;
 
 __device__ __forceinline__ uint32_t cost_bucket(uint32_t c) {
@@ -293,7 +293,7 @@ static int auto_first_level(int32_t xdrop) {
     if (xdrop <= 230) return 3;  // W = 256
     if (xdrop <= 480) return 4;  // W = 512
     if (xdrop <= 1000) return 5; // W = 1024
-    if (xdrop <= RING_XMAX) return RING_LEVEL;  // the band follows the alignment's width
+    if (xdrop <= BAND_XMAX) return BAND_LEVEL;  // the band follows the alignment's width
     return WIDE_LEVEL;           // unbounded CTA level
 }
 
@@ -418,10 +418,14 @@ static int run_batch(const Params &P, const logan_options_t *opt, logan_result_t
                     e = launch_width<FMT>(lv, false, false, P, io, io, sms, s, w0);
                 }
             }
-        } else if (lv == RING_LEVEL) {
-            e = cudaFuncSetAttribute(k_ring<FMT>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)RING_SMEM);
+        } else if (lv == BAND_LEVEL) {
+            const int smem = (int)BandSmem<FMT>::BYTES;
+            e = cudaFuncSetAttribute(k_band<FMT>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+            int per_sm = 0;
+            if (e == cudaSuccess)
+                e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_band<FMT>, BAND_NT, smem);
             if (e == cudaSuccess) {
-                k_ring<FMT><<<sms, RING_WARPS * 32, RING_SMEM, s>>>(P, io);
+                k_band<FMT><<<sms * (per_sm > 0 ? per_sm : 1), BAND_NT, smem, s>>>(P, io);
                 e = cudaGetLastError();
             }
         } else {
