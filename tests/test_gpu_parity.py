@@ -412,3 +412,18 @@ def test_ring_overflow_and_large_x_go_to_cta_level():
             assert_same(*got, *ref, what=f"ring overflow X={X} level={lvl}")
             s = logan.stats_dict(st)
             assert s["tasks_finished"][7] >= 1  # the 9 kb extension finished on the CTA level
+
+
+def test_band_level_restages_codes_on_long_reads():
+    """Extensions much longer than the band level's staged code window (a 16384-
+    position circular buffer, refilled when the band drifts out of it): 14 kb
+    homologous reads at X = 300, forced onto level 7 and on the automatic
+    path, both pool formats; burst insertions drift the band off the diagonal."""
+    w = datagen.CONFIGS[3].with_(tlen_min=14000, tlen_max=14000, err=0.12, burst=0.3)
+    b = datagen.generate(w, n_pairs=6, pair_base=11)
+    for X in (300, 1500):
+        ref = oracle_run(b, X)
+        for fmt in FMTS:
+            for lvl in (7, None):
+                got = gpu_run(b, X, fmt=fmt, first_level=lvl)
+                assert_same(*got, *ref, what=f"band restage X={X} fmt={fmt} level={lvl}")
