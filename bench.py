@@ -322,10 +322,10 @@ def main():
         except (OSError, ValueError):
             traffic = None
     level_names = ["window32", "window64", "window128", "window256", "window512", "window1024",
-                   "ring8192", "wide_cta"]
+                   "band8192", "wide_cta"]
     roofline = {"bound": "alu", "achieved": achieved_tops, "peak": peak_tops, "unit": "TOP/s",
                 "frac": achieved_tops / peak_tops, "traffic": traffic,
-                "kernel": f"{'k_window' if dom_level < 6 else ('k_ring' if dom_level == 6 else 'k_wide')} "
+                "kernel": f"{'k_window' if dom_level < 6 else ('k_band' if dom_level == 6 else 'k_wide')} "
                           f"level {dom_level + 1} ({level_names[dom_level]})",
                 "kernel_ms": dom_ms, "kernel_share_of_step": dom_ms / (total_ms / args.steps),
                 "ops_per_cell": N_REF_OPS_PER_CELL,

@@ -77,9 +77,10 @@ enum {
 /* Options (may be passed as NULL = all defaults).
  *  first_level   : 0 = automatic from xdrop; 1..6 force the first
  *                  register-window level (windows of 32, 64, 128, 256, 512,
- *                  1024 diagonal slots); 7 starts every task on the ring
- *                  level (one warp per task, band in an 8192-slot shared-
- *                  memory ring; used for X <= 30000, wider bands go on);
+ *                  1024 diagonal slots); 7 starts every task on the band
+ *                  level (one CTA per task, the band as int16 pairs in an
+ *                  8192-slot shared-memory ring; used for X <= 30000, wider
+ *                  bands go on);
  *                  8 forces every task onto the unbounded CTA level.
  *                  Results never depend on it (tests assert this); only
  *                  speed does.
