@@ -48,9 +48,19 @@ namespace logan {
 constexpr int BAND_SLOTS = 8192;              // ring slots per parity
 constexpr int BAND_WORDS = BAND_SLOTS / 2;    // int16x2 words per parity
 constexpr int BAND_XMAX = 30000;              // live u <= X + 2*127 must fit int16
-constexpr int BAND_MARGIN = 64;               // slots kept free between the band's ends
-constexpr int BAND_CAP = 16384;               // code positions per read buffer (circular)
-constexpr int BAND_PAD = 1024;                // codes staged beyond the needed range
+constexpr int BAND_MARGIN = 128;              // slots kept free between the band's ends
+#ifndef LOGAN_BAND_CAP
+#define LOGAN_BAND_CAP 8192
+#endif
+#ifndef LOGAN_BAND_PAD
+#define LOGAN_BAND_PAD 48
+#endif
+// code positions per read buffer (circular): the codes a planned antidiagonal
+// needs span at most BAND_SLOTS - BAND_MARGIN + 2 positions; with BAND_PAD of
+// slack on both sides and word rounding they must fit
+constexpr int BAND_CAP = LOGAN_BAND_CAP;
+constexpr int BAND_PAD = LOGAN_BAND_PAD;      // codes staged beyond the needed range
+static_assert(BAND_SLOTS - BAND_MARGIN + 2 + 2 * BAND_PAD + 16 <= BAND_CAP, "code buffer too small for the ring");
 constexpr uint32_t D16X2 = 0xC000C000u;       // two dead slots (-16384 each)
 #ifndef LOGAN_BAND_NT
 #define LOGAN_BAND_NT 128
