@@ -92,6 +92,10 @@ enum {
  *                  combine. Stages not launched leave their events untouched.
  *  flags         : bit 0 = run the first level in its latency shape (one
  *                  warp per task) instead of its throughput shape.
+ *                  bit 1 = test knob: the band level fills its shared-memory
+ *                  code buffers with garbage before each task, so the tests
+ *                  see the worst case of stale shared memory. Results never
+ *                  depend on it.
  *  first_slots   : 0 = automatic; 20, 24, 28 or 32 force the width of the
  *                  first window (one lane per task) when the first level is
  *                  level 1. Results never depend on it.

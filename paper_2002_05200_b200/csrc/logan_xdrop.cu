@@ -528,6 +528,7 @@ int logan_xdrop_batch(const uint8_t *seq_pool, int32_t seq_fmt, int64_t pool_len
     P.k = k;
     P.match = sc.match; P.mismatch = sc.mismatch; P.gap = sc.gap; P.xdrop = sc.xdrop;
     P.one = 1;
+    P.poison = (opt && (opt->flags & 2)) ? 1 : 0;
 
     // extension lengths beyond the wide scratch would overflow it: such pairs
     // are rejected up front by the caller-side bound (documented in the header)

@@ -131,10 +131,13 @@ template <> struct BandCodes<LOGAN_SEQ_2BIT> {
     __device__ __forceinline__ static int32_t word_off(int32_t off) { return off >> 3; }
     __device__ __forceinline__ static uint32_t bit_off(int32_t off) { return 4u * (uint32_t)(off & 7); }
     __device__ __forceinline__ static void masks(const BandCodes &a, const BandCodes &b, uint32_t (&mk)[4]) {
-        // codes are 0..3: (a ^ b) + 7 per nibble sets the nibble's bit 3 iff they
-        // differ and never carries; z has slot 2k+1's flag at bit 7 of byte k,
-        // z << 4 has slot 2k's flag there
-        const uint32_t z = (a.x ^ b.x) + 0x77777777u;
+        // codes are 0..3: ((a ^ b) & 3) + 7 per nibble sets the nibble's bit 3 iff
+        // they differ and never carries. The & 3 (one LOP3 with the XOR) matters:
+        // nibbles of slots outside the staged code range hold stale shared memory,
+        // and a stale nibble > 8 would carry into the flag of the slot above it
+        // (those slots are masked dead afterwards, their neighbours are not).
+        // z has slot 2k+1's flag at bit 7 of byte k, z << 4 has slot 2k's flag there
+        const uint32_t z = ((a.x ^ b.x) & 0x33333333u) + 0x77777777u;
         const uint32_t z4 = z << 4;
 #pragma unroll
         for (int k = 0; k < 4; ++k)
@@ -228,6 +231,9 @@ struct BandCta {
         const uint4 z = make_uint4(D16X2, D16X2, D16X2, D16X2);
 #pragma unroll 4
         for (int q = tid; q < 2 * BAND_WORDS / 4; q += BAND_NT) v4[q] = z;
+        if (P.poison) {  // test knob: code buffers start as garbage (stale smem is arbitrary)
+            for (int q = tid; q < 2 * (S::CAPW + S::MIRROR); q += BAND_NT) ca()[q] = 0xffffffffu;  // every nibble 15: the worst case for the mismatch-flag carry
+        }
         __syncthreads();
     }
 
@@ -293,6 +299,9 @@ struct BandCta {
     // 1 = finished, 2 = band too wide for the ring.
     template <int PAR>
     __device__ __forceinline__ int step(const Params &P) {
+#ifdef LOGAN_BAND_SYNC
+        __syncthreads();
+#endif
         const int32_t d = t.d + 1;
         const int32_t ch = PAR ? (d + 1) >> 1 : d >> 1, fh = PAR ? (d - 1) >> 1 : d >> 1;
 
@@ -513,7 +522,11 @@ __global__ void __launch_bounds__(BAND_NT) k_band(const Params P, const LevelIO 
         if (pos >= count) return;
         const uint32_t task = io.list[pos];
         int rc = 2;
+#ifdef LOGAN_BAND_SKIP
+        if (false) {
+#else
         if (P.xdrop <= BAND_XMAX) {
+#endif
             const uint32_t rec = io.in_recs ? io.in_recs[pos] : NO_REC;
             if (rec != NO_REC) c.resume(P, io.rec_in + (size_t)rec * io.rec_in_stride);
             else c.init(P, task);

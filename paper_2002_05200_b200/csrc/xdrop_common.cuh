@@ -28,6 +28,7 @@ struct Params {
     int32_t k;
     int32_t match, mismatch, gap, xdrop;
     int32_t one;  // = 1 at run time; opaque to the compiler (see Window::cell)
+    int32_t poison;  // test knob (options.flags bit 1): fill shared staging buffers with garbage first
 };
 
 // Result of one extension task (L or R of one pair), 24 bytes.

@@ -280,6 +280,26 @@ def test_forced_handover_is_exact(period):
                             what=f"handover {period} level {lvl} lat={lat} X={X}")
 
 
+@pytest.mark.parametrize("fmt", FMTS)
+def test_band_level_with_stale_shared_memory(fmt):
+    """The band level's code buffers start as garbage (options.flags bit 1):
+    stale codes of slots outside the staged range must not change the mismatch
+    flags of the staged slots next to them (regression: a stale nibble > 8
+    carried into its neighbour's flag, so an extension could miss its last
+    cell depending on what an earlier kernel left in shared memory)."""
+    for seed in (102, 106, 140):
+        b = _mixed_pairs(seed)
+        for X in (3, 10, 30):
+            ref = oracle_run(b, X)
+            for lvl, ho in ((1, 6), (2, 40), (6, 6), (7, 0)):
+                db = logan.to_device(b, fmt)
+                out, cells = logan.xdrop_batch(db, 1, -1, -1, X, first_level=lvl, latency_first=True,
+                                               handover=ho, poison=True)
+                torch.cuda.synchronize()
+                assert_same(out.cpu().numpy(), cells.cpu().numpy().view(np.uint64), *ref,
+                            what=f"poisoned band seed={seed} X={X} level {lvl} handover {ho} fmt={fmt}")
+
+
 def test_mass_overflow_with_helpers():
     """Most tasks overflow the first window (X far above its width): helpers take
     what they can while level 1 runs, the next launch takes the rest; results exact."""
