@@ -321,8 +321,8 @@ def main():
             traffic = tj.get(key)
         except (OSError, ValueError):
             traffic = None
-    level_names = ["window32", "window64", "window128", "window256", "window512", "window1024",
-                   "band8192", "wide_cta"]
+    level_names = [f"window{logan._lib.load().logan_level_width(lv + 1, w.xdrop, db.max_ext_len, 0)}" for lv in range(6)] + \
+        ["band8192", "wide_cta"]
     roofline = {"bound": "alu", "achieved": achieved_tops, "peak": peak_tops, "unit": "TOP/s",
                 "frac": achieved_tops / peak_tops, "traffic": traffic,
                 "kernel": f"{'k_window' if dom_level < 6 else ('k_band' if dom_level == 6 else 'k_wide')} "

@@ -77,7 +77,8 @@ enum {
 /* Options (may be passed as NULL = all defaults).
  *  first_level   : 0 = automatic from xdrop; 1..6 force the first
  *                  register-window level (windows of 32, 64, 128, 256, 512,
- *                  1024 diagonal slots); 7 starts every task on the band
+ *                  1024 diagonal slots; level 6 is 640 or 768 slots wide
+ *                  when 480 < xdrop <= 680); 7 starts every task on the band
  *                  level (one CTA per task, the band as int16 pairs in an
  *                  8192-slot shared-memory ring; used for X <= 30000, wider
  *                  bands go on);
@@ -215,6 +216,16 @@ const char *logan_strerror(int status);
 
 /* ABI version the library was built with (LOGAN_ABI_VERSION). */
 int logan_abi_version(void);
+
+/* Diagnostics (host only, no GPU needed): the diagonal-slot width of the
+ * register window that level `level` (1..6) would run in a call with this
+ * xdrop, max_ext_len (as for logan_workspace_bytes) and options.first_slots
+ * (0 = automatic): level 1 is 20, 24, 28 or 32 slots, levels 2..5 are 64,
+ * 128, 256 and 512, level 6 is 640, 768, 896 or 1024. Returns 0 for levels
+ * that are not register windows (7 = band level, 8 = CTA level) or out of
+ * range. Results never depend on the widths; bench.py uses this to name the
+ * kernel it reports. */
+int logan_level_width(int32_t level, int32_t xdrop, int64_t max_ext_len, int32_t first_slots);
 
 #ifdef __cplusplus
 }

@@ -19,7 +19,7 @@ LOGAN_OK, LOGAN_EINVAL, LOGAN_ECUDA, LOGAN_ENOSPC = 0, 1, 2, 3
 #: every symbol include/logan_xdrop.h declares
 EXPORTS = ("logan_workspace_bytes", "logan_xdrop_batch", "logan_host_arena_bytes",
            "logan_xdrop_batch_host", "logan_xdrop_batch_host_async", "logan_strerror",
-           "logan_abi_version")
+           "logan_abi_version", "logan_level_width")
 
 
 class Scoring(ctypes.Structure):
@@ -81,6 +81,8 @@ def load(path: str | None = None) -> ctypes.CDLL:
     lib.logan_strerror.restype = ctypes.c_char_p
     lib.logan_abi_version.argtypes = []
     lib.logan_abi_version.restype = ctypes.c_int
+    lib.logan_level_width.argtypes = [i32, i32, i64, i32]
+    lib.logan_level_width.restype = ctypes.c_int
     _lib = lib
     return lib
 

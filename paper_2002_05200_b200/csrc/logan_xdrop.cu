@@ -258,16 +258,25 @@ static cudaError_t launch_first(int w0, bool helpers, const Params &P, const Lev
 
 template <int FMT>
 static cudaError_t launch_width(int wi, bool latency, bool helpers, const Params &P, const LevelIO &io,
-                                const LevelIO &hio, int sms, cudaStream_t s, int w0) {
+                                const LevelIO &hio, int sms, cudaStream_t s, int w0, int w5) {
     if (wi == 0 && !(latency && w0 == 32)) return launch_first<FMT>(w0, helpers && !latency, P, io, hio, sms, s);
     if (helpers && !latency) {
         switch (wi) {
             case 1: return launch_win<2, 32, FMT, LOGAN_HSHAPE(128)>(P, io, hio, sms, s);
             case 2: return launch_win<4, 32, FMT, LOGAN_HSHAPE(256)>(P, io, hio, sms, s);
             case 3: return launch_win<8, 32, FMT, LOGAN_HSHAPE(512)>(P, io, hio, sms, s);
-            case 4: return launch_win<16, 32, FMT, 32, 32>(P, io, hio, sms, s);
+            case 4:
+                if (w5 == 640) return launch_win<16, 32, FMT, 32, 20>(P, io, hio, sms, s);
+                if (w5 == 768) return launch_win<16, 32, FMT, 32, 24>(P, io, hio, sms, s);
+                if (w5 == 896) return launch_win<16, 32, FMT, 32, 28>(P, io, hio, sms, s);
+                return launch_win<16, 32, FMT, 32, 32>(P, io, hio, sms, s);
             default: break;
         }
+    }
+    if (wi == 5) {  // the top window: one warp per task, R = w5 / 32 slots per lane
+        if (w5 == 640) return launch_win<32, 20, FMT, 0, 0>(P, io, hio, sms, s);
+        if (w5 == 768) return launch_win<32, 24, FMT, 0, 0>(P, io, hio, sms, s);
+        if (w5 == 896) return launch_win<32, 28, FMT, 0, 0>(P, io, hio, sms, s);
     }
     switch (wi * 2 + (latency ? 1 : 0)) {
         case 1: return launch_win<32, 1, FMT, 0, 0>(P, io, hio, sms, s);
@@ -295,6 +304,18 @@ static int auto_first_level(int32_t xdrop) {
     if (xdrop <= 1000) return 5; // W = 1024
     if (xdrop <= BAND_XMAX) return BAND_LEVEL;  // the band follows the alignment's width
     return WIDE_LEVEL;           // unbounded CTA level
+}
+
+// Width of the top window level (one warp per task): 640, 768 or 896 slots when
+// X starts tasks there with a band of about X + 8 slots (X in (480, 820]), so
+// the window is not half empty; 1024 otherwise (X near 1000, or bands that
+// escalated from narrower windows, e.g. spurious pairs at small X).
+static int auto_top_width(int32_t xdrop) {
+    if (xdrop <= 480) return 1024;
+    if (xdrop <= 560) return 640;
+    if (xdrop <= 680) return 768;
+    if (xdrop <= 820) return 896;
+    return 1024;
 }
 
 // Slots of the first window: the band of true pairs is about X + 8 slots wide at
@@ -348,7 +369,8 @@ static int run_batch(const Params &P, const logan_options_t *opt, logan_result_t
     if (first < 0 || first > NLEVEL - 1) return LOGAN_EINVAL;
     uint32_t *recs[2] = {(uint32_t *)(ws + L.recsA), (uint32_t *)(ws + L.recsB)};
     const int w0 = (opt && opt->first_slots > 0) ? opt->first_slots : auto_first_slots(P.xdrop, L.wide_stride - 2);
-    auto width_of = [&](int lv) { return lv == 0 ? w0 : kWidth[lv]; };
+    const int w5 = auto_top_width(P.xdrop);
+    auto width_of = [&](int lv) { return lv == 0 ? w0 : (lv == NWIDTH - 1 ? w5 : kWidth[lv]); };
     const uint32_t *in_list = queue;
     const uint32_t *in_recs = nullptr;
     const int32_t *rec_in = nullptr;
@@ -408,14 +430,14 @@ static int run_batch(const Params &P, const logan_options_t *opt, logan_result_t
                     if (cudaMemsetAsync(lists[out_sel], 0xff, sizeof(uint32_t) * (size_t)L.ntask, s) != cudaSuccess)
                         return LOGAN_ECUDA;
                 }
-                e = launch_width<FMT>(lv, latency_first, helpers, P, io, hio, sms, s, w0);
+                e = launch_width<FMT>(lv, latency_first, helpers, P, io, hio, sms, s, w0, w5);
             } else {
                 io.max_count = latency_below;
-                e = launch_width<FMT>(lv, true, false, P, io, io, sms, s, w0);
+                e = launch_width<FMT>(lv, true, false, P, io, io, sms, s, w0, w5);
                 if (e == cudaSuccess) {
                     io.min_count = latency_below;
                     io.max_count = 0xffffffffu;
-                    e = launch_width<FMT>(lv, false, false, P, io, io, sms, s, w0);
+                    e = launch_width<FMT>(lv, false, false, P, io, io, sms, s, w0, w5);
                 }
             }
         } else if (lv == BAND_LEVEL) {
@@ -458,6 +480,13 @@ using namespace logan;
 extern "C" {
 
 int logan_abi_version(void) { return LOGAN_ABI_VERSION; }
+
+int logan_level_width(int32_t level, int32_t xdrop, int64_t max_ext_len, int32_t first_slots) {
+    if (level == 1) return first_slots > 0 ? first_slots : auto_first_slots(xdrop, max_ext_len);
+    if (level >= 2 && level <= NWIDTH - 1) return kWidth[level - 1];
+    if (level == NWIDTH) return auto_top_width(xdrop);
+    return 0;
+}
 
 const char *logan_strerror(int status) {
     switch (status) {

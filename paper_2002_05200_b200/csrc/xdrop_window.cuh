@@ -355,8 +355,8 @@ struct Window {
         for (int q = 0; q < NW; ++q) X[q] = Aw[q] ^ Bw[q];
 
         // (4) cells
-        int32_t kq[4] = {INT32_MIN, INT32_MIN, INT32_MIN, INT32_MIN};
-        uint32_t dq[4] = {0, 0, 0, 0};
+        int32_t kq[4];
+        uint32_t dq[4];
         constexpr int RQ = (R + 3) / 4;
         if (PAR == 1) {
             int32_t nb = DEAD;  // E[R] of this lane = E[0] of the next lane
@@ -383,22 +383,28 @@ struct Window {
                 E[r] = cell(O[r], left, E[r], mis, gp, fg, sma, smi, P.one);
             }
         }
-        // keys u * KEYMUL + 1023 - r and sign chains over the new antidiagonal
+        // keys u * KEYMUL + 1023 - r and dead masks over the new antidiagonal
 #pragma unroll
         for (int r = R - 1; r >= 0; --r) {
             const int32_t u = PAR ? O[r] : E[r];
             const int c = r / RQ;
-            kq[c] = max(kq[c], u * KEYMUL + (1023 - r));
-            // append sign(u) (1 = dead) as bit (r - c*RQ): dq = 2*dq + (u >>> 31)
+            const bool top = (r == R - 1) || (r == (c + 1) * RQ - 1);  // first slot of chain c
+            const int32_t key = u * KEYMUL + (1023 - r);
+            kq[c] = top ? key : max(kq[c], key);
             if (LOGAN_MASK_FMA_CHAINS > c) {  // two IMADs on the FMA pipe
+                // append sign(u) (1 = dead) as bit (r - c*RQ): dq = 2*dq + (u >>> 31)
                 uint32_t sg;
                 asm("mul.hi.u32 %0, %1, %2;" : "=r"(sg) : "r"((uint32_t)u), "r"(two));
-                asm("mad.lo.u32 %0, %1, %2, %3;" : "=r"(dq[c]) : "r"(dq[c]), "r"(two), "r"(sg));
-            } else {  // one funnel shift on the ALU pipe
-                dq[c] = __funnelshift_l((uint32_t)u, dq[c], 1);
+                if (top) dq[c] = sg;
+                else asm("mad.lo.u32 %0, %1, %2, %3;" : "=r"(dq[c]) : "r"(dq[c]), "r"(two), "r"(sg));
+            } else {  // one funnel shift on the ALU pipe (same bit order)
+                dq[c] = top ? ((uint32_t)u >> 31) : __funnelshift_l((uint32_t)u, dq[c], 1);
             }
         }
-        int32_t kmax = max(max(kq[0], kq[1]), max(kq[2], kq[3]));
+        int32_t kmax = kq[0];
+#pragma unroll
+        for (int c = 1; c < 4; ++c)
+            if (c * RQ < R) kmax = max(kmax, kq[c]);
         uint32_t dead = 0;
 #pragma unroll
         for (int c = 0; c < 4; ++c)

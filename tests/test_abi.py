@@ -54,6 +54,12 @@ def test_library_is_sm100a(lib):
 
 def test_host_side_checks_without_gpu(lib):
     assert lib.logan_abi_version() == 1
+    # window widths by level (diagnostics; results never depend on them)
+    assert lib.logan_level_width(1, 20, 2500, 0) == 28 and lib.logan_level_width(1, 20, 9000, 0) == 32
+    assert lib.logan_level_width(1, 10, 2500, 0) == 20 and lib.logan_level_width(1, 20, 2500, 24) == 24
+    assert [lib.logan_level_width(lv, 50, 2500, 0) for lv in range(2, 6)] == [64, 128, 256, 512]
+    assert [lib.logan_level_width(6, x, 2500, 0) for x in (50, 500, 600, 700, 1000)] == [1024, 640, 768, 896, 1024]
+    assert lib.logan_level_width(7, 5000, 2500, 0) == 0 and lib.logan_level_width(0, 20, 2500, 0) == 0
     assert lib.logan_strerror(1) == b"invalid argument"
     assert lib.logan_workspace_bytes(-1, 0) == 0
     small, big = lib.logan_workspace_bytes(10, 100), lib.logan_workspace_bytes(1000, 100)

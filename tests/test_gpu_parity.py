@@ -300,6 +300,23 @@ def test_band_level_with_stale_shared_memory(fmt):
                             what=f"poisoned band seed={seed} X={X} level {lvl} handover {ho} fmt={fmt}")
 
 
+@pytest.mark.parametrize("X", [481, 560, 600, 680, 820])
+def test_top_window_widths(X):
+    """Level 6 runs 640-, 768- or 896-slot windows for 480 < X <= 820: as the
+    automatic first level, forced hand-overs into and out of it (from the
+    512-slot level, into the band level), and both pool formats."""
+    w = datagen.CONFIGS[1].with_(xdrop=X)
+    b = datagen.generate(w, n_pairs=24)
+    ref = oracle_run(b, X)
+    for fmt in FMTS:
+        for lvl, ho in ((None, 0), (5, 0), (5, 60), (6, 40)):
+            db = logan.to_device(b, fmt)
+            out, cells = logan.xdrop_batch(db, 1, -1, -1, X, first_level=lvl, handover=ho)
+            torch.cuda.synchronize()
+            assert_same(out.cpu().numpy(), cells.cpu().numpy().view(np.uint64), *ref,
+                        what=f"top window X={X} level {lvl} handover {ho} fmt={fmt}")
+
+
 def test_mass_overflow_with_helpers():
     """Most tasks overflow the first window (X far above its width): helpers take
     what they can while level 1 runs, the next launch takes the rest; results exact."""
