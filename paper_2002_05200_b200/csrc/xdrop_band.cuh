@@ -299,9 +299,6 @@ struct BandCta {
     // 1 = finished, 2 = band too wide for the ring.
     template <int PAR>
     __device__ __forceinline__ int step(const Params &P) {
-#ifdef LOGAN_BAND_SYNC
-        __syncthreads();
-#endif
         const int32_t d = t.d + 1;
         const int32_t ch = PAR ? (d + 1) >> 1 : d >> 1, fh = PAR ? (d - 1) >> 1 : d >> 1;
 
@@ -366,7 +363,10 @@ struct BandCta {
         int32_t lc = -1;                        // last chunk with a live cell
         if (hlo <= hhi) {
 #pragma unroll 1
-            for (int32_t c8w = c8base + 32 * warp; c8w <= c8last; c8w += BAND_NT) {
+            // the highest warp takes the first chunks of every pass: in a partial
+            // last pass warp 0, which has the per-antidiagonal extra work (exact
+            // extents, cell count, argmax) after the barrier, is the idle one
+            for (int32_t c8w = c8base + 32 * (BAND_NW - 1 - warp); c8w <= c8last; c8w += BAND_NT) {
                 const int32_t c8 = c8w + lane;
                 const int32_t s0 = 8 * c8;
                 const bool active = c8 <= c8last;
@@ -522,11 +522,7 @@ __global__ void __launch_bounds__(BAND_NT) k_band(const Params P, const LevelIO 
         if (pos >= count) return;
         const uint32_t task = io.list[pos];
         int rc = 2;
-#ifdef LOGAN_BAND_SKIP
-        if (false) {
-#else
         if (P.xdrop <= BAND_XMAX) {
-#endif
             const uint32_t rec = io.in_recs ? io.in_recs[pos] : NO_REC;
             if (rec != NO_REC) c.resume(P, io.rec_in + (size_t)rec * io.rec_in_stride);
             else c.init(P, task);
