@@ -229,3 +229,75 @@ def from_strings(pairs, k: int, w: Workload | None = None) -> Batch:
     return Batch(w, 0, np.array(qo_, np.int64), np.array(ql_, np.int32), np.array(to_, np.int64),
                  np.array(tl_, np.int32), np.array(qs_, np.int32), np.array(ts_, np.int32),
                  pool_len, pu8, p2)
+
+
+# ---------------------------------------------------------------------------
+# Protein-like pairs for the substitution-matrix generalisation (SURVEY.md §8f
+# row 4; the paper names protein alignment as future work). Pure numpy,
+# counter-based per pair like the DNA generator: pair p depends only on
+# (seed, p). Holds none of the method's arithmetic: the matrix below is an
+# INPUT of the method (like match / mismatch), not a computation of it.
+PROTEIN_ALPHABET = 20
+PROTEIN_SEED = SEED_BASE + 7
+
+
+def protein_matrix(seed: int = PROTEIN_SEED) -> np.ndarray:
+    """A synthetic symmetric 20 x 20 substitution matrix shaped like the
+    BLOSUM family (NOT BLOSUM itself): diagonal 4..11, off-diagonal -4..1."""
+    rng = np.random.default_rng(seed)
+    off = np.triu(rng.integers(-4, 2, size=(PROTEIN_ALPHABET, PROTEIN_ALPHABET)), 1)
+    m = off + off.T
+    m[np.diag_indices(PROTEIN_ALPHABET)] = rng.integers(4, 12, PROTEIN_ALPHABET)
+    return m.astype(np.int8)
+
+
+def _mutate_protein(rng, t: np.ndarray, u: int, k: int, sub: float, indel: float) -> tuple[np.ndarray, int]:
+    """One read from template t: per residue a substitution (prob sub), a
+    deletion (indel/2) or an insertion after it (indel/2); residues [u, u+k)
+    (the seed) are copied verbatim. Returns (read, read position of t[u])."""
+    L = len(t)
+    r = rng.random(L)
+    subm = r < sub
+    delm = (r >= sub) & (r < sub + indel / 2)
+    insm = (r >= sub + indel / 2) & (r < sub + indel)
+    subm[u:u + k] = delm[u:u + k] = insm[u:u + k] = False
+    codes = t.copy()
+    codes[subm] = (t[subm] + rng.integers(1, PROTEIN_ALPHABET, int(subm.sum()))) % PROTEIN_ALPHABET
+    vals = np.stack([codes, rng.integers(0, PROTEIN_ALPHABET, L)], 1)
+    mask = np.stack([~delm, insm], 1)
+    read = vals[mask].astype(np.uint8)
+    return read, int(mask.ravel()[:2 * u].sum())
+
+
+def protein_pairs(n_pairs: int, len_lo: int = 200, len_hi: int = 1000, sub: float = 0.15,
+                  indel: float = 0.02, k: int = 6, seed: int = PROTEIN_SEED, pair_base: int = 0,
+                  xdrop: int = 50, gap: int = -4) -> Batch:
+    """Homologous protein-like pairs: template length uniform in [len_lo,
+    len_hi], residues uniform over 20 codes; each read = mutate(template) with
+    substitution rate ``sub`` and indel rate ``indel`` per residue (so ~2x
+    between the reads); seed = a k-mer copied verbatim into both reads. The u8
+    pool holds codes 0..19 (not letters)."""
+    w = Workload(f"protein_{len_lo}-{len_hi}_x{xdrop}", n_pairs, tlen_min=len_lo, tlen_max=len_hi,
+                 err=2 * (sub + indel), k=k, match=0, mismatch=0, gap=gap, xdrop=xdrop, seed=seed)
+    qs_, ts_, ql_, tl_, qo_, to_ = [], [], [], [], [], []
+    parts = []
+    off = 0
+    for p in range(n_pairs):
+        rng = np.random.default_rng([seed, pair_base + p])
+        L = int(rng.integers(len_lo, len_hi + 1))
+        t = rng.integers(0, PROTEIN_ALPHABET, L).astype(np.int64)
+        u = int(rng.integers(0, L - k + 1))
+        q, qs = _mutate_protein(rng, t, u, k, sub, indel)
+        r, rs = _mutate_protein(rng, t, u, k, sub, indel)
+        for read, pos, offs, lens, seeds in ((q, qs, qo_, ql_, qs_), (r, rs, to_, tl_, ts_)):
+            pad = (-len(read)) % 4
+            offs.append(off); lens.append(len(read)); seeds.append(pos)
+            parts.append(read); parts.append(np.zeros(pad, np.uint8))
+            off += len(read) + pad
+    pool_len = off
+    pu8 = np.zeros(_pad16(pool_len) + 16, np.uint8)
+    if parts:
+        pu8[:pool_len] = np.concatenate(parts)
+    return Batch(w, pair_base, np.array(qo_, np.int64), np.array(ql_, np.int32), np.array(to_, np.int64),
+                 np.array(tl_, np.int32), np.array(qs_, np.int32), np.array(ts_, np.int32), pool_len, pu8, None,
+                 meta={"alphabet": PROTEIN_ALPHABET})

@@ -65,6 +65,14 @@ def _load():
                                      i64, i64, i64, i64, i64, i64, i32p,
                                      ctypes.POINTER(ctypes.c_uint64), ctypes.c_int]
         lib.oracle_pairs.restype = ctypes.c_int
+        i8p = ctypes.POINTER(ctypes.c_int8)
+        lib.oracle_extend_subst.argtypes = [u8p, i64, u8p, i64, i8p, i64, i64, i64, ctypes.c_int,
+                                            ctypes.POINTER(_Ext)]
+        lib.oracle_extend_subst.restype = ctypes.c_int
+        lib.oracle_pairs_subst.argtypes = [u8p, i64, i64p, i32p, i64p, i32p, i32p, i32p,
+                                           i64, i64, i8p, i64, i64, i64, i32p,
+                                           ctypes.POINTER(ctypes.c_uint64), ctypes.c_int]
+        lib.oracle_pairs_subst.restype = ctypes.c_int
         _lib = lib
     return _lib
 
@@ -140,3 +148,56 @@ def pair(q, t, qs: int, ts: int, k: int, X: int, match: int = 1, mismatch: int =
     out, cells = pairs(pool, 0, [0], [len(qa)], [len(qa)], [len(ta)], [qs], [ts], k,
                        match, mismatch, gap, X, n_threads=1)
     return tuple(int(x) for x in out[0]), int(cells[0])
+
+
+def _subst_table(subst) -> tuple[np.ndarray, int]:
+    t = np.ascontiguousarray(subst, dtype=np.int8)
+    if t.ndim != 2 or t.shape[0] != t.shape[1]:
+        raise ValueError("subst must be a square alphabet x alphabet matrix")
+    return t, t.shape[0]
+
+
+def extend_subst(A, B, X: int, subst, gap: int, full_scan: bool = False) -> ExtResult:
+    """One X-drop extension scored with a substitution matrix:
+    s(a_i, b_j) = subst[a_i][b_j] (codes 0..alphabet-1)."""
+    a, b = _as_u8(A), _as_u8(B)
+    t, alph = _subst_table(subst)
+    out = _Ext()
+    P = ctypes.POINTER
+    st = _load().oracle_extend_subst(a.ctypes.data_as(P(ctypes.c_uint8)), len(a),
+                                     b.ctypes.data_as(P(ctypes.c_uint8)), len(b),
+                                     t.ctypes.data_as(P(ctypes.c_int8)), alph, gap, X, int(full_scan),
+                                     ctypes.byref(out))
+    if st != 0:
+        raise RuntimeError(f"oracle_extend_subst failed with status {st}")
+    return ExtResult(out.best, out.i, out.j, out.cells, out.last_d)
+
+
+def pairs_subst(pool: np.ndarray, q_off, q_len, t_off, t_len, q_seed, t_seed, k: int, subst,
+                gap: int, X: int, pool_len: int | None = None, n_threads: int | None = None):
+    """Batch of pairs in a u8 pool of codes < alphabet, scored with ``subst``
+    -> (int32[n,5] results, uint64[n] cells)."""
+    pool = np.ascontiguousarray(pool, dtype=np.uint8)
+    t, alph = _subst_table(subst)
+    if pool_len is None:
+        pool_len = len(pool)
+    cols = [np.ascontiguousarray(x, dtype=dt) for x, dt in
+            ((q_off, np.int64), (q_len, np.int32), (t_off, np.int64), (t_len, np.int32),
+             (q_seed, np.int32), (t_seed, np.int32))]
+    n = len(cols[0])
+    out = np.zeros((n, 5), dtype=np.int32)
+    cells = np.zeros(n, dtype=np.uint64)
+    if n_threads is None:
+        n_threads = len(os.sched_getaffinity(0))
+    P = ctypes.POINTER
+    st = _load().oracle_pairs_subst(
+        pool.ctypes.data_as(P(ctypes.c_uint8)), pool_len,
+        cols[0].ctypes.data_as(P(ctypes.c_int64)), cols[1].ctypes.data_as(P(ctypes.c_int32)),
+        cols[2].ctypes.data_as(P(ctypes.c_int64)), cols[3].ctypes.data_as(P(ctypes.c_int32)),
+        cols[4].ctypes.data_as(P(ctypes.c_int32)), cols[5].ctypes.data_as(P(ctypes.c_int32)),
+        n, k, t.ctypes.data_as(P(ctypes.c_int8)), alph, gap, X,
+        out.ctypes.data_as(P(ctypes.c_int32)), cells.ctypes.data_as(P(ctypes.c_uint64)),
+        int(n_threads))
+    if st != 0:
+        raise RuntimeError(f"oracle_pairs_subst failed with status {st}")
+    return out, cells

@@ -18,8 +18,10 @@ TEST INFRASTRUCTURE ONLY (see ``oracle/__init__.py``).
 from __future__ import annotations
 
 
-def full_dp(A: str, B: str, match: int = 1, mismatch: int = -1, gap: int = -1):
-    """Full prefix DP matrix (m+1) x (n+1) as a list of lists (eq. P:85)."""
+def full_dp(A, B, match: int = 1, mismatch: int = -1, gap: int = -1, subst=None):
+    """Full prefix DP matrix (m+1) x (n+1) as a list of lists (eq. P:85).
+    With ``subst`` (a square matrix indexed by symbol codes) the substitution
+    score is subst[a_i][b_j] instead of match / mismatch."""
     m, n = len(A), len(B)
     S = [[0] * (n + 1) for _ in range(m + 1)]
     for i in range(1, m + 1):
@@ -28,16 +30,19 @@ def full_dp(A: str, B: str, match: int = 1, mismatch: int = -1, gap: int = -1):
         S[0][j] = j * gap
     for i in range(1, m + 1):
         for j in range(1, n + 1):
-            s = match if A[i - 1] == B[j - 1] else mismatch
+            if subst is not None:
+                s = subst[A[i - 1]][B[j - 1]]
+            else:
+                s = match if A[i - 1] == B[j - 1] else mismatch
             S[i][j] = max(S[i - 1][j - 1] + s, S[i][j - 1] + gap, S[i - 1][j] + gap)
     return S
 
 
-def full_dp_best(A: str, B: str, match: int = 1, mismatch: int = -1, gap: int = -1):
+def full_dp_best(A, B, match: int = 1, mismatch: int = -1, gap: int = -1, subst=None):
     """(best, i*, j*) of the unpruned prefix alignment: best = max(0, max S);
     argmax = the cell with S = best on the smallest antidiagonal i+j, then the
     smallest i; (0, 0) when best = 0 (the empty alignment)."""
-    S = full_dp(A, B, match, mismatch, gap)
+    S = full_dp(A, B, match, mismatch, gap, subst)
     m, n = len(A), len(B)
     best, bi, bj = 0, 0, 0
     for d in range(0, m + n + 1):

@@ -38,6 +38,10 @@
  * definition, so skipping it changes nothing. `full_scan = 1` visits every
  * column of the antidiagonal instead (tests check both give the same result).
  *
+ * Substitution matrices (protein alignment is the paper's
+ * future work): oracle_extend_subst / oracle_pairs_subst replace
+ * "a_i == b_j ? match : mismatch" by subst[a_i * alph + b_j] and nothing else.
+ *
  * Parity pins (tests/test_oracle_pins.py): brute-force full DP at X = inf,
  * closed forms (identical reads, disjoint alphabets, identical prefix + all
  * mismatch tail, X = 0 on identical reads), hand-worked examples
@@ -110,9 +114,41 @@ static void antidiag_clear(antidiag_t *a) {
     a->has_live = 0;
 }
 
+/*
+ * Substitution score s(a_i, b_j) of eq. P:85: match / mismatch, or, in the
+ * substitution-matrix generalisation (protein alignment is
+ * the paper's stated future work), the matrix entry subst[a * alph + b].
+ */
+static int64_t sub_score(uint8_t a, uint8_t b, int64_t match, int64_t mismatch,
+                         const int8_t *subst, int64_t alph) {
+    if (subst) return subst[(int64_t)a * alph + b];
+    return a == b ? match : mismatch;
+}
+
+static int extend_impl(const uint8_t *A, int64_t m, const uint8_t *B, int64_t n,
+                       int64_t match, int64_t mismatch, const int8_t *subst, int64_t alph,
+                       int64_t gap, int64_t X, int full_scan, oracle_ext_t *out);
+
 int oracle_extend(const uint8_t *A, int64_t m, const uint8_t *B, int64_t n,
                   int64_t match, int64_t mismatch, int64_t gap, int64_t X,
                   int full_scan, oracle_ext_t *out) {
+    return extend_impl(A, m, B, n, match, mismatch, NULL, 0, gap, X, full_scan, out);
+}
+
+/* The same extension with s(a, b) = subst[a * alph + b]; every code of A and B
+ * must be < alph (ORACLE_EINVAL otherwise). */
+int oracle_extend_subst(const uint8_t *A, int64_t m, const uint8_t *B, int64_t n,
+                        const int8_t *subst, int64_t alph, int64_t gap, int64_t X,
+                        int full_scan, oracle_ext_t *out) {
+    if (!subst || alph < 1 || alph > 256) return ORACLE_EINVAL;
+    for (int64_t i = 0; i < m; ++i) if (A[i] >= alph) return ORACLE_EINVAL;
+    for (int64_t j = 0; j < n; ++j) if (B[j] >= alph) return ORACLE_EINVAL;
+    return extend_impl(A, m, B, n, 0, 0, subst, alph, gap, X, full_scan, out);
+}
+
+static int extend_impl(const uint8_t *A, int64_t m, const uint8_t *B, int64_t n,
+                       int64_t match, int64_t mismatch, const int8_t *subst, int64_t alph,
+                       int64_t gap, int64_t X, int full_scan, oracle_ext_t *out) {
     if (!out || m < 0 || n < 0 || X < 0 || (m > 0 && !A) || (n > 0 && !B)) return ORACLE_EINVAL;
     out->best = 0;
     out->i = 0;
@@ -209,7 +245,7 @@ int oracle_extend(const uint8_t *A, int64_t m, const uint8_t *B, int64_t n,
             int64_t v = 0;
             /* diagonal predecessor (i-1, j-1) on d-2 */
             if (i >= 1 && j >= 1 && prev2_exists && is_live(p2, i - 1)) {
-                int64_t s = (A[i - 1] == B[j - 1]) ? match : mismatch;
+                int64_t s = sub_score(A[i - 1], B[j - 1], match, mismatch, subst, alph);
                 int64_t c = p2->val[i - 1] + s;
                 if (!have || c > v) v = c;
                 have = 1;
@@ -277,11 +313,26 @@ static uint8_t pool_base(const uint8_t *pool, int fmt, int64_t p) {
  * Right extension: A = q[qs+k:M), B = t[ts+k:N). seed_score = sum over the k
  * seed columns (c-amb-10). Coordinates per c-amb-8.
  */
+static int pair_impl(const uint8_t *pool, int fmt, int64_t pool_len,
+                     int64_t q_off, int64_t q_len, int64_t t_off, int64_t t_len,
+                     int64_t qs, int64_t ts, int64_t k,
+                     int64_t match, int64_t mismatch, const int8_t *subst, int64_t alph,
+                     int64_t gap, int64_t X, oracle_pair_t *res, uint64_t *cells_out);
+
 int oracle_pair(const uint8_t *pool, int fmt, int64_t pool_len,
                 int64_t q_off, int64_t q_len, int64_t t_off, int64_t t_len,
                 int64_t qs, int64_t ts, int64_t k,
                 int64_t match, int64_t mismatch, int64_t gap, int64_t X,
                 oracle_pair_t *res, uint64_t *cells_out) {
+    return pair_impl(pool, fmt, pool_len, q_off, q_len, t_off, t_len, qs, ts, k, match, mismatch,
+                     NULL, 0, gap, X, res, cells_out);
+}
+
+static int pair_impl(const uint8_t *pool, int fmt, int64_t pool_len,
+                     int64_t q_off, int64_t q_len, int64_t t_off, int64_t t_len,
+                     int64_t qs, int64_t ts, int64_t k,
+                     int64_t match, int64_t mismatch, const int8_t *subst, int64_t alph,
+                     int64_t gap, int64_t X, oracle_pair_t *res, uint64_t *cells_out) {
     res->score = INT32_MIN;
     res->q_begin = res->q_end = res->t_begin = res->t_end = -1;
     if (cells_out) *cells_out = 0;
@@ -304,12 +355,21 @@ int oracle_pair(const uint8_t *pool, int fmt, int64_t pool_len,
     for (int64_t j = 1; j <= nR; ++j) BR[j - 1] = pool_base(pool, fmt, t_off + ts + k + j - 1);
 
     int64_t seed = 0;
-    for (int64_t u = 0; u < k; ++u)
-        seed += (pool_base(pool, fmt, q_off + qs + u) == pool_base(pool, fmt, t_off + ts + u)) ? match : mismatch;
+    int bad_code = 0;
+    for (int64_t u = 0; u < k; ++u) {
+        const uint8_t a = pool_base(pool, fmt, q_off + qs + u), b = pool_base(pool, fmt, t_off + ts + u);
+        if (subst && (a >= alph || b >= alph)) bad_code = 1;
+        else seed += sub_score(a, b, match, mismatch, subst, alph);
+    }
 
     oracle_ext_t L, R;
-    int st = oracle_extend(AL, mL, BL, nL, match, mismatch, gap, X, 0, &L);
-    if (st == ORACLE_OK) st = oracle_extend(AR, mR, BR, nR, match, mismatch, gap, X, 0, &R);
+    int st = bad_code ? ORACLE_EINVAL : ORACLE_OK;
+    if (st == ORACLE_OK)
+        st = subst ? oracle_extend_subst(AL, mL, BL, nL, subst, alph, gap, X, 0, &L)
+                   : oracle_extend(AL, mL, BL, nL, match, mismatch, gap, X, 0, &L);
+    if (st == ORACLE_OK)
+        st = subst ? oracle_extend_subst(AR, mR, BR, nR, subst, alph, gap, X, 0, &R)
+                   : oracle_extend(AR, mR, BR, nR, match, mismatch, gap, X, 0, &R);
     free(AL); free(BL); free(AR); free(BR);
     if (st != ORACLE_OK) return st;
 
@@ -337,6 +397,8 @@ typedef struct {
     const int32_t *q_len, *t_len, *q_seed, *t_seed;
     int64_t n;
     int64_t k, match, mismatch, gap, X;
+    const int8_t *subst;
+    int64_t alph;
     oracle_pair_t *out;
     uint64_t *cells;
     int64_t next; /* shared cursor */
@@ -355,10 +417,10 @@ static void *batch_worker(void *arg) {
         int64_t e = b + 8 < job->n ? b + 8 : job->n;
         for (int64_t p = b; p < e; ++p) {
             uint64_t c = 0;
-            int st = oracle_pair(job->pool, job->fmt, job->pool_len, job->q_off[p], job->q_len[p],
-                                 job->t_off[p], job->t_len[p], job->q_seed[p], job->t_seed[p],
-                                 job->k, job->match, job->mismatch, job->gap, job->X,
-                                 &job->out[p], &c);
+            int st = pair_impl(job->pool, job->fmt, job->pool_len, job->q_off[p], job->q_len[p],
+                               job->t_off[p], job->t_len[p], job->q_seed[p], job->t_seed[p],
+                               job->k, job->match, job->mismatch, job->subst, job->alph, job->gap, job->X,
+                               &job->out[p], &c);
             if (job->cells) job->cells[p] = c;
             if (st != ORACLE_OK) {
                 pthread_mutex_lock(&job->mu);
@@ -370,17 +432,47 @@ static void *batch_worker(void *arg) {
     return NULL;
 }
 
+static int pairs_impl(const uint8_t *pool, int fmt, int64_t pool_len,
+                      const int64_t *q_off, const int32_t *q_len,
+                      const int64_t *t_off, const int32_t *t_len,
+                      const int32_t *q_seed, const int32_t *t_seed, int64_t n_pairs,
+                      int64_t k, int64_t match, int64_t mismatch, const int8_t *subst, int64_t alph,
+                      int64_t gap, int64_t X, oracle_pair_t *out, uint64_t *cells, int n_threads);
+
 int oracle_pairs(const uint8_t *pool, int fmt, int64_t pool_len,
                  const int64_t *q_off, const int32_t *q_len,
                  const int64_t *t_off, const int32_t *t_len,
                  const int32_t *q_seed, const int32_t *t_seed, int64_t n_pairs,
                  int64_t k, int64_t match, int64_t mismatch, int64_t gap, int64_t X,
                  oracle_pair_t *out, uint64_t *cells, int n_threads) {
+    return pairs_impl(pool, fmt, pool_len, q_off, q_len, t_off, t_len, q_seed, t_seed, n_pairs, k,
+                      match, mismatch, NULL, 0, gap, X, out, cells, n_threads);
+}
+
+/* Pairs scored with a substitution matrix subst[alph * alph] (u8 pool of
+ * codes < alph): seed score and both extensions use s(a, b) = subst[a*alph+b]. */
+int oracle_pairs_subst(const uint8_t *pool, int64_t pool_len,
+                       const int64_t *q_off, const int32_t *q_len,
+                       const int64_t *t_off, const int32_t *t_len,
+                       const int32_t *q_seed, const int32_t *t_seed, int64_t n_pairs,
+                       int64_t k, const int8_t *subst, int64_t alph, int64_t gap, int64_t X,
+                       oracle_pair_t *out, uint64_t *cells, int n_threads) {
+    if (!subst || alph < 1 || alph > 256) return ORACLE_EINVAL;
+    return pairs_impl(pool, 0, pool_len, q_off, q_len, t_off, t_len, q_seed, t_seed, n_pairs, k,
+                      0, 0, subst, alph, gap, X, out, cells, n_threads);
+}
+
+static int pairs_impl(const uint8_t *pool, int fmt, int64_t pool_len,
+                      const int64_t *q_off, const int32_t *q_len,
+                      const int64_t *t_off, const int32_t *t_len,
+                      const int32_t *q_seed, const int32_t *t_seed, int64_t n_pairs,
+                      int64_t k, int64_t match, int64_t mismatch, const int8_t *subst, int64_t alph,
+                      int64_t gap, int64_t X, oracle_pair_t *out, uint64_t *cells, int n_threads) {
     if (n_pairs < 0 || (n_pairs > 0 && (!pool || !q_off || !q_len || !t_off || !t_len || !q_seed ||
                                         !t_seed || !out)))
         return ORACLE_EINVAL;
     batch_job_t job = {pool, fmt, pool_len, q_off, t_off, q_len, t_len, q_seed, t_seed, n_pairs,
-                       k, match, mismatch, gap, X, out, cells, 0, PTHREAD_MUTEX_INITIALIZER, 0};
+                       k, match, mismatch, gap, X, subst, alph, out, cells, 0, PTHREAD_MUTEX_INITIALIZER, 0};
     if (n_threads < 1) n_threads = 1;
     if (n_threads == 1) {
         batch_worker(&job);

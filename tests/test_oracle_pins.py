@@ -219,3 +219,74 @@ def test_invalid_pairs_get_invalid_result():
     o, c = oracle.pairs(b.pool_u8, 0, b.q_off, b.q_len, b.t_off, b.t_len, [0], [0], 8,
                         1, -1, -1, 10, pool_len=b.pool_len)
     assert tuple(o[0]) == (8, 0, 8, 0, 8) and c[0] == 0
+
+
+# ---------------------------------------------------------------------------
+# Substitution-matrix generalisation
+
+def test_subst_golden_s1():
+    """Hand-worked example S1 (tests/golden/DERIVATIONS.md)."""
+    M = [[3, -2, -1], [-2, 2, -3], [-1, -3, 1]]
+    r = oracle.extend_subst(bytes([0, 1, 2]), bytes([0, 2, 1]), 2, M, -2)
+    assert (r.best, r.i, r.j, r.cells) == (3, 1, 1, 9)
+
+
+def test_subst_infinite_x_is_full_dp():
+    """X = inf with a matrix equals the textbook full prefix DP with that matrix
+    (exhaustive over all strings of length <= 3 on a 3-letter alphabet, a
+    symmetric and an asymmetric matrix, two gap penalties)."""
+    import itertools
+    mats = [[[3, -2, -1], [-2, 2, -3], [-1, -3, 1]], [[2, -3, 1], [0, 4, -2], [-1, -1, 1]]]
+    strs = [list(s) for L in range(4) for s in itertools.product(range(3), repeat=L)]
+    for M in mats:
+        for gap in (-1, -3):
+            for A in strs:
+                for B in strs:
+                    r = oracle.extend_subst(bytes(A), bytes(B), 10 ** 6, M, gap)
+                    best, bi, bj = full_dp_best(A, B, gap=gap, subst=M)
+                    assert (r.best, r.i, r.j, r.cells) == (best, bi, bj, len(A) * len(B)), (A, B, M, gap)
+
+
+def test_subst_reduces_to_match_mismatch():
+    """The matrix M[a][b] = (a == b ? match : mismatch) gives exactly the pinned
+    match / mismatch oracle, extension by extension and pair by pair."""
+    rng = np.random.default_rng(7)
+    for match, mismatch, gap in ((1, -1, -1), (2, -3, -1), (3, -1, -2)):
+        M = [[match if a == b else mismatch for b in range(4)] for a in range(4)]
+        for _ in range(60):
+            A = rng.integers(0, 4, rng.integers(0, 40)).astype(np.uint8)
+            B = A.copy() if rng.random() < 0.5 else rng.integers(0, 4, rng.integers(0, 40)).astype(np.uint8)
+            if len(B) and rng.random() < 0.5:
+                B[rng.integers(0, len(B), 3)] = rng.integers(0, 4, 3)
+            X = int(rng.integers(0, 12))
+            r1 = oracle.extend_subst(A.tobytes(), B.tobytes(), X, M, gap)
+            r2 = oracle.extend(A.tobytes(), B.tobytes(), X, match, mismatch, gap)
+            assert r1 == r2
+    w = datagen.CONFIGS[1]
+    b = datagen.generate(w, n_pairs=40)
+    codes = np.frombuffer(bytes.maketrans(b"ACGT", bytes([0, 1, 2, 3])), np.uint8)[b.pool_u8]
+    M = [[1 if a == c else -1 for c in range(4)] for a in range(4)]
+    o1, c1 = oracle.pairs_subst(codes, b.q_off, b.q_len, b.t_off, b.t_len, b.q_seed, b.t_seed, w.k, M, -1, 50,
+                                pool_len=b.pool_len)
+    o2, c2 = oracle.pairs(b.pool_u8, 0, b.q_off, b.q_len, b.t_off, b.t_len, b.q_seed, b.t_seed, w.k,
+                          1, -1, -1, 50, pool_len=b.pool_len)
+    assert (o1 == o2).all() and (c1 == c2).all()
+
+
+def test_subst_protein_invariants():
+    """Protein-like pairs (datagen.protein_pairs): swap symmetry of best and
+    cells for a symmetric matrix, 0 <= best <= full-DP value at the argmax, and
+    codes outside the alphabet are rejected."""
+    M = datagen.protein_matrix()
+    b = datagen.protein_pairs(6, len_lo=30, len_hi=60)
+    for p in range(b.n_pairs):
+        q = b.pool_u8[b.q_off[p]:b.q_off[p] + b.q_len[p]]
+        t = b.pool_u8[b.t_off[p]:b.t_off[p] + b.t_len[p]]
+        for X in (5, 20, 60):
+            r = oracle.extend_subst(q.tobytes(), t.tobytes(), X, M, -4)
+            s = oracle.extend_subst(t.tobytes(), q.tobytes(), X, M, -4)
+            assert (r.best, r.cells) == (s.best, s.cells)
+            S = full_dp(list(q), list(t), gap=-4, subst=M.tolist())
+            assert 0 <= r.best <= S[r.i][r.j]
+    with pytest.raises(RuntimeError):
+        oracle.extend_subst(bytes([0, 25]), bytes([1]), 5, M, -4)
