@@ -104,15 +104,32 @@ enum {
  *                  window level is handed over to the next level every
  *                  `handover` antidiagonals, exercising the exact hand-over.
  *                  Results never depend on it.
+ *  subst, alphabet : substitution-matrix scoring (the
+ *                  paper names protein alignment as future work).
+ *                  NULL = match / mismatch. Otherwise a DEVICE pointer to an
+ *                  int8 matrix of alphabet x alphabet entries, row-major,
+ *                  1 <= alphabet <= 32, owned by the caller and read during
+ *                  the call (both entry points): s(a_i, b_j) =
+ *                  subst[a_i * alphabet + b_j] replaces "a_i == b_j ? match
+ *                  : mismatch" in eq. P:85 and in the seed score; nothing
+ *                  else changes. Requires seq_fmt = LOGAN_SEQ_U8 with every
+ *                  base a code < alphabet (a larger code reads a 0 score);
+ *                  scoring.match / .mismatch are then ignored (gap < 0 and
+ *                  xdrop as usual). Every task runs on the CTA level with
+ *                  the table in shared memory.
  */
 #define LOGAN_N_STAGES 10
+#define LOGAN_MAX_ALPHABET 32
 typedef struct {
     int32_t first_level;
     int32_t flags;
     void *const *timing_events;
     int32_t handover;
     int32_t first_slots;
-    int64_t reserved[5];
+    const int8_t *subst;
+    int32_t alphabet;
+    int32_t pad_;
+    int64_t reserved[3];
 } logan_options_t;
 
 /* Per-call device-side statistics (optional output in DEVICE memory, may be

@@ -178,9 +178,12 @@ __global__ void k_combine(const Params P, const TaskRes *tres, logan_result_t *o
             const int64_t qo = P.q_off[p], to = P.t_off[p];
             const int32_t qs = P.q_seed[p], ts = P.t_seed[p];
             int32_t seed = 0;  // ungapped seed score (c-amb-10)
-            for (int32_t u = 0; u < P.k; ++u)
-                seed += (pool_base<FMT>(P, qo + qs + u) == pool_base<FMT>(P, to + ts + u)) ? P.match
-                                                                                             : P.mismatch;
+            for (int32_t u = 0; u < P.k; ++u) {
+                const uint32_t a = pool_base<FMT>(P, qo + qs + u), b = pool_base<FMT>(P, to + ts + u);
+                if (P.subst) seed += (a < (uint32_t)P.alphabet && b < (uint32_t)P.alphabet)
+                                         ? P.subst[a * P.alphabet + b] : 0;
+                else seed += a == b ? P.match : P.mismatch;
+            }
             r.score = seed + L.best + R.best;
             r.q_begin = qs - L.i;
             r.q_end = qs + P.k + R.i;
@@ -366,6 +369,7 @@ static int run_batch(const Params &P, const logan_options_t *opt, logan_result_t
     if (!mark(0, 1)) return LOGAN_ECUDA;
 
     int first = (opt && opt->first_level > 0) ? opt->first_level - 1 : auto_first_level(P.xdrop);
+    if (P.subst) first = WIDE_LEVEL;  // substitution matrices: the CTA level, table in shared memory
     if (first < 0 || first > NLEVEL - 1) return LOGAN_EINVAL;
     uint32_t *recs[2] = {(uint32_t *)(ws + L.recsA), (uint32_t *)(ws + L.recsB)};
     const int w0 = (opt && opt->first_slots > 0) ? opt->first_slots : auto_first_slots(P.xdrop, L.wide_stride - 2);
@@ -451,7 +455,8 @@ static int run_batch(const Params &P, const logan_options_t *opt, logan_result_t
                 e = cudaGetLastError();
             }
         } else {
-            k_wide<FMT><<<WIDE_CTAS, WIDE_THREADS, 0, s>>>(P, io, wide, L.wide_stride);
+            if (P.subst) k_wide<FMT, SUBST_THREADS, true><<<WIDE_CTAS, SUBST_THREADS, 0, s>>>(P, io, wide, L.wide_stride);
+            else k_wide<FMT><<<WIDE_CTAS, WIDE_THREADS, 0, s>>>(P, io, wide, L.wide_stride);
             e = cudaGetLastError();
         }
         if (e != cudaSuccess) return LOGAN_ECUDA;
@@ -510,9 +515,12 @@ static int check_args(const uint8_t *seq_pool, int32_t seq_fmt, int64_t pool_len
     if (n_pairs < 0 || n_pairs > ((int64_t)1 << 30)) return LOGAN_EINVAL;
     if (seq_fmt != LOGAN_SEQ_U8 && seq_fmt != LOGAN_SEQ_2BIT) return LOGAN_EINVAL;
     if (k < 0 || pool_len < 0) return LOGAN_EINVAL;
-    if (sc.match <= 0 || sc.match > 127 || sc.mismatch >= 0 || sc.mismatch < -127 || sc.gap >= 0 ||
-        sc.gap < -127 || sc.xdrop < 0 || sc.xdrop > (1 << 19))
+    const bool subst = opt && opt->subst;
+    if (subst && (seq_fmt != LOGAN_SEQ_U8 || opt->alphabet < 1 || opt->alphabet > LOGAN_MAX_ALPHABET))
         return LOGAN_EINVAL;
+    if (!subst && (sc.match <= 0 || sc.match > 127 || sc.mismatch >= 0 || sc.mismatch < -127))
+        return LOGAN_EINVAL;
+    if (sc.gap >= 0 || sc.gap < -127 || sc.xdrop < 0 || sc.xdrop > (1 << 19)) return LOGAN_EINVAL;
     if (opt && (opt->first_level < 0 || opt->first_level > NLEVEL)) return LOGAN_EINVAL;
     if (opt && opt->first_slots != 0 && opt->first_slots != 20 && opt->first_slots != 24 &&
         opt->first_slots != 28 && opt->first_slots != 32)
@@ -558,6 +566,8 @@ int logan_xdrop_batch(const uint8_t *seq_pool, int32_t seq_fmt, int64_t pool_len
     P.match = sc.match; P.mismatch = sc.mismatch; P.gap = sc.gap; P.xdrop = sc.xdrop;
     P.one = 1;
     P.poison = (opt && (opt->flags & 2)) ? 1 : 0;
+    P.subst = opt ? opt->subst : nullptr;
+    P.alphabet = (opt && opt->subst) ? opt->alphabet : 0;
 
     // extension lengths beyond the wide scratch would overflow it: such pairs
     // are rejected up front by the caller-side bound (documented in the header)

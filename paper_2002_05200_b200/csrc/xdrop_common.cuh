@@ -29,6 +29,8 @@ struct Params {
     int32_t match, mismatch, gap, xdrop;
     int32_t one;  // = 1 at run time; opaque to the compiler (see Window::cell)
     int32_t poison;  // test knob (options.flags bit 1): fill shared staging buffers with garbage first
+    const int8_t *subst;  // NULL, or an alphabet x alphabet substitution matrix (device memory)
+    int32_t alphabet;
 };
 
 // Result of one extension task (L or R of one pair), 24 bytes.

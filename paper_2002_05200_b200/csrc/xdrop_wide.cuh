@@ -23,15 +23,34 @@
 namespace logan {
 
 constexpr int WIDE_THREADS = 1024;
-constexpr int WIDE_WARPS = WIDE_THREADS / 32;
+constexpr int SUBST_THREADS = 256;  // substitution-matrix path: narrower CTAs (bands ~X cells)
+constexpr int SUBST_MAX_ALPHABET = 32;
 constexpr int32_t WDEAD = INT32_MIN;
 
-template <int FMT>
-__global__ void __launch_bounds__(WIDE_THREADS) k_wide(const Params P, const LevelIO io,
-                                                       int32_t *scratch, int64_t stride) {
-    __shared__ int32_t s_v[2][WIDE_WARPS], s_i[2][WIDE_WARPS], s_f[2][WIDE_WARPS], s_l[2][WIDE_WARPS];
+// Substitution score s(a_i, b_j) (eq. P:85): match / mismatch, or with SUB the
+// entry of the caller's matrix (protein alignment P:381),
+// staged in shared memory as a 32 x 32 int8 table (codes < alphabet <= 32).
+template <bool SUB>
+__device__ __forceinline__ int32_t subst_score(const Params &P, const int8_t *tab, uint32_t a, uint32_t b) {
+    if (SUB) return (int32_t)tab[(a & 31u) * SUBST_MAX_ALPHABET + (b & 31u)];
+    return a == b ? P.match : P.mismatch;
+}
+
+template <int FMT, int NT = WIDE_THREADS, bool SUB = false>
+__global__ void __launch_bounds__(NT) k_wide(const Params P, const LevelIO io,
+                                             int32_t *scratch, int64_t stride) {
+    constexpr int NWARP = NT / 32;
+    __shared__ int32_t s_v[2][32], s_i[2][32], s_f[2][32], s_l[2][32];
     __shared__ uint32_t s_task;
+    __shared__ int8_t s_tab[SUB ? SUBST_MAX_ALPHABET * SUBST_MAX_ALPHABET : 4];
     const int tid = threadIdx.x, wid = tid >> 5, lane = tid & 31;
+    if (SUB) {
+        for (int q = tid; q < SUBST_MAX_ALPHABET * SUBST_MAX_ALPHABET; q += NT) {
+            const int a = q / SUBST_MAX_ALPHABET, b = q % SUBST_MAX_ALPHABET;
+            s_tab[q] = (a < P.alphabet && b < P.alphabet) ? P.subst[a * P.alphabet + b] : (int8_t)0;
+        }
+        __syncthreads();
+    }
     int32_t *V[3] = {scratch + (int64_t)blockIdx.x * 3 * stride,
                      scratch + (int64_t)blockIdx.x * 3 * stride + stride,
                      scratch + (int64_t)blockIdx.x * 3 * stride + 2 * stride};
@@ -80,7 +99,7 @@ __global__ void __launch_bounds__(WIDE_THREADS) k_wide(const Params P, const Lev
             const int32_t vlo = max(lo, max(0, d - n)), vhi = min(hi, min(m, d));
             const int32_t thr = best - P.xdrop;
             int32_t bv = INT32_MIN, bi = INT32_MAX, lf = INT32_MAX, ll = INT32_MIN;
-            for (int32_t i = vlo + tid; i <= vhi; i += WIDE_THREADS) {
+            for (int32_t i = vlo + tid; i <= vhi; i += NT) {
                 const int32_t j = d - i;
                 bool have = false;
                 int32_t v = 0;
@@ -89,7 +108,7 @@ __global__ void __launch_bounds__(WIDE_THREADS) k_wide(const Params P, const Lev
                     if (p != WDEAD) {
                         const uint32_t a = pool_base<FMT>(P, td.a.base + (int64_t)td.a.dir * (i - 1));
                         const uint32_t b = pool_base<FMT>(P, td.b.base + (int64_t)td.b.dir * (j - 1));
-                        v = p + (a == b ? P.match : P.mismatch);
+                        v = p + subst_score<SUB>(P, s_tab, a, b);
                         have = true;
                     }
                 }
@@ -119,11 +138,12 @@ __global__ void __launch_bounds__(WIDE_THREADS) k_wide(const Params P, const Lev
             __syncthreads();  // also orders the V0 writes before the next antidiagonal
             // every warp folds the 32 partials the same way: lane q reads warp
             // q's slot (one LDS each) and CREDUX combines them
-            const int32_t qv = s_v[par][lane], qi = s_i[par][lane];
+            const bool q_ok = lane < NWARP;
+            const int32_t qv = q_ok ? s_v[par][lane] : INT32_MIN, qi = q_ok ? s_i[par][lane] : INT32_MAX;
             const int32_t gv = __reduce_max_sync(0xffffffffu, qv);
             const int32_t gi = __reduce_min_sync(0xffffffffu, qv == gv ? qi : INT32_MAX);
-            const int32_t gf = __reduce_min_sync(0xffffffffu, s_f[par][lane]);
-            const int32_t gl = __reduce_max_sync(0xffffffffu, s_l[par][lane]);
+            const int32_t gf = __reduce_min_sync(0xffffffffu, q_ok ? s_f[par][lane] : INT32_MAX);
+            const int32_t gl = __reduce_max_sync(0xffffffffu, q_ok ? s_l[par][lane] : INT32_MIN);
             const bool h0 = (gf != INT32_MAX);
             if (h0 && gv > best) { best = gv; ai = gi; aj = d - gi; }  // P:178, strict increase
             if (!h0 && !h1) break;  // P:186, c-amb-7

@@ -79,6 +79,18 @@ def test_host_side_checks_without_gpu(lib):
     st = lib.logan_xdrop_batch(None, 1, 0, None, None, None, None, None, None, 3, 17, sc,
                                None, None, None, None, None, 0, None)
     assert st == _lib.LOGAN_EINVAL  # NULL device pointers
+    # substitution matrices: u8 pool only, 1 <= alphabet <= 32 (checked before any launch)
+    opt = _lib.Options()
+    opt.subst = 0x1000
+    opt.alphabet = 20
+    st = lib.logan_xdrop_batch(None, 1, 0, None, None, None, None, None, None, 3, 17, sc,
+                               ctypes.byref(opt), None, None, None, None, 0, None)
+    assert st == _lib.LOGAN_EINVAL  # 2-bit pool with a matrix
+    opt.alphabet = 33
+    st = lib.logan_xdrop_batch(None, 0, 0, None, None, None, None, None, None, 3, 17, sc,
+                               ctypes.byref(opt), None, None, None, None, 0, None)
+    assert st == _lib.LOGAN_EINVAL  # alphabet too large
+    assert ctypes.sizeof(_lib.Options) == 64  # layout of logan_options_t
 
 
 def test_product_path_does_not_import_oracle():

@@ -464,3 +464,55 @@ def test_band_level_restages_codes_on_long_reads():
             for lvl in (7, None):
                 got = gpu_run(b, X, fmt=fmt, first_level=lvl)
                 assert_same(*got, *ref, what=f"band restage X={X} fmt={fmt} level={lvl}")
+
+
+# --------------------------------------------------------------------------
+# Substitution-matrix scoring (P:381 protein alignment)
+
+def _subst_run(b, M, gap, X, **kw):
+    db = logan.to_device(b, logan.LOGAN_SEQ_U8)
+    sub = torch.as_tensor(np.ascontiguousarray(M, dtype=np.int8)).cuda()
+    out, cells = logan.xdrop_batch(db, 1, -1, gap, X, subst=sub, **kw)
+    torch.cuda.synchronize()
+    return out.cpu().numpy(), cells.cpu().numpy().view(np.uint64)
+
+
+@pytest.mark.parametrize("X", [0, 10, 50, 200])
+def test_subst_protein_pairs(X):
+    """Protein-like pairs (20 codes, synthetic BLOSUM-shaped matrix), bit-exact
+    against oracle.pairs_subst; includes a 30% share of unrelated pairs."""
+    M = datagen.protein_matrix()
+    b = datagen.protein_pairs(300, len_lo=50, len_hi=700, xdrop=X)
+    rng = np.random.default_rng(X)
+    unrel = rng.random(b.n_pairs) < 0.3  # pair an unrelated target with the query
+    b.t_off = np.where(unrel, np.roll(b.t_off, 7), b.t_off)
+    b.t_len = np.where(unrel, np.roll(b.t_len, 7), b.t_len).astype(np.int32)
+    b.t_seed = np.where(unrel, np.minimum(np.roll(b.t_seed, 7), b.t_len - b.workload.k), b.t_seed).astype(np.int32)
+    ref = oracle.pairs_subst(b.pool_u8, b.q_off, b.q_len, b.t_off, b.t_len, b.q_seed, b.t_seed,
+                             b.workload.k, M, -4, X, pool_len=b.pool_len)
+    assert_same(*_subst_run(b, M, -4, X), *ref, what=f"protein subst X={X}")
+
+
+def test_subst_matrix_equals_match_mismatch_path():
+    """A DNA matrix M[a][b] = (a == b ? 1 : -1) on code pools gives the same
+    results as the register-window path on the letter pool."""
+    w = datagen.CONFIGS[1]
+    b = datagen.generate(w, n_pairs=300)
+    ref = gpu_run(b, 50, fmt=logan.LOGAN_SEQ_U8)
+    codes = np.frombuffer(bytes.maketrans(b"ACGT", bytes([0, 1, 2, 3])), np.uint8)[b.pool_u8]
+    bc = datagen.Batch(b.workload, 0, b.q_off, b.q_len, b.t_off, b.t_len, b.q_seed, b.t_seed, b.pool_len, codes)
+    M = [[1 if a == c else -1 for c in range(4)] for a in range(4)]
+    assert_same(*_subst_run(bc, M, -1, 50), *ref, what="DNA matrix vs match/mismatch")
+
+
+def test_subst_tiny_exhaustive_and_asymmetric():
+    """Exhaustive short strings over 3 codes with an asymmetric matrix, several X."""
+    M = [[2, -3, 1], [0, 4, -2], [-1, -1, 1]]
+    strs = [bytes(s) for L in range(5) for s in itertools.product(range(3), repeat=L)]
+    rng = random.Random(5)
+    pairs = [(a, bb, 0, 0) for a in strs for bb in rng.sample(strs, 12)]
+    b = datagen.from_strings(pairs, k=0)
+    for X in (0, 2, 5, 1000):
+        ref = oracle.pairs_subst(b.pool_u8, b.q_off, b.q_len, b.t_off, b.t_len, b.q_seed, b.t_seed, 0, M, -2, X,
+                                 pool_len=b.pool_len)
+        assert_same(*_subst_run(b, M, -2, X), *ref, what=f"tiny subst X={X}")
