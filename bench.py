@@ -41,7 +41,9 @@ def parse_args():
     ap.add_argument("--steps", type=int, default=30)
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
-    ap.add_argument("--config", type=int, default=2, help="datagen.CONFIGS key (BASELINE configs[c-1])")
+    ap.add_argument("--config", type=int, default=2,
+                    help="datagen.CONFIGS key (BASELINE configs[c-1]); 7 = protein-like pairs scored with a "
+                         "substitution matrix (SURVEY §8f row 4)")
     ap.add_argument("--pairs", type=int, default=None, help="pairs per GPU (default: the config's)")
     ap.add_argument("--xdrop", type=int, default=None)
     ap.add_argument("--fmt", choices=["2bit", "u8"], default="2bit")
@@ -58,8 +60,16 @@ def parse_args():
     return ap.parse_args()
 
 
+PROTEIN_CONFIG = 7  # not a BASELINE config: SURVEY §8f row 4 (substitution matrices)
+PROTEIN_PAIRS = 100_000
+
+
 def workload(args):
     import datagen
+    if args.config == PROTEIN_CONFIG:
+        n = args.pairs if args.pairs is not None else PROTEIN_PAIRS
+        w = datagen.protein_pairs(0, xdrop=args.xdrop if args.xdrop is not None else 50).workload
+        return w, n
     w = datagen.CONFIGS[args.config]
     if args.xdrop is not None:
         w = w.with_(xdrop=args.xdrop)
@@ -67,11 +77,37 @@ def workload(args):
     return w, n
 
 
+def make_batch(args, w, n, pair_base=0, u8=False, two_bit=True):
+    import datagen
+    if args.config == PROTEIN_CONFIG:
+        return datagen.protein_pairs(n, pair_base=pair_base, xdrop=w.xdrop, gap=w.gap)
+    return datagen.generate(w, n_pairs=n, pair_base=pair_base, u8=u8, two_bit=two_bit)
+
+
+def run_oracle(batch, w, sl, threads):
+    """The oracle on pairs ``sl`` of the batch -> per-pair cells."""
+    import oracle
+    import datagen
+    if batch.pool_2bit is None:  # protein codes: the substitution-matrix oracle
+        _, cells = oracle.pairs_subst(batch.pool_u8, batch.q_off[sl], batch.q_len[sl], batch.t_off[sl],
+                                      batch.t_len[sl], batch.q_seed[sl], batch.t_seed[sl], w.k,
+                                      datagen.protein_matrix(), w.gap, w.xdrop, pool_len=batch.pool_len,
+                                      n_threads=threads)
+        return cells
+    _, cells = oracle.pairs(batch.pool_2bit, 1, batch.q_off[sl], batch.q_len[sl], batch.t_off[sl],
+                            batch.t_len[sl], batch.q_seed[sl], batch.t_seed[sl], w.k, w.match,
+                            w.mismatch, w.gap, w.xdrop, pool_len=batch.pool_len, n_threads=threads)
+    return cells
+
+
 def config_dict(w, n, fmt, first_level, world):
     d = {"workload": w.name, "pairs_per_gpu": n, "total_pairs": n * world,
-         "read_len": w.tlen_max if w.mode == 0 else f"{w.len_lo}-{w.len_hi}",
+         "read_len": (f"{w.tlen_min}-{w.tlen_max} residues" if w.name.startswith("protein") else
+                      w.tlen_max if w.mode == 0 else f"{w.len_lo}-{w.len_hi}"),
          "error": w.err, "k": w.k, "X": w.xdrop,
-         "scoring": f"{w.match:+d}/{w.mismatch:+d}/{w.gap:+d}", "fmt": fmt,
+         "scoring": (f"synthetic 20x20 substitution matrix (datagen.protein_matrix), gap {w.gap:+d}"
+                     if w.name.startswith("protein") else f"{w.match:+d}/{w.mismatch:+d}/{w.gap:+d}"),
+         "fmt": fmt,
          "seed": w.seed, "l2": "flushed between timed steps (256 MiB write)",
          "parallelism": f"pairs sharded over {world} GPU(s), no data-path collective"}
     if first_level:
@@ -136,9 +172,7 @@ def oracle_sample(batch, w, seconds, threads):
     def run(k):
         sl = slice(0, k)
         t0 = time.perf_counter()
-        _, cells = oracle.pairs(batch.pool_2bit, 1, batch.q_off[sl], batch.q_len[sl], batch.t_off[sl],
-                                batch.t_len[sl], batch.q_seed[sl], batch.t_seed[sl], w.k, w.match,
-                                w.mismatch, w.gap, w.xdrop, pool_len=batch.pool_len, n_threads=threads)
+        cells = run_oracle(batch, w, sl, threads)
         return time.perf_counter() - t0, int(np.asarray(cells, dtype=np.uint64).sum())
 
     k = min(batch.n_pairs, max(threads * 4, 64))
@@ -157,18 +191,15 @@ def run_reference(args):
     import datagen
     w, n = workload(args)
     threads = len(os.sched_getaffinity(0))
-    probe = datagen.generate(w, n_pairs=min(n, max(threads * 64, 512)), two_bit=True, u8=False)
+    probe = make_batch(args, w, min(n, max(threads * 64, 512)))
     cal = oracle_sample(probe, w, args.ref_step_seconds, threads)
     per_step = cal["pairs"]
-    batch = datagen.generate(w, n_pairs=min(n, per_step), two_bit=True, u8=False)
+    batch = make_batch(args, w, min(n, per_step))
     times, cells = [], 0
     for s in range(args.warmup + args.steps):
         import numpy as np
-        import oracle
         t0 = time.perf_counter()
-        _, c = oracle.pairs(batch.pool_2bit, 1, batch.q_off, batch.q_len, batch.t_off, batch.t_len,
-                            batch.q_seed, batch.t_seed, w.k, w.match, w.mismatch, w.gap, w.xdrop,
-                            pool_len=batch.pool_len, n_threads=threads)
+        c = run_oracle(batch, w, slice(0, batch.n_pairs), threads)
         dt = time.perf_counter() - t0
         if s >= args.warmup:
             times.append(dt)
@@ -181,7 +212,7 @@ def run_reference(args):
             "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
             "ms_per_step": 1e3 * total / len(times), "higher_is_better": True, "scaling": "weak",
             "vs_baseline": None, "dtype": "int64", "data": "synthetic",
-            "config": config_dict(w, n, "2bit", 0, 1),
+            "config": config_dict(w, n, "u8" if args.config == PROTEIN_CONFIG else "2bit", 0, 1),
             "cpu_baseline": {"value": value, "unit": UNIT, "cores": threads, "kind": "oracle",
                              "sample": sample},
             "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
@@ -215,8 +246,12 @@ def main():
         dist.init_process_group("nccl", device_id=dev)
 
     w, n = workload(args)
+    protein = args.config == PROTEIN_CONFIG
+    if protein:
+        args.fmt = "u8"
     fmt = logan.LOGAN_SEQ_2BIT if args.fmt == "2bit" else logan.LOGAN_SEQ_U8
-    batch = datagen.generate(w, n_pairs=n, pair_base=rank * n, u8=(args.fmt == "u8"), two_bit=True)
+    batch = make_batch(args, w, n, pair_base=rank * n, u8=(args.fmt == "u8"), two_bit=True)
+    subst = torch.as_tensor(datagen.protein_matrix()).to(dev) if protein else None
     db = logan.to_device(batch, fmt, device=dev)
     ws = logan.make_workspace(n, db.max_ext_len, dev)
     out = torch.empty((n, 5), dtype=torch.int32, device=dev)
@@ -227,7 +262,7 @@ def main():
     def step(events=None, stats=None):
         logan.xdrop_batch(db, w.match, w.mismatch, w.gap, w.xdrop, workspace=ws, out=out, cells=cells,
                           stats=stats, first_level=first, stream=stream, timing_events=events,
-                          latency_first=args.latency_first)
+                          latency_first=args.latency_first, subst=subst)
 
     # one untimed run with device stats: per-level task and cell counts (deterministic)
     st = logan.new_stats(dev)
@@ -321,8 +356,10 @@ def main():
             traffic = tj.get(key)
         except (OSError, ValueError):
             traffic = None
-    level_names = [f"window{logan._lib.load().logan_level_width(lv + 1, w.xdrop, db.max_ext_len, 0)}" for lv in range(6)] + \
-        ["band8192", "wide_cta"]
+    # the library picks window widths from X (from ceil(X / |gap|) with a substitution matrix)
+    xband = -(-w.xdrop // -w.gap) if subst is not None else w.xdrop
+    level_names = [f"window{logan._lib.load().logan_level_width(lv + 1, xband, db.max_ext_len, 0)}"
+                   for lv in range(6)] + ["band8192", "wide_cta"]
     roofline = {"bound": "alu", "achieved": achieved_tops, "peak": peak_tops, "unit": "TOP/s",
                 "frac": achieved_tops / peak_tops, "traffic": traffic,
                 "kernel": f"{'k_window' if dom_level < 6 else ('k_band' if dom_level == 6 else 'k_wide')} "
@@ -350,7 +387,7 @@ def main():
         def e2e_step(s):
             logan.xdrop_batch_host(hp[0], fmt, batch.pool_len, *hp[1:], w.k, w.match, w.mismatch,
                                    w.gap, w.xdrop, arenas[s % 2], out=hout[s % 2], cells=hcells[s % 2],
-                                   first_level=first, stream=streams[s % 2], asynchronous=True)
+                                   first_level=first, stream=streams[s % 2], asynchronous=True, subst=subst)
 
         for s_ in range(2):
             e2e_step(s_)

@@ -113,10 +113,13 @@ enum {
  *                  subst[a_i * alphabet + b_j] replaces "a_i == b_j ? match
  *                  : mismatch" in eq. P:85 and in the seed score; nothing
  *                  else changes. Requires seq_fmt = LOGAN_SEQ_U8 with every
- *                  base a code < alphabet (a larger code reads a 0 score);
+ *                  base a code < alphabet (a code c is read as c mod 32 and
+ *                  scores 0 against anything if that is >= alphabet);
  *                  scoring.match / .mismatch are then ignored (gap < 0 and
- *                  xdrop as usual). Every task runs on the CTA level with
- *                  the table in shared memory.
+ *                  xdrop as usual). The register windows (levels 1-6) look
+ *                  the score up in a shared-memory table; levels are chosen
+ *                  from X / |gap|; there is no band level (7): bands wider
+ *                  than the widest window go to the CTA level (8).
  */
 #define LOGAN_N_STAGES 10
 #define LOGAN_MAX_ALPHABET 32

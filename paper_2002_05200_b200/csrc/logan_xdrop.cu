@@ -180,8 +180,8 @@ __global__ void k_combine(const Params P, const TaskRes *tres, logan_result_t *o
             int32_t seed = 0;  // ungapped seed score (c-amb-10)
             for (int32_t u = 0; u < P.k; ++u) {
                 const uint32_t a = pool_base<FMT>(P, qo + qs + u), b = pool_base<FMT>(P, to + ts + u);
-                if (P.subst) seed += (a < (uint32_t)P.alphabet && b < (uint32_t)P.alphabet)
-                                         ? P.subst[a * P.alphabet + b] : 0;
+                if (P.subst) seed += ((a & 31u) < (uint32_t)P.alphabet && (b & 31u) < (uint32_t)P.alphabet)
+                                         ? P.subst[(a & 31u) * P.alphabet + (b & 31u)] : 0;
                 else seed += a == b ? P.match : P.mismatch;
             }
             r.score = seed + L.best + R.best;
@@ -219,7 +219,7 @@ template <int G, int R, int FMT, int HG, int HR>
 static cudaError_t launch_win(const Params &P, const LevelIO &io_in, const LevelIO &hio, int sms, cudaStream_t s) {
     constexpr int S1 = Window<G, R, FMT>::SB_STRIDE;
     constexpr int S2 = HR > 0 ? Window<(HG > 0 ? HG : 32), (HR > 0 ? HR : 1), FMT>::SB_STRIDE : 0;
-    const size_t smem = 128 * sizeof(int32_t) * (S1 > S2 ? S1 : S2);
+    const size_t smem = 128 * sizeof(int32_t) * (S1 > S2 ? S1 : S2) + (FMT == FMT_U8S ? SUBST_TAB_BYTES : 0);
     auto kern = k_window<G, R, FMT, HG, HR>;
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return e;
@@ -247,6 +247,14 @@ static cudaError_t launch_first(int w0, bool helpers, const Params &P, const Lev
 #ifdef LOGAN_L0_R
     w0 = LOGAN_L0_R;
 #endif
+    if constexpr (FMT == FMT_U8S) {  // substitution matrices: no in-kernel helpers
+        switch (w0) {
+            case 20: return launch_win<1, 20, FMT, 0, 0>(P, io, hio, sms, s);
+            case 24: return launch_win<1, 24, FMT, 0, 0>(P, io, hio, sms, s);
+            case 28: return launch_win<1, 28, FMT, 0, 0>(P, io, hio, sms, s);
+            default: return launch_win<1, 32, FMT, 0, 0>(P, io, hio, sms, s);
+        }
+    }
     switch (w0) {
         case 20: return helpers ? launch_win<1, 20, FMT, LOGAN_HSHAPE(64)>(P, io, hio, sms, s)
                                 : launch_win<1, 20, FMT, 0, 0>(P, io, hio, sms, s);
@@ -263,8 +271,8 @@ template <int FMT>
 static cudaError_t launch_width(int wi, bool latency, bool helpers, const Params &P, const LevelIO &io,
                                 const LevelIO &hio, int sms, cudaStream_t s, int w0, int w5) {
     if (wi == 0 && !(latency && w0 == 32)) return launch_first<FMT>(w0, helpers && !latency, P, io, hio, sms, s);
-    if (helpers && !latency) {
-        switch (wi) {
+    if (FMT != FMT_U8S && helpers && !latency) {
+        if constexpr (FMT != FMT_U8S) switch (wi) {
             case 1: return launch_win<2, 32, FMT, LOGAN_HSHAPE(128)>(P, io, hio, sms, s);
             case 2: return launch_win<4, 32, FMT, LOGAN_HSHAPE(256)>(P, io, hio, sms, s);
             case 3: return launch_win<8, 32, FMT, LOGAN_HSHAPE(512)>(P, io, hio, sms, s);
@@ -368,12 +376,16 @@ static int run_batch(const Params &P, const logan_options_t *opt, logan_result_t
     if (cudaGetLastError() != cudaSuccess) return LOGAN_ECUDA;
     if (!mark(0, 1)) return LOGAN_ECUDA;
 
-    int first = (opt && opt->first_level > 0) ? opt->first_level - 1 : auto_first_level(P.xdrop);
-    if (P.subst) first = WIDE_LEVEL;  // substitution matrices: the CTA level, table in shared memory
+    // level choice from the expected band width: about X slots under +1/-1/-1;
+    // with a substitution matrix about X / |gap| (moving one slot off the
+    // alignment's diagonal costs two gaps against at most X of slack)
+    const int32_t xband = FMT == FMT_U8S ? (P.xdrop + (-P.gap) - 1) / (-P.gap) : P.xdrop;
+    int first = (opt && opt->first_level > 0) ? opt->first_level - 1 : auto_first_level(xband);
+    if (FMT == FMT_U8S && first == BAND_LEVEL) first = WIDE_LEVEL;  // no band level for matrices
     if (first < 0 || first > NLEVEL - 1) return LOGAN_EINVAL;
     uint32_t *recs[2] = {(uint32_t *)(ws + L.recsA), (uint32_t *)(ws + L.recsB)};
-    const int w0 = (opt && opt->first_slots > 0) ? opt->first_slots : auto_first_slots(P.xdrop, L.wide_stride - 2);
-    const int w5 = auto_top_width(P.xdrop);
+    const int w0 = (opt && opt->first_slots > 0) ? opt->first_slots : auto_first_slots(xband, L.wide_stride - 2);
+    const int w5 = auto_top_width(xband);
     auto width_of = [&](int lv) { return lv == 0 ? w0 : (lv == NWIDTH - 1 ? w5 : kWidth[lv]); };
     const uint32_t *in_list = queue;
     const uint32_t *in_recs = nullptr;
@@ -418,6 +430,9 @@ static int run_batch(const Params &P, const logan_options_t *opt, logan_result_t
     const bool few_tasks = first > 0 && first < NWIDTH && groups_needed < (int64_t)sms * 16;
     const bool latency_first = (opt && (opt->flags & 1)) || few_tasks;
     for (int lv = first; lv < NLEVEL; ++lv) {
+        // substitution matrices have no band level: tasks that outgrow the widest
+        // window go straight on to the CTA level (which restarts them)
+        if (FMT == FMT_U8S && lv == BAND_LEVEL) continue;
         LevelIO io = level_io(lv, in_list, in_count, in_recs, rec_in, rec_in_stride, out_sel);
         cudaError_t e = cudaSuccess;
         if (!mark(1 + lv, 0)) return LOGAN_ECUDA;
@@ -445,6 +460,7 @@ static int run_batch(const Params &P, const logan_options_t *opt, logan_result_t
                 }
             }
         } else if (lv == BAND_LEVEL) {
+          if constexpr (FMT != FMT_U8S) {
             const int smem = (int)BandSmem<FMT>::BYTES;
             e = cudaFuncSetAttribute(k_band<FMT>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
             int per_sm = 0;
@@ -454,9 +470,12 @@ static int run_batch(const Params &P, const logan_options_t *opt, logan_result_t
                 k_band<FMT><<<sms * (per_sm > 0 ? per_sm : 1), BAND_NT, smem, s>>>(P, io);
                 e = cudaGetLastError();
             }
+          }
         } else {
-            if (P.subst) k_wide<FMT, SUBST_THREADS, true><<<WIDE_CTAS, SUBST_THREADS, 0, s>>>(P, io, wide, L.wide_stride);
-            else k_wide<FMT><<<WIDE_CTAS, WIDE_THREADS, 0, s>>>(P, io, wide, L.wide_stride);
+            if constexpr (FMT == FMT_U8S)
+                k_wide<FMT, SUBST_THREADS, true><<<WIDE_CTAS, SUBST_THREADS, 0, s>>>(P, io, wide, L.wide_stride);
+            else
+                k_wide<FMT><<<WIDE_CTAS, WIDE_THREADS, 0, s>>>(P, io, wide, L.wide_stride);
             e = cudaGetLastError();
         }
         if (e != cudaSuccess) return LOGAN_ECUDA;
@@ -573,6 +592,7 @@ int logan_xdrop_batch(const uint8_t *seq_pool, int32_t seq_fmt, int64_t pool_len
     // are rejected up front by the caller-side bound (documented in the header)
     cudaStream_t s = (cudaStream_t)stream;
     uint8_t *ws = (uint8_t *)workspace;
+    if (P.subst) return run_batch<FMT_U8S>(P, opt, out, cells, stats, ws, L, s);
     if (seq_fmt == LOGAN_SEQ_2BIT) return run_batch<LOGAN_SEQ_2BIT>(P, opt, out, cells, stats, ws, L, s);
     return run_batch<LOGAN_SEQ_U8>(P, opt, out, cells, stats, ws, L, s);
 }

@@ -131,6 +131,25 @@ template <> struct PoolFmt<LOGAN_SEQ_U8> {
     static constexpr int LOG_CPW = 2, BITS = 8;
     static constexpr uint32_t MASK = 0xffu;
 };
+// Internal format id: a u8 pool of symbol codes scored with a substitution
+// matrix (options.subst). Same pool layout as LOGAN_SEQ_U8.
+constexpr int FMT_U8S = 2;
+template <> struct PoolFmt<FMT_U8S> : PoolFmt<LOGAN_SEQ_U8> {};
+
+// Substitution table of the register windows (FMT_U8S), in shared memory:
+// entry (a << 6) + b for codes a, b < 32 (a code is read modulo 32; entries
+// beyond the alphabet are 0), row / column 32 = the past-the-end sentinels
+// (-127: cells outside the matrix stay below every earlier best).
+constexpr int SUBST_TAB_BYTES = (32 << 6) + 33 + 15;  // 2096, padded to 16
+__device__ __forceinline__ void load_subst_tab(const Params &P, int8_t *tab, int tid, int nt) {
+    for (int q = tid; q < SUBST_TAB_BYTES; q += nt) {
+        const int a = q >> 6, b = q & 63;
+        int8_t v = 0;
+        if (a == 32 || b == 32) v = -127;
+        else if (b < 32 && a < P.alphabet && b < P.alphabet) v = P.subst[a * P.alphabet + b];
+        tab[q] = v;
+    }
+}
 
 __device__ __forceinline__ uint32_t pool_word(const Params &P, int64_t wi) {
     wi = wi < 0 ? 0 : (wi >= P.pool_words ? P.pool_words - 1 : wi);

@@ -70,10 +70,24 @@ template <int FMT> struct RegFmt;
 template <> struct RegFmt<LOGAN_SEQ_2BIT> {
     static constexpr int CB = 4;                 // bits per register field
     static constexpr uint32_t SA = 4u, SB = 8u;  // sentinels past the ends of A / B
+    // field of a base (or sentinel) entering the A / B registers
+    __device__ __forceinline__ static uint32_t fa(uint32_t x) { return x; }
+    __device__ __forceinline__ static uint32_t fb(uint32_t x) { return x; }
 };
 template <> struct RegFmt<LOGAN_SEQ_U8> {
     static constexpr int CB = 16;
     static constexpr uint32_t SA = 0x100u, SB = 0x200u;
+    __device__ __forceinline__ static uint32_t fa(uint32_t x) { return x; }
+    __device__ __forceinline__ static uint32_t fb(uint32_t x) { return x; }
+};
+// Substitution-matrix scoring: an A field holds code << 6, a B field the code
+// (both mod 32), so A + B of two packed words is two table indices at once;
+// the sentinels are row / column 32 of the table (load_subst_tab).
+template <> struct RegFmt<FMT_U8S> {
+    static constexpr int CB = 16;
+    static constexpr uint32_t SA = 0x100u, SB = 0x100u;  // raw sentinels (> any byte); fa / fb map them to 32
+    __device__ __forceinline__ static uint32_t fa(uint32_t x) { return x < 256u ? (x & 31u) << 6 : 32u << 6; }
+    __device__ __forceinline__ static uint32_t fb(uint32_t x) { return x < 256u ? (x & 31u) : 32u; }
 };
 
 // Group-uniform state of one task (replicated in each lane of the group).
@@ -149,6 +163,15 @@ struct Window {
     // the mismatch test live there), so diag + s' is computed on the FMA pipe:
     // an IMAD by an opaque run-time 1 for the match case, overwritten by a
     // predicated IMAD for a mismatch -- no SEL, no IADD3.
+    // Substitution-matrix cell: s = the table entry, sr = the diagonal rebase.
+    __device__ __forceinline__ static int32_t cell_s(int32_t up, int32_t left, int32_t diag, int32_t s,
+                                                     int32_t gp, int32_t fg, int32_t sr) {
+        const int32_t t0 = __vimax3_s32(up, left, fg);
+        const int32_t u = __viaddmax_s32(t0, gp, diag + s + sr);
+        return (int32_t)min((uint32_t)u, DEADU);
+    }
+    const int8_t *tab;  // FMT_U8S: the substitution table in shared memory
+
     __device__ __forceinline__ static int32_t cell(int32_t up, int32_t left, int32_t diag, bool mis,
                                                    int32_t gp, int32_t fg, int32_t sma, int32_t smi,
                                                    int32_t one) {
@@ -235,10 +258,10 @@ struct Window {
         for (int q = 0; q < NW; ++q) { Aw[q] = 0; Bw[q] = 0; }
         st.sa.seek(P, s0 + ch);
 #pragma unroll 1
-        for (int r = 0; r < R; ++r) shift_down(Aw, st.sa.next(P, RF::SA));       // field r = a_{s0+r+ch}
+        for (int r = 0; r < R; ++r) shift_down(Aw, RF::fa(st.sa.next(P, RF::SA)));  // field r = a_{s0+r+ch}
         st.sb.seek(P, fh - (s0 + R - 1));
 #pragma unroll 1
-        for (int r = R - 1; r >= 0; --r) shift_up(Bw, st.sb.next(P, RF::SB));   // field r = b_{fh-(s0+r)}
+        for (int r = R - 1; r >= 0; --r) shift_up(Bw, RF::fb(st.sb.next(P, RF::SB)));  // field r = b_{fh-(s0+r)}
         if (gl == G - 1) st.sa.seek(P, st.S0 + W + ch);  // sa.idx = S0 + W + ceil(d/2)
         if (gl == 0) st.sb.seek(P, fh - st.S0 + 1);      // sb.idx = floor(d/2) - S0 + 1
     }
@@ -332,12 +355,12 @@ struct Window {
         if (PAR == 1) {  // i advances: A fields move down one slot
             uint32_t in = 0;
             if (G > 1) in = __shfl_down_sync(gmask, Aw[0], 1, G) & FM;
-            if (gl == G - 1) in = st.sa.next(P, RF::SA);
+            if (gl == G - 1) in = RF::fa(st.sa.next(P, RF::SA));
             shift_down(Aw, in);
         } else {         // j advances: B fields move up one slot
             uint32_t in = 0;
             if (G > 1) in = __shfl_up_sync(gmask, top_field(Bw), 1, G);
-            if (gl == 0) in = st.sb.next(P, RF::SB);
+            if (gl == 0) in = RF::fb(st.sb.next(P, RF::SB));
             shift_up(Bw, in);
         }
 
@@ -350,9 +373,11 @@ struct Window {
         const int32_t fg = DEAD - gp;  // max(up, left, fg) + gp >= DEAD: the floor
 
         const uint32_t two = 2u * (uint32_t)P.one;  // = 2, opaque to the compiler
+        constexpr bool SUB = FMT == FMT_U8S;
+        const int32_t sr = -(Tc - st.Tq[PAR]);  // diagonal rebase (SUB: s' = table entry + sr)
         uint32_t X[NW];
 #pragma unroll
-        for (int q = 0; q < NW; ++q) X[q] = Aw[q] ^ Bw[q];
+        for (int q = 0; q < NW; ++q) X[q] = SUB ? Aw[q] + Bw[q] : Aw[q] ^ Bw[q];  // SUB: two table indices
 
         // (4) cells
         int32_t kq[4];
@@ -367,8 +392,12 @@ struct Window {
 #pragma unroll
             for (int r = 0; r < R; ++r) {
                 const int32_t up = (r < R - 1) ? E[r + 1] : nb;
-                const bool mis = ((X[r / FPW] >> (CB * (r % FPW))) & FM) != 0;
-                O[r] = cell(up, E[r], O[r], mis, gp, fg, sma, smi, P.one);
+                if (SUB) {
+                    O[r] = cell_s(up, E[r], O[r], tab[(X[r / FPW] >> (CB * (r % FPW))) & FM], gp, fg, sr);
+                } else {
+                    const bool mis = ((X[r / FPW] >> (CB * (r % FPW))) & FM) != 0;
+                    O[r] = cell(up, E[r], O[r], mis, gp, fg, sma, smi, P.one);
+                }
             }
         } else {
             int32_t nb = DEAD;  // O[-1] of this lane = O[R-1] of the previous lane
@@ -379,8 +408,12 @@ struct Window {
 #pragma unroll
             for (int r = 0; r < R; ++r) {
                 const int32_t left = (r > 0) ? O[r - 1] : nb;
-                const bool mis = ((X[r / FPW] >> (CB * (r % FPW))) & FM) != 0;
-                E[r] = cell(O[r], left, E[r], mis, gp, fg, sma, smi, P.one);
+                if (SUB) {
+                    E[r] = cell_s(O[r], left, E[r], tab[(X[r / FPW] >> (CB * (r % FPW))) & FM], gp, fg, sr);
+                } else {
+                    const bool mis = ((X[r / FPW] >> (CB * (r % FPW))) & FM) != 0;
+                    E[r] = cell(O[r], left, E[r], mis, gp, fg, sma, smi, P.one);
+                }
             }
         }
         // keys u * KEYMUL + 1023 - r and dead masks over the new antidiagonal
@@ -490,8 +523,8 @@ struct Window {
         if (gl == G - 1) {
             eIn = DEAD;
             oIn = DEAD;
-            aIn = st.sa.next(P, RF::SA);  // a_{S1 + W - 1 + ceil(d/2)}
-            bIn = seq_at<FMT>(P, st.sb.s, floor_half(d) - S1 - (W - 1), RF::SB);
+            aIn = RF::fa(st.sa.next(P, RF::SA));  // a_{S1 + W - 1 + ceil(d/2)}
+            bIn = RF::fb(seq_at<FMT>(P, st.sb.s, floor_half(d) - S1 - (W - 1), RF::SB));
         }
         if (gl == 0) st.sb.seek(P, st.sb.idx - 1);  // b stream steps back one base
         // rotate E/O through this thread's shared-memory slice: the reloads land in
@@ -522,8 +555,8 @@ struct Window {
         if (gl == 0) {
             eIn = DEAD;
             oIn = DEAD;
-            aIn = seq_at<FMT>(P, st.sa.s, S1 + ceil_half(d), RF::SA);
-            bIn = st.sb.next(P, RF::SB);  // b_{floor(d/2) - S1}
+            aIn = RF::fa(seq_at<FMT>(P, st.sa.s, S1 + ceil_half(d), RF::SA));
+            bIn = RF::fb(st.sb.next(P, RF::SB));  // b_{floor(d/2) - S1}
         }
         if (gl == G - 1) st.sa.seek(P, st.sa.idx - 1);  // a stream steps back one base
         spill(E, O);
@@ -643,10 +676,19 @@ __global__ void __launch_bounds__(128, (G == 1 ? LOGAN_L0_MINB : 1))
     if (remaining < io.min_count || remaining >= io.max_count) return;
     extern __shared__ int32_t win_smem[];
     const int lane = threadIdx.x & 31;
+    int8_t *tab = nullptr;
+    if (FMT == FMT_U8S) {  // the substitution table behind the per-thread shift slices
+        constexpr int S1 = Window<G, R, FMT>::SB_STRIDE;
+        constexpr int S2 = HR > 0 ? Window<(HG > 0 ? HG : 32), (HR > 0 ? HR : 1), FMT>::SB_STRIDE : 0;
+        tab = (int8_t *)(win_smem + blockDim.x * (S1 > S2 ? S1 : S2));
+        load_subst_tab(P, tab, threadIdx.x, blockDim.x);
+        __syncthreads();
+    }
     const bool helper = HR > 0 && (int)blockIdx.x < io.helpers && (threadIdx.x >> 5) == (blockDim.x >> 5) - 1;
     if (HR > 0 && helper) {
         constexpr int HG_ = HG > 0 ? HG : 32, HR_ = HR > 0 ? HR : 1;
         Window<HG_, HR_, FMT> w;
+        w.tab = tab;
         w.sbase = win_smem + threadIdx.x * Window<HG_, HR_, FMT>::SB_STRIDE;
         w.gl = lane % HG_;
         w.gmask = (HG_ == 32) ? 0xffffffffu : (((1u << HG_) - 1u) << (lane - w.gl));
@@ -683,6 +725,7 @@ __global__ void __launch_bounds__(128, (G == 1 ? LOGAN_L0_MINB : 1))
         return;
     }
     Window<G, R, FMT> w;
+    w.tab = tab;
     w.sbase = win_smem + threadIdx.x * Window<G, R, FMT>::SB_STRIDE;
     w.gl = lane % G;
     w.gmask = (G == 32) ? 0xffffffffu : (((1u << G) - 1u) << (lane - w.gl));

@@ -516,3 +516,18 @@ def test_subst_tiny_exhaustive_and_asymmetric():
         ref = oracle.pairs_subst(b.pool_u8, b.q_off, b.q_len, b.t_off, b.t_len, b.q_seed, b.t_seed, 0, M, -2, X,
                                  pool_len=b.pool_len)
         assert_same(*_subst_run(b, M, -2, X), *ref, what=f"tiny subst X={X}")
+
+
+@pytest.mark.parametrize("lvl", [1, 2, 3, 4, 5, 6, 7, 8])
+def test_subst_every_level(lvl):
+    """Substitution-matrix scoring forced onto every level (register windows 1-6
+    with the shared-memory table, 7 = the band level which matrices skip, 8 = the
+    CTA level), in both shapes and with forced hand-overs: bit-exact."""
+    M = datagen.protein_matrix()
+    b = datagen.protein_pairs(120, len_lo=40, len_hi=400, xdrop=40)
+    for X in (0, 12, 40, 150):
+        ref = oracle.pairs_subst(b.pool_u8, b.q_off, b.q_len, b.t_off, b.t_len, b.q_seed, b.t_seed,
+                                 b.workload.k, M, -4, X, pool_len=b.pool_len)
+        for lat, ho in ((False, 0), (True, 0), (False, 6)):
+            got = _subst_run(b, M, -4, X, first_level=lvl, latency_first=lat, handover=ho)
+            assert_same(*got, *ref, what=f"subst level {lvl} lat={lat} handover {ho} X={X}")
