@@ -24,6 +24,10 @@
  *        best_d = max(best_{d-1}, max live S on d)
  *  (3) stop after the first d at which antidiagonals d and d-1 have no live
  *      cell (band empty, c-amb-7)
+ *  (3b) optional Z-drop (minimap2's heuristic, which the paper names as an
+ *      X-drop variant; reading c-amb-19): after antidiagonal d (best
+ *      already updated), stop if best - M_d > Z + |gap| * |(i_d - i*) - (j_d - j*)|
+ *      where M_d is the largest live score on d at (i_d, j_d), smallest i
  *  (4) result: best; (i*, j*) = the live cell with S = best on the smallest d,
  *      smallest i on that d; (0,0) if best = 0                 (c-amb-8, c-amb-9)
  *  (5) cells = sum over d >= 2 of |[lo_d, hi_d]| with
@@ -127,12 +131,12 @@ static int64_t sub_score(uint8_t a, uint8_t b, int64_t match, int64_t mismatch,
 
 static int extend_impl(const uint8_t *A, int64_t m, const uint8_t *B, int64_t n,
                        int64_t match, int64_t mismatch, const int8_t *subst, int64_t alph,
-                       int64_t gap, int64_t X, int full_scan, oracle_ext_t *out);
+                       int64_t gap, int64_t X, int64_t zdrop, int full_scan, oracle_ext_t *out);
 
 int oracle_extend(const uint8_t *A, int64_t m, const uint8_t *B, int64_t n,
                   int64_t match, int64_t mismatch, int64_t gap, int64_t X,
                   int full_scan, oracle_ext_t *out) {
-    return extend_impl(A, m, B, n, match, mismatch, NULL, 0, gap, X, full_scan, out);
+    return extend_impl(A, m, B, n, match, mismatch, NULL, 0, gap, X, -1, full_scan, out);
 }
 
 /* The same extension with s(a, b) = subst[a * alph + b]; every code of A and B
@@ -143,12 +147,25 @@ int oracle_extend_subst(const uint8_t *A, int64_t m, const uint8_t *B, int64_t n
     if (!subst || alph < 1 || alph > 256) return ORACLE_EINVAL;
     for (int64_t i = 0; i < m; ++i) if (A[i] >= alph) return ORACLE_EINVAL;
     for (int64_t j = 0; j < n; ++j) if (B[j] >= alph) return ORACLE_EINVAL;
-    return extend_impl(A, m, B, n, 0, 0, subst, alph, gap, X, full_scan, out);
+    return extend_impl(A, m, B, n, 0, 0, subst, alph, gap, X, -1, full_scan, out);
+}
+
+/* The general extension: subst = NULL for match / mismatch, zdrop < 0 for no
+ * Z-drop (otherwise step (3b) of the header applies). */
+int oracle_extend_z(const uint8_t *A, int64_t m, const uint8_t *B, int64_t n,
+                    int64_t match, int64_t mismatch, const int8_t *subst, int64_t alph,
+                    int64_t gap, int64_t X, int64_t zdrop, int full_scan, oracle_ext_t *out) {
+    if (subst) {
+        if (alph < 1 || alph > 256) return ORACLE_EINVAL;
+        for (int64_t i = 0; i < m; ++i) if (A[i] >= alph) return ORACLE_EINVAL;
+        for (int64_t j = 0; j < n; ++j) if (B[j] >= alph) return ORACLE_EINVAL;
+    }
+    return extend_impl(A, m, B, n, match, mismatch, subst, alph, gap, X, zdrop, full_scan, out);
 }
 
 static int extend_impl(const uint8_t *A, int64_t m, const uint8_t *B, int64_t n,
                        int64_t match, int64_t mismatch, const int8_t *subst, int64_t alph,
-                       int64_t gap, int64_t X, int full_scan, oracle_ext_t *out) {
+                       int64_t gap, int64_t X, int64_t zdrop, int full_scan, oracle_ext_t *out) {
     if (!out || m < 0 || n < 0 || X < 0 || (m > 0 && !A) || (n > 0 && !B)) return ORACLE_EINVAL;
     out->best = 0;
     out->i = 0;
@@ -285,6 +302,14 @@ static int extend_impl(const uint8_t *A, int64_t m, const uint8_t *B, int64_t n,
             arg_i = dmax_i;
             arg_j = d - dmax_i;
         }
+        /* (3b) Z-drop (the variant the paper names; c-amb-19): stop after
+         * antidiagonal d when best - M_d > Z + |gap| * |(i_d - i*) - (j_d - j*)|,
+         * M_d / (i_d, j_d) = d's max live score and its cell (smallest i). */
+        if (zdrop >= 0 && have_max) {
+            int64_t off = (dmax_i - arg_i) - ((d - dmax_i) - arg_j);
+            if (off < 0) off = -off;
+            if (best - dmax > zdrop + (-gap) * off) break;
+        }
         /* (3) termination: antidiagonals d and d-1 both empty */
         if (!cur->has_live && !p1->has_live) break;
         if (d > m + n + 2) break; /* cannot happen; defensive */
@@ -317,7 +342,7 @@ static int pair_impl(const uint8_t *pool, int fmt, int64_t pool_len,
                      int64_t q_off, int64_t q_len, int64_t t_off, int64_t t_len,
                      int64_t qs, int64_t ts, int64_t k,
                      int64_t match, int64_t mismatch, const int8_t *subst, int64_t alph,
-                     int64_t gap, int64_t X, oracle_pair_t *res, uint64_t *cells_out);
+                     int64_t gap, int64_t X, int64_t zdrop, oracle_pair_t *res, uint64_t *cells_out);
 
 int oracle_pair(const uint8_t *pool, int fmt, int64_t pool_len,
                 int64_t q_off, int64_t q_len, int64_t t_off, int64_t t_len,
@@ -325,14 +350,14 @@ int oracle_pair(const uint8_t *pool, int fmt, int64_t pool_len,
                 int64_t match, int64_t mismatch, int64_t gap, int64_t X,
                 oracle_pair_t *res, uint64_t *cells_out) {
     return pair_impl(pool, fmt, pool_len, q_off, q_len, t_off, t_len, qs, ts, k, match, mismatch,
-                     NULL, 0, gap, X, res, cells_out);
+                     NULL, 0, gap, X, -1, res, cells_out);
 }
 
 static int pair_impl(const uint8_t *pool, int fmt, int64_t pool_len,
                      int64_t q_off, int64_t q_len, int64_t t_off, int64_t t_len,
                      int64_t qs, int64_t ts, int64_t k,
                      int64_t match, int64_t mismatch, const int8_t *subst, int64_t alph,
-                     int64_t gap, int64_t X, oracle_pair_t *res, uint64_t *cells_out) {
+                     int64_t gap, int64_t X, int64_t zdrop, oracle_pair_t *res, uint64_t *cells_out) {
     res->score = INT32_MIN;
     res->q_begin = res->q_end = res->t_begin = res->t_end = -1;
     if (cells_out) *cells_out = 0;
@@ -364,12 +389,8 @@ static int pair_impl(const uint8_t *pool, int fmt, int64_t pool_len,
 
     oracle_ext_t L, R;
     int st = bad_code ? ORACLE_EINVAL : ORACLE_OK;
-    if (st == ORACLE_OK)
-        st = subst ? oracle_extend_subst(AL, mL, BL, nL, subst, alph, gap, X, 0, &L)
-                   : oracle_extend(AL, mL, BL, nL, match, mismatch, gap, X, 0, &L);
-    if (st == ORACLE_OK)
-        st = subst ? oracle_extend_subst(AR, mR, BR, nR, subst, alph, gap, X, 0, &R)
-                   : oracle_extend(AR, mR, BR, nR, match, mismatch, gap, X, 0, &R);
+    if (st == ORACLE_OK) st = oracle_extend_z(AL, mL, BL, nL, match, mismatch, subst, alph, gap, X, zdrop, 0, &L);
+    if (st == ORACLE_OK) st = oracle_extend_z(AR, mR, BR, nR, match, mismatch, subst, alph, gap, X, zdrop, 0, &R);
     free(AL); free(BL); free(AR); free(BR);
     if (st != ORACLE_OK) return st;
 
@@ -399,6 +420,7 @@ typedef struct {
     int64_t k, match, mismatch, gap, X;
     const int8_t *subst;
     int64_t alph;
+    int64_t zdrop;
     oracle_pair_t *out;
     uint64_t *cells;
     int64_t next; /* shared cursor */
@@ -420,7 +442,7 @@ static void *batch_worker(void *arg) {
             int st = pair_impl(job->pool, job->fmt, job->pool_len, job->q_off[p], job->q_len[p],
                                job->t_off[p], job->t_len[p], job->q_seed[p], job->t_seed[p],
                                job->k, job->match, job->mismatch, job->subst, job->alph, job->gap, job->X,
-                               &job->out[p], &c);
+                               job->zdrop, &job->out[p], &c);
             if (job->cells) job->cells[p] = c;
             if (st != ORACLE_OK) {
                 pthread_mutex_lock(&job->mu);
@@ -437,7 +459,7 @@ static int pairs_impl(const uint8_t *pool, int fmt, int64_t pool_len,
                       const int64_t *t_off, const int32_t *t_len,
                       const int32_t *q_seed, const int32_t *t_seed, int64_t n_pairs,
                       int64_t k, int64_t match, int64_t mismatch, const int8_t *subst, int64_t alph,
-                      int64_t gap, int64_t X, oracle_pair_t *out, uint64_t *cells, int n_threads);
+                      int64_t gap, int64_t X, int64_t zdrop, oracle_pair_t *out, uint64_t *cells, int n_threads);
 
 int oracle_pairs(const uint8_t *pool, int fmt, int64_t pool_len,
                  const int64_t *q_off, const int32_t *q_len,
@@ -446,7 +468,7 @@ int oracle_pairs(const uint8_t *pool, int fmt, int64_t pool_len,
                  int64_t k, int64_t match, int64_t mismatch, int64_t gap, int64_t X,
                  oracle_pair_t *out, uint64_t *cells, int n_threads) {
     return pairs_impl(pool, fmt, pool_len, q_off, q_len, t_off, t_len, q_seed, t_seed, n_pairs, k,
-                      match, mismatch, NULL, 0, gap, X, out, cells, n_threads);
+                      match, mismatch, NULL, 0, gap, X, -1, out, cells, n_threads);
 }
 
 /* Pairs scored with a substitution matrix subst[alph * alph] (u8 pool of
@@ -459,7 +481,20 @@ int oracle_pairs_subst(const uint8_t *pool, int64_t pool_len,
                        oracle_pair_t *out, uint64_t *cells, int n_threads) {
     if (!subst || alph < 1 || alph > 256) return ORACLE_EINVAL;
     return pairs_impl(pool, 0, pool_len, q_off, q_len, t_off, t_len, q_seed, t_seed, n_pairs, k,
-                      0, 0, subst, alph, gap, X, out, cells, n_threads);
+                      0, 0, subst, alph, gap, X, -1, out, cells, n_threads);
+}
+
+/* The general batch: subst = NULL for match / mismatch (then fmt selects the
+ * pool format), zdrop < 0 for no Z-drop. */
+int oracle_pairs_z(const uint8_t *pool, int fmt, int64_t pool_len,
+                   const int64_t *q_off, const int32_t *q_len,
+                   const int64_t *t_off, const int32_t *t_len,
+                   const int32_t *q_seed, const int32_t *t_seed, int64_t n_pairs,
+                   int64_t k, int64_t match, int64_t mismatch, const int8_t *subst, int64_t alph,
+                   int64_t gap, int64_t X, int64_t zdrop, oracle_pair_t *out, uint64_t *cells, int n_threads) {
+    if (subst && (alph < 1 || alph > 256 || fmt != 0)) return ORACLE_EINVAL;
+    return pairs_impl(pool, fmt, pool_len, q_off, q_len, t_off, t_len, q_seed, t_seed, n_pairs, k,
+                      match, mismatch, subst, alph, gap, X, zdrop, out, cells, n_threads);
 }
 
 static int pairs_impl(const uint8_t *pool, int fmt, int64_t pool_len,
@@ -467,12 +502,12 @@ static int pairs_impl(const uint8_t *pool, int fmt, int64_t pool_len,
                       const int64_t *t_off, const int32_t *t_len,
                       const int32_t *q_seed, const int32_t *t_seed, int64_t n_pairs,
                       int64_t k, int64_t match, int64_t mismatch, const int8_t *subst, int64_t alph,
-                      int64_t gap, int64_t X, oracle_pair_t *out, uint64_t *cells, int n_threads) {
+                      int64_t gap, int64_t X, int64_t zdrop, oracle_pair_t *out, uint64_t *cells, int n_threads) {
     if (n_pairs < 0 || (n_pairs > 0 && (!pool || !q_off || !q_len || !t_off || !t_len || !q_seed ||
                                         !t_seed || !out)))
         return ORACLE_EINVAL;
     batch_job_t job = {pool, fmt, pool_len, q_off, t_off, q_len, t_len, q_seed, t_seed, n_pairs,
-                       k, match, mismatch, gap, X, subst, alph, out, cells, 0, PTHREAD_MUTEX_INITIALIZER, 0};
+                       k, match, mismatch, gap, X, subst, alph, zdrop, out, cells, 0, PTHREAD_MUTEX_INITIALIZER, 0};
     if (n_threads < 1) n_threads = 1;
     if (n_threads == 1) {
         batch_worker(&job);

@@ -290,3 +290,57 @@ def test_subst_protein_invariants():
             assert 0 <= r.best <= S[r.i][r.j]
     with pytest.raises(RuntimeError):
         oracle.extend_subst(bytes([0, 25]), bytes([1]), 5, M, -4)
+
+
+# ---------------------------------------------------------------------------
+# Z-drop (the X-drop variant the paper names; oracle header step 3b, c-amb-19)
+
+def test_zdrop_closed_form():
+    """Identical prefix of length p, then disjoint tails (A-only vs C/G-only), X
+    unbounded: the antidiagonal maxima fall 1 per two antidiagonals on the
+    diagonal, and the best off-diagonal cell trails by one |gap| on odd ones, so
+    Z-drop stops after antidiagonal 2p + 2Z + 2 (for +1/-1/-1 and +1/-1/-2).
+    Pins the '>' (not '>='), the antidiagonal max, and the |gap| * offset term:
+    without the offset term (or with a multiplier of 1 at gap -2) the stop
+    comes one antidiagonal earlier."""
+    for gap in (-1, -2):
+        for p in (0, 3, 10, 25):
+            for Z in (0, 1, 2, 5, 9):
+                A, B = "A" * p + "C" * 40, "A" * p + "G" * 40
+                r = oracle.extend_z(A, B, 10 ** 6, Z, gap=gap)
+                assert (r.best, r.i, r.j, r.last_d) == (p, p, p, 2 * p + 2 * Z + 2), (gap, p, Z, r)
+
+
+def test_zdrop_off_or_unbounded_is_xdrop():
+    """Z < 0 (off) and Z above any reachable drop reproduce the pinned X-drop
+    oracle exactly, with and without a substitution matrix."""
+    rng = np.random.default_rng(11)
+    M = datagen.protein_matrix()
+    for _ in range(80):
+        A = rng.integers(0, 4, rng.integers(0, 60)).astype(np.uint8)
+        B = A.copy() if rng.random() < 0.6 else rng.integers(0, 4, rng.integers(0, 60)).astype(np.uint8)
+        if len(B):
+            B[rng.integers(0, len(B), 4)] = rng.integers(0, 4, 4)
+        X = int(rng.integers(0, 30))
+        ref = oracle.extend(A.tobytes(), B.tobytes(), X)
+        assert oracle.extend_z(A.tobytes(), B.tobytes(), X, -1) == ref
+        assert oracle.extend_z(A.tobytes(), B.tobytes(), X, 10 ** 6) == ref
+        refm = oracle.extend_subst(A.tobytes(), B.tobytes(), X, M, -4)
+        assert oracle.extend_z(A.tobytes(), B.tobytes(), X, 10 ** 6, gap=-4, subst=M) == refm
+
+
+def test_zdrop_truncates_the_xdrop_sweep():
+    """With Z-drop the sweep is a prefix of the X-drop sweep: it stops no later,
+    best and cells never exceed the X-drop values, and when it stops before the
+    band empties the last antidiagonal satisfies the Z condition."""
+    rng = np.random.default_rng(12)
+    for _ in range(200):
+        A = rng.integers(0, 4, rng.integers(1, 80)).astype(np.uint8)
+        B = A.copy()
+        B[rng.integers(0, len(B), max(1, len(B) // 5))] = rng.integers(0, 4, max(1, len(B) // 5))
+        X, Z = int(rng.integers(5, 40)), int(rng.integers(0, 8))
+        full = oracle.extend(A.tobytes(), B.tobytes(), X)
+        z = oracle.extend_z(A.tobytes(), B.tobytes(), X, Z)
+        assert z.last_d <= full.last_d and z.best <= full.best and z.cells <= full.cells
+        if z.last_d == full.last_d:
+            assert z == full
