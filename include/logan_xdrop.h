@@ -93,6 +93,7 @@ enum {
  *                  combine. Stages not launched leave their events untouched.
  *  flags         : bit 0 = run the first level in its latency shape (one
  *                  warp per task) instead of its throughput shape.
+ *                  bit 2 = Z-drop on, threshold `zdrop` (0 <= zdrop <= 2^19).
  *                  bit 1 = test knob: the band level fills its shared-memory
  *                  code buffers with garbage before each task, so the tests
  *                  see the worst case of stale shared memory. Results never
@@ -104,6 +105,14 @@ enum {
  *                  window level is handed over to the next level every
  *                  `handover` antidiagonals, exercising the exact hand-over.
  *                  Results never depend on it.
+ *  zdrop         : with flags bit 2, the Z-drop stop (the X-drop variant the
+ *                  paper names; reading c-amb-19): after
+ *                  antidiagonal d, an extension ends if best - M_d > zdrop +
+ *                  |gap| * |(i_d - i*) - (j_d - j*)|, M_d the largest live
+ *                  score on d at (i_d, j_d) (smallest i), (i*, j*) the argmax
+ *                  so far. X-drop pruning still applies. Tasks with Z-drop
+ *                  skip the band level (bands wider than the widest window
+ *                  restart on the CTA level).
  *  subst, alphabet : substitution-matrix scoring (the
  *                  paper names protein alignment as future work).
  *                  NULL = match / mismatch. Otherwise a DEVICE pointer to an
@@ -131,7 +140,7 @@ typedef struct {
     int32_t first_slots;
     const int8_t *subst;
     int32_t alphabet;
-    int32_t pad_;
+    int32_t zdrop;
     int64_t reserved[3];
 } logan_options_t;
 

@@ -34,7 +34,7 @@ class Options(ctypes.Structure):
     _fields_ = [("first_level", ctypes.c_int32), ("flags", ctypes.c_int32),
                 ("timing_events", ctypes.c_void_p), ("handover", ctypes.c_int32),
                 ("first_slots", ctypes.c_int32), ("subst", ctypes.c_void_p),
-                ("alphabet", ctypes.c_int32), ("pad_", ctypes.c_int32), ("reserved", ctypes.c_int64 * 3)]
+                ("alphabet", ctypes.c_int32), ("zdrop", ctypes.c_int32), ("reserved", ctypes.c_int64 * 3)]
 
 
 class Result(ctypes.Structure):

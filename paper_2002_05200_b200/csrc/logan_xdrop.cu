@@ -219,7 +219,7 @@ template <int G, int R, int FMT, int HG, int HR>
 static cudaError_t launch_win(const Params &P, const LevelIO &io_in, const LevelIO &hio, int sms, cudaStream_t s) {
     constexpr int S1 = Window<G, R, FMT>::SB_STRIDE;
     constexpr int S2 = HR > 0 ? Window<(HG > 0 ? HG : 32), (HR > 0 ? HR : 1), FMT>::SB_STRIDE : 0;
-    const size_t smem = 128 * sizeof(int32_t) * (S1 > S2 ? S1 : S2) + (FMT == FMT_U8S ? SUBST_TAB_BYTES : 0);
+    const size_t smem = 128 * sizeof(int32_t) * (S1 > S2 ? S1 : S2) + (fmt_base(FMT) == FMT_U8S ? SUBST_TAB_BYTES : 0);
     auto kern = k_window<G, R, FMT, HG, HR>;
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return e;
@@ -247,7 +247,7 @@ static cudaError_t launch_first(int w0, bool helpers, const Params &P, const Lev
 #ifdef LOGAN_L0_R
     w0 = LOGAN_L0_R;
 #endif
-    if constexpr (FMT == FMT_U8S) {  // substitution matrices: no in-kernel helpers
+    if constexpr (fmt_base(FMT) == FMT_U8S || fmt_z(FMT)) {  // matrices, Z-drop: no in-kernel helpers
         switch (w0) {
             case 20: return launch_win<1, 20, FMT, 0, 0>(P, io, hio, sms, s);
             case 24: return launch_win<1, 24, FMT, 0, 0>(P, io, hio, sms, s);
@@ -271,8 +271,9 @@ template <int FMT>
 static cudaError_t launch_width(int wi, bool latency, bool helpers, const Params &P, const LevelIO &io,
                                 const LevelIO &hio, int sms, cudaStream_t s, int w0, int w5) {
     if (wi == 0 && !(latency && w0 == 32)) return launch_first<FMT>(w0, helpers && !latency, P, io, hio, sms, s);
-    if (FMT != FMT_U8S && helpers && !latency) {
-        if constexpr (FMT != FMT_U8S) switch (wi) {
+    constexpr bool HELP = fmt_base(FMT) != FMT_U8S && !fmt_z(FMT);
+    if (HELP && helpers && !latency) {
+        if constexpr (HELP) switch (wi) {
             case 1: return launch_win<2, 32, FMT, LOGAN_HSHAPE(128)>(P, io, hio, sms, s);
             case 2: return launch_win<4, 32, FMT, LOGAN_HSHAPE(256)>(P, io, hio, sms, s);
             case 3: return launch_win<8, 32, FMT, LOGAN_HSHAPE(512)>(P, io, hio, sms, s);
@@ -379,9 +380,11 @@ static int run_batch(const Params &P, const logan_options_t *opt, logan_result_t
     // level choice from the expected band width: about X slots under +1/-1/-1;
     // with a substitution matrix about X / |gap| (moving one slot off the
     // alignment's diagonal costs two gaps against at most X of slack)
-    const int32_t xband = FMT == FMT_U8S ? (P.xdrop + (-P.gap) - 1) / (-P.gap) : P.xdrop;
+    const int32_t xband = fmt_base(FMT) == FMT_U8S ? (P.xdrop + (-P.gap) - 1) / (-P.gap) : P.xdrop;
     int first = (opt && opt->first_level > 0) ? opt->first_level - 1 : auto_first_level(xband);
-    if (FMT == FMT_U8S && first == BAND_LEVEL) first = WIDE_LEVEL;  // no band level for matrices
+    // no band level for matrices or Z-drop: those tasks go on to the CTA level
+    constexpr bool no_band = fmt_base(FMT) == FMT_U8S || fmt_z(FMT);
+    if (no_band && first == BAND_LEVEL) first = WIDE_LEVEL;
     if (first < 0 || first > NLEVEL - 1) return LOGAN_EINVAL;
     uint32_t *recs[2] = {(uint32_t *)(ws + L.recsA), (uint32_t *)(ws + L.recsB)};
     const int w0 = (opt && opt->first_slots > 0) ? opt->first_slots : auto_first_slots(xband, L.wide_stride - 2);
@@ -432,7 +435,7 @@ static int run_batch(const Params &P, const logan_options_t *opt, logan_result_t
     for (int lv = first; lv < NLEVEL; ++lv) {
         // substitution matrices have no band level: tasks that outgrow the widest
         // window go straight on to the CTA level (which restarts them)
-        if (FMT == FMT_U8S && lv == BAND_LEVEL) continue;
+        if (no_band && lv == BAND_LEVEL) continue;
         LevelIO io = level_io(lv, in_list, in_count, in_recs, rec_in, rec_in_stride, out_sel);
         cudaError_t e = cudaSuccess;
         if (!mark(1 + lv, 0)) return LOGAN_ECUDA;
@@ -460,7 +463,7 @@ static int run_batch(const Params &P, const logan_options_t *opt, logan_result_t
                 }
             }
         } else if (lv == BAND_LEVEL) {
-          if constexpr (FMT != FMT_U8S) {
+          if constexpr (!no_band) {
             const int smem = (int)BandSmem<FMT>::BYTES;
             e = cudaFuncSetAttribute(k_band<FMT>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
             int per_sm = 0;
@@ -472,7 +475,7 @@ static int run_batch(const Params &P, const logan_options_t *opt, logan_result_t
             }
           }
         } else {
-            if constexpr (FMT == FMT_U8S)
+            if constexpr (fmt_base(FMT) == FMT_U8S)
                 k_wide<FMT, SUBST_THREADS, true><<<WIDE_CTAS, SUBST_THREADS, 0, s>>>(P, io, wide, L.wide_stride);
             else
                 k_wide<FMT><<<WIDE_CTAS, WIDE_THREADS, 0, s>>>(P, io, wide, L.wide_stride);
@@ -540,6 +543,7 @@ static int check_args(const uint8_t *seq_pool, int32_t seq_fmt, int64_t pool_len
     if (!subst && (sc.match <= 0 || sc.match > 127 || sc.mismatch >= 0 || sc.mismatch < -127))
         return LOGAN_EINVAL;
     if (sc.gap >= 0 || sc.gap < -127 || sc.xdrop < 0 || sc.xdrop > (1 << 19)) return LOGAN_EINVAL;
+    if (opt && (opt->flags & 4) && (opt->zdrop < 0 || opt->zdrop > (1 << 19))) return LOGAN_EINVAL;
     if (opt && (opt->first_level < 0 || opt->first_level > NLEVEL)) return LOGAN_EINVAL;
     if (opt && opt->first_slots != 0 && opt->first_slots != 20 && opt->first_slots != 24 &&
         opt->first_slots != 28 && opt->first_slots != 32)
@@ -587,11 +591,17 @@ int logan_xdrop_batch(const uint8_t *seq_pool, int32_t seq_fmt, int64_t pool_len
     P.poison = (opt && (opt->flags & 2)) ? 1 : 0;
     P.subst = opt ? opt->subst : nullptr;
     P.alphabet = (opt && opt->subst) ? opt->alphabet : 0;
+    P.zdrop = (opt && (opt->flags & 4)) ? opt->zdrop : -1;
 
     // extension lengths beyond the wide scratch would overflow it: such pairs
     // are rejected up front by the caller-side bound (documented in the header)
     cudaStream_t s = (cudaStream_t)stream;
     uint8_t *ws = (uint8_t *)workspace;
+    if (P.zdrop >= 0) {  // the Z-drop builds of the kernels (FMT | FMT_Z)
+        if (P.subst) return run_batch<FMT_U8S | FMT_Z>(P, opt, out, cells, stats, ws, L, s);
+        if (seq_fmt == LOGAN_SEQ_2BIT) return run_batch<LOGAN_SEQ_2BIT | FMT_Z>(P, opt, out, cells, stats, ws, L, s);
+        return run_batch<LOGAN_SEQ_U8 | FMT_Z>(P, opt, out, cells, stats, ws, L, s);
+    }
     if (P.subst) return run_batch<FMT_U8S>(P, opt, out, cells, stats, ws, L, s);
     if (seq_fmt == LOGAN_SEQ_2BIT) return run_batch<LOGAN_SEQ_2BIT>(P, opt, out, cells, stats, ws, L, s);
     return run_batch<LOGAN_SEQ_U8>(P, opt, out, cells, stats, ws, L, s);

@@ -31,6 +31,7 @@ struct Params {
     int32_t poison;  // test knob (options.flags bit 1): fill shared staging buffers with garbage first
     const int8_t *subst;  // NULL, or an alphabet x alphabet substitution matrix (device memory)
     int32_t alphabet;
+    int32_t zdrop;        // Z-drop threshold (c-amb-19), < 0 = off
 };
 
 // Result of one extension task (L or R of one pair), 24 bytes.
@@ -135,6 +136,14 @@ template <> struct PoolFmt<LOGAN_SEQ_U8> {
 // matrix (options.subst). Same pool layout as LOGAN_SEQ_U8.
 constexpr int FMT_U8S = 2;
 template <> struct PoolFmt<FMT_U8S> : PoolFmt<LOGAN_SEQ_U8> {};
+// FMT | FMT_Z: the same format with the Z-drop stop compiled in (c-amb-19);
+// the plain formats carry no Z-drop code at all (register pressure).
+constexpr int FMT_Z = 4;
+template <> struct PoolFmt<LOGAN_SEQ_U8 | FMT_Z> : PoolFmt<LOGAN_SEQ_U8> {};
+template <> struct PoolFmt<LOGAN_SEQ_2BIT | FMT_Z> : PoolFmt<LOGAN_SEQ_2BIT> {};
+template <> struct PoolFmt<FMT_U8S | FMT_Z> : PoolFmt<LOGAN_SEQ_U8> {};
+__host__ __device__ constexpr int fmt_base(int f) { return f & 3; }
+__host__ __device__ constexpr bool fmt_z(int f) { return (f & FMT_Z) != 0; }
 
 // Substitution table of the register windows (FMT_U8S), in shared memory:
 // entry (a << 6) + b for codes a, b < 32 (a code is read modulo 32; entries

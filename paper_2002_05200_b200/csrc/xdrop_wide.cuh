@@ -146,6 +146,10 @@ __global__ void __launch_bounds__(NT) k_wide(const Params P, const LevelIO io,
             const int32_t gl = __reduce_max_sync(0xffffffffu, q_ok ? s_l[par][lane] : INT32_MIN);
             const bool h0 = (gf != INT32_MAX);
             if (h0 && gv > best) { best = gv; ai = gi; aj = d - gi; }  // P:178, strict increase
+            if (h0 && P.zdrop >= 0) {  // Z-drop stop (c-amb-19)
+                const int32_t off = abs((gi - ai) - ((d - gi) - aj));
+                if (best - gv > P.zdrop - P.gap * off) break;
+            }
             if (!h0 && !h1) break;  // P:186, c-amb-7
             // rotate: d becomes "1", d-1 becomes "2"
             lo2 = lo1; hi2 = hi1; F2 = F1; L2 = L1; h2 = h1;

@@ -89,6 +89,9 @@ template <> struct RegFmt<FMT_U8S> {
     __device__ __forceinline__ static uint32_t fa(uint32_t x) { return x < 256u ? (x & 31u) << 6 : 32u << 6; }
     __device__ __forceinline__ static uint32_t fb(uint32_t x) { return x < 256u ? (x & 31u) : 32u; }
 };
+template <> struct RegFmt<LOGAN_SEQ_2BIT | FMT_Z> : RegFmt<LOGAN_SEQ_2BIT> {};
+template <> struct RegFmt<LOGAN_SEQ_U8 | FMT_Z> : RegFmt<LOGAN_SEQ_U8> {};
+template <> struct RegFmt<FMT_U8S | FMT_Z> : RegFmt<FMT_U8S> {};
 
 // Group-uniform state of one task (replicated in each lane of the group).
 template <int FMT>
@@ -373,7 +376,7 @@ struct Window {
         const int32_t fg = DEAD - gp;  // max(up, left, fg) + gp >= DEAD: the floor
 
         const uint32_t two = 2u * (uint32_t)P.one;  // = 2, opaque to the compiler
-        constexpr bool SUB = FMT == FMT_U8S;
+        constexpr bool SUB = fmt_base(FMT) == FMT_U8S;
         const int32_t sr = -(Tc - st.Tq[PAR]);  // diagonal rebase (SUB: s' = table entry + sr)
         uint32_t X[NW];
 #pragma unroll
@@ -458,10 +461,23 @@ struct Window {
         int32_t lf = live ? gl * R + __ffs(live) - 1 : INT32_MAX;
         int32_t ll = live ? gl * R + 31 - __clz(live) : INT32_MIN;
         kmax = kmax - gl * R;  // key = u*KEYMUL + 1023 - (gl*R + r)
+        // Z-drop (c-amb-19) needs the max over in-matrix cells only: cells past
+        // the matrix stay below an earlier best (harmless for best) but can top
+        // an antidiagonal; near the matrix edges the key is recomputed masked
+        int32_t kz = kmax;
+        const bool zon = fmt_z(FMT) && P.zdrop >= 0;
+        if (zon && vmask != ((R == 32) ? 0xffffffffu : ((1u << R) - 1u))) {
+            kz = INT32_MIN / 2;  // no valid slot (the offset below must not wrap)
+#pragma unroll
+            for (int r = 0; r < R; ++r)
+                if ((vmask >> r) & 1u) kz = max(kz, (PAR ? O[r] : E[r]) * KEYMUL + (1023 - r));
+            kz -= gl * R;
+        }
         if (G > 1) {
             kmax = grp_max<G>(kmax, gmask);
             lf = grp_min<G>(lf, gmask);
             ll = grp_max<G>(ll, gmask);
+            if (zon) kz = grp_max<G>(kz, gmask);
         }
         const bool h = (lf != INT32_MAX);
 
@@ -476,6 +492,14 @@ struct Window {
                 st.arg_j = d - st.arg_i;
             }
         }
+        // Z-drop stop (c-amb-19): best - M_d > Z + |gap| * |(i_d - i*) - (j_d - j*)|
+        bool zstop = false;
+        if (zon && kz >= 0) {
+            const int32_t kzu = kz / KEYMUL;
+            const int32_t zi = st.S0 + (1023 - (kz - kzu * KEYMUL)) + ch;
+            const int32_t off = abs((zi - st.arg_i) - ((d - zi) - st.arg_j));
+            zstop = st.best - (kzu + Tc) > P.zdrop - P.gap * off;
+        }
         st.Tq[PAR] = Tc;
         st.Tn = st.best - P.xdrop;
         st.d = d;
@@ -488,10 +512,10 @@ struct Window {
         // every cell outside the window dead through both steps of the next
         // iteration. An odd antidiagonal that ends the task is followed by one
         // extra even one whose band is empty: no cells, no best change.
-        if (PAR == 1) return 0;
+        if (PAR == 1) return zstop ? 1 : 0;
 
-        // (7) termination: antidiagonals d and d-1 both empty (c-amb-7)
-        if (st.sF[0] == EMPTY_F && st.sF[1] == EMPTY_F) return 1;
+        // (7) termination: antidiagonals d and d-1 both empty (c-amb-7), or Z-drop
+        if (zstop || (st.sF[0] == EMPTY_F && st.sF[1] == EMPTY_F)) return 1;
 
         // (8) keep the live band of d and d-1 inside [S0+1, S0+W-2]
         const int32_t Fm = min(st.sF[0], st.sF[1]), Lm = max(st.sL[0], st.sL[1]);
@@ -677,7 +701,7 @@ __global__ void __launch_bounds__(128, (G == 1 ? LOGAN_L0_MINB : 1))
     extern __shared__ int32_t win_smem[];
     const int lane = threadIdx.x & 31;
     int8_t *tab = nullptr;
-    if (FMT == FMT_U8S) {  // the substitution table behind the per-thread shift slices
+    if (fmt_base(FMT) == FMT_U8S) {  // the substitution table behind the per-thread shift slices
         constexpr int S1 = Window<G, R, FMT>::SB_STRIDE;
         constexpr int S2 = HR > 0 ? Window<(HG > 0 ? HG : 32), (HR > 0 ? HR : 1), FMT>::SB_STRIDE : 0;
         tab = (int8_t *)(win_smem + blockDim.x * (S1 > S2 ? S1 : S2));

@@ -531,3 +531,37 @@ def test_subst_every_level(lvl):
         for lat, ho in ((False, 0), (True, 0), (False, 6)):
             got = _subst_run(b, M, -4, X, first_level=lvl, latency_first=lat, handover=ho)
             assert_same(*got, *ref, what=f"subst level {lvl} lat={lat} handover {ho} X={X}")
+
+
+# --------------------------------------------------------------------------
+# Z-drop (c-amb-19; the X-drop variant the paper names)
+
+@pytest.mark.parametrize("Z", [0, 3, 15, 60])
+def test_zdrop_dna_every_level(Z):
+    """Z-drop on DNA pairs (burst errors make it fire inside alignments),
+    forced onto every level and both shapes, with hand-overs: bit-exact."""
+    w = datagen.CONFIGS[1].with_(burst=0.5)
+    b = datagen.generate(w, n_pairs=120)
+    for X in (10, 40, 200):
+        ref = oracle.pairs_z(b.pool_u8, 0, b.q_off, b.q_len, b.t_off, b.t_len, b.q_seed, b.t_seed, w.k,
+                             1, -1, -1, X, Z, pool_len=b.pool_len)
+        for lvl, lat, ho in ((None, False, 0), (1, False, 0), (1, True, 6), (2, False, 40), (3, True, 0),
+                             (6, False, 0), (7, False, 0), (8, False, 0)):
+            for fmt in FMTS:
+                db = logan.to_device(b, fmt)
+                out, cells = logan.xdrop_batch(db, 1, -1, -1, X, first_level=lvl, latency_first=lat,
+                                               handover=ho, zdrop=Z)
+                torch.cuda.synchronize()
+                assert_same(out.cpu().numpy(), cells.cpu().numpy().view(np.uint64), *ref,
+                            what=f"zdrop Z={Z} X={X} level {lvl} lat={lat} ho={ho} fmt={fmt}")
+
+
+def test_zdrop_with_substitution_matrix():
+    M = datagen.protein_matrix()
+    b = datagen.protein_pairs(150, len_lo=50, len_hi=500, xdrop=60)
+    for X, Z in ((60, 10), (200, 40), (40, 0)):
+        ref = oracle.pairs_z(b.pool_u8, 0, b.q_off, b.q_len, b.t_off, b.t_len, b.q_seed, b.t_seed,
+                             b.workload.k, 0, 0, -4, X, Z, subst=M, pool_len=b.pool_len)
+        for lvl in (None, 1, 3, 8):
+            got = _subst_run(b, M, -4, X, first_level=lvl, zdrop=Z)
+            assert_same(*got, *ref, what=f"zdrop+subst X={X} Z={Z} level {lvl}")
