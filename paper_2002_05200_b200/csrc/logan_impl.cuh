@@ -1,0 +1,496 @@
+// logan_impl.cuh — device pipeline of the B200 X-drop library (kernels, level
+// table, run_batch<FMT>). Included by logan_xdrop.cu (the C ABI) and by one
+// translation unit per format (logan_fmt*.cu), which instantiate run_batch for
+// that format only, so the build compiles the formats in parallel.
+#pragma once
+#include <cstdio>
+#include <cstring>
+#include "logan_xdrop.h"
+#include "xdrop_common.cuh"
+#include "xdrop_band.cuh"
+#include "xdrop_wide.cuh"
+#include "xdrop_window.cuh"
+
+namespace logan {
+
+constexpr int NBUCKET = 2048;
+constexpr int NLEVEL = 8;  // 6 window levels + the band level + the CTA level
+constexpr int BAND_LEVEL = 6, WIDE_LEVEL = 7;
+constexpr int SETUP_THREADS = 256;
+
+__device__ __forceinline__ uint32_t cost_bucket(uint32_t c) {
+    // monotone log-linear bucket: 32 octaves x 64 sub-buckets (c >= 1)
+    const uint32_t e = 31u - __clz(c);
+    const uint32_t mant = e >= 6 ? (c >> (e - 6)) & 63u : (c << (6 - e)) & 63u;
+    return e * 64u + mant;
+}
+
+// Workspace layout (each region 256-byte aligned).
+// First-level window: one lane per task x w0 slots, w0 in {20, 24, 28, 32}
+// chosen at run time from X and the read lengths (auto_first_slots), or forced
+// by options.first_slots. LOGAN_L0_R (build knob) restricts it to one value.
+constexpr int NWIDTH = 6;  // register-window widths w0, 64, 128, 256, 512, 1024
+static const int kWidth[NWIDTH] = {32, 64, 128, 256, 512, 1024};  // [0]: the largest w0 (pool sizing)
+
+struct Layout {
+    size_t tres, tbucket, queue, listA, listB, recsA, recsB, hist, cursor_b, counters, wide, total;
+    size_t pool[NWIDTH];         // hand-over records written by window level w
+    uint32_t pool_cap[NWIDTH];
+    int64_t ntask, wide_stride;
+};
+
+constexpr int WIDE_CTAS = 296;  // 2 per SM on B200
+constexpr int NCTR = 64;
+constexpr int CTR_OUT = 16, CTR_FILL = 32, CTR_DONE = 48;
+
+static size_t align256(size_t x) { return (x + 255) & ~(size_t)255; }
+
+static Layout make_layout(int64_t n_pairs, int64_t max_ext_len) {
+    Layout L{};
+    const int64_t nt = 2 * n_pairs;
+    L.ntask = nt;
+    size_t o = 0;
+    L.tres = o;     o += align256(sizeof(TaskRes) * (size_t)nt);
+    L.tbucket = o;  o += align256(sizeof(uint16_t) * (size_t)nt);
+    L.queue = o;    o += align256(sizeof(uint32_t) * (size_t)nt);
+    L.listA = o;    o += align256(sizeof(uint32_t) * (size_t)nt);
+    L.listB = o;    o += align256(sizeof(uint32_t) * (size_t)nt);
+    L.recsA = o;    o += align256(sizeof(uint32_t) * (size_t)nt);
+    L.recsB = o;    o += align256(sizeof(uint32_t) * (size_t)nt);
+    for (int w = 0; w < NWIDTH; ++w) {
+        // at most 128 MiB of records per level; tasks beyond that restart
+        const int64_t rec_bytes = (int64_t)sizeof(int32_t) * rec_ints(kWidth[w]);
+        int64_t cap = ((int64_t)128 << 20) / rec_bytes;
+        if (cap > nt) cap = nt;
+        L.pool_cap[w] = (uint32_t)cap;
+        L.pool[w] = o;
+        o += align256((size_t)(rec_bytes * cap));
+    }
+    L.hist = o;     o += align256(sizeof(uint32_t) * NBUCKET);
+    L.cursor_b = o; o += align256(sizeof(uint32_t) * NBUCKET);
+    // counters: [0] queue count, [1 + lv] level cursors, [16 + lv] out counts,
+    // [32 + lv] record pool fill, [48] producer groups done (helpers)
+    L.counters = o; o += align256(sizeof(uint32_t) * NCTR);
+    L.wide_stride = max_ext_len + 2;
+    L.wide = o;     o += align256(sizeof(int32_t) * 3 * (size_t)L.wide_stride * WIDE_CTAS);
+    L.total = o;
+    return L;
+}
+
+// ---------------------------------------------------------------------------
+static __global__ void k_expand(const Params P, TaskRes *tres, uint16_t *tbucket, uint32_t *hist) {
+    __shared__ uint32_t sh[NBUCKET];
+    for (int b = threadIdx.x; b < NBUCKET; b += blockDim.x) sh[b] = 0;
+    __syncthreads();
+    for (int64_t p = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; p < P.n_pairs;
+         p += (int64_t)gridDim.x * blockDim.x) {
+        const bool ok = pair_valid(P, p);
+#pragma unroll
+        for (int side = 0; side < 2; ++side) {
+            const uint32_t task = (uint32_t)(2 * p + side);
+            int32_t m = 0, n = 0;
+            if (ok) {
+                const int32_t ql = P.q_len[p], tl = P.t_len[p], qs = P.q_seed[p], ts = P.t_seed[p];
+                m = side == 0 ? qs : ql - qs - P.k;
+                n = side == 0 ? ts : tl - ts - P.k;
+            }
+            uint16_t bk = 0xffff;  // not queued
+            if (ok && m > 0 && n > 0) {
+                bk = (uint16_t)cost_bucket((uint32_t)(m + n));
+                atomicAdd(&sh[bk], 1u);
+            } else {
+                TaskRes tr;
+                tr.best = 0; tr.i = 0; tr.j = 0; tr.flags = ok ? 0 : 1; tr.cells = 0;
+                tres[task] = tr;  // empty extension (c-amb-13) or invalid pair
+            }
+            tbucket[task] = bk;
+        }
+    }
+    __syncthreads();
+    for (int b = threadIdx.x; b < NBUCKET; b += blockDim.x)
+        if (sh[b]) atomicAdd(&hist[b], sh[b]);
+}
+
+// descending exclusive scan of the histogram (largest costs first)
+static __global__ void k_scan(const uint32_t *hist, uint32_t *cursor_b, uint32_t *qcount) {
+    __shared__ uint32_t part[SETUP_THREADS];
+    constexpr int PER = NBUCKET / SETUP_THREADS;
+    const int t = threadIdx.x;
+    // thread t owns buckets in descending order: positions [t*PER, (t+1)*PER) of the reversed array
+    uint32_t loc[PER];
+    uint32_t s = 0;
+#pragma unroll
+    for (int q = 0; q < PER; ++q) {
+        loc[q] = hist[NBUCKET - 1 - (t * PER + q)];
+        s += loc[q];
+    }
+    part[t] = s;
+    __syncthreads();
+    for (int o = 1; o < SETUP_THREADS; o <<= 1) {
+        const uint32_t v = t >= o ? part[t - o] : 0;
+        __syncthreads();
+        part[t] += v;
+        __syncthreads();
+    }
+    uint32_t run = part[t] - s;  // exclusive
+#pragma unroll
+    for (int q = 0; q < PER; ++q) {
+        cursor_b[NBUCKET - 1 - (t * PER + q)] = run;
+        run += loc[q];
+    }
+    if (t == SETUP_THREADS - 1) *qcount = part[t];
+}
+
+static __global__ void k_scatter(int64_t ntask, const uint16_t *tbucket, uint32_t *cursor_b, uint32_t *queue) {
+    for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < ntask;
+         t += (int64_t)gridDim.x * blockDim.x) {
+        const uint16_t b = tbucket[t];
+        if (b != 0xffff) {
+            const uint32_t pos = atomicAdd(&cursor_b[b], 1u);
+            queue[pos] = (uint32_t)t;
+        }
+    }
+}
+
+template <int FMT>
+static __global__ void k_combine(const Params P, const TaskRes *tres, logan_result_t *out, uint64_t *cells) {
+    for (int64_t p = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; p < P.n_pairs;
+         p += (int64_t)gridDim.x * blockDim.x) {
+        const TaskRes L = tres[2 * p], R = tres[2 * p + 1];
+        logan_result_t r;
+        if ((L.flags | R.flags) & 3) {  // invalid pair, or wide scratch too small (max_ext_len)
+            r = {INT32_MIN, -1, -1, -1, -1};
+            if (cells) cells[p] = 0;
+        } else {
+            const int64_t qo = P.q_off[p], to = P.t_off[p];
+            const int32_t qs = P.q_seed[p], ts = P.t_seed[p];
+            int32_t seed = 0;  // ungapped seed score (c-amb-10)
+            for (int32_t u = 0; u < P.k; ++u) {
+                const uint32_t a = pool_base<FMT>(P, qo + qs + u), b = pool_base<FMT>(P, to + ts + u);
+                if (P.subst) seed += ((a & 31u) < (uint32_t)P.alphabet && (b & 31u) < (uint32_t)P.alphabet)
+                                         ? P.subst[(a & 31u) * P.alphabet + (b & 31u)] : 0;
+                else seed += a == b ? P.match : P.mismatch;
+            }
+            r.score = seed + L.best + R.best;
+            r.q_begin = qs - L.i;
+            r.q_end = qs + P.k + R.i;
+            r.t_begin = ts - L.j;
+            r.t_end = ts + P.k + R.j;
+            if (cells) cells[p] = L.cells + R.cells;
+        }
+        out[p] = r;
+    }
+}
+
+// ---------------------------------------------------------------------------
+// Level table: register windows of W = 32, 64, 128, 256, 1024 diagonal slots.
+// Throughput shape: G = W/32 lanes x R = 32 slots (many tasks in flight).
+// Latency shape: one warp per task, R = W/32 slots per lane (few tasks left:
+// the step's critical path is short). Level 5 is the unbounded CTA path.
+// Helper shape for the first level: the next width's throughput shape (many
+// tasks per helper warp, default) or its latency shape (one warp per task);
+// LOGAN_HELPER_WARPS warps (the last warp of as many blocks) are helpers.
+#ifndef LOGAN_HELPER_THROUGHPUT
+#define LOGAN_HELPER_THROUGHPUT 1
+#endif
+#ifndef LOGAN_HELPER_WARPS
+#define LOGAN_HELPER_WARPS 96
+#endif
+#if LOGAN_HELPER_THROUGHPUT
+#define LOGAN_HSHAPE(W) ((W) / 32), 32
+#else
+#define LOGAN_HSHAPE(W) 32, ((W) / 32)
+#endif
+
+template <int G, int R, int FMT, int HG, int HR>
+static cudaError_t launch_win(const Params &P, const LevelIO &io_in, const LevelIO &hio, int sms, cudaStream_t s) {
+    constexpr int S1 = Window<G, R, FMT>::SB_STRIDE;
+    constexpr int S2 = HR > 0 ? Window<(HG > 0 ? HG : 32), (HR > 0 ? HR : 1), FMT>::SB_STRIDE : 0;
+    const size_t smem = 128 * sizeof(int32_t) * (S1 > S2 ? S1 : S2) + (fmt_base(FMT) == FMT_U8S ? SUBST_TAB_BYTES : 0);
+    auto kern = k_window<G, R, FMT, HG, HR>;
+    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e != cudaSuccess) return e;
+    int occ = 0;
+    e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, 128, smem);
+    if (e != cudaSuccess) return e;
+    if (occ < 1) occ = 1;
+    const int grid = sms * occ;
+    LevelIO io = io_in;
+    if (HR > 0) {
+        io.helpers = grid < LOGAN_HELPER_WARPS ? grid : LOGAN_HELPER_WARPS;
+        io.workers = (uint32_t)((grid * 128 - io.helpers * 32) / G);
+    } else {
+        io.helpers = 0;
+    }
+    kern<<<grid, 128, smem, s>>>(P, io, hio);
+    return cudaGetLastError();
+}
+
+// wi = width index; latency = run the latency shape; helpers = first level with
+// in-kernel escalation helpers running the next width
+template <int FMT>
+static cudaError_t launch_first(int w0, bool helpers, const Params &P, const LevelIO &io, const LevelIO &hio,
+                                int sms, cudaStream_t s) {
+#ifdef LOGAN_L0_R
+    w0 = LOGAN_L0_R;
+#endif
+    if constexpr (fmt_base(FMT) == FMT_U8S || fmt_z(FMT)) {  // matrices, Z-drop: no in-kernel helpers
+        switch (w0) {
+            case 20: return launch_win<1, 20, FMT, 0, 0>(P, io, hio, sms, s);
+            case 24: return launch_win<1, 24, FMT, 0, 0>(P, io, hio, sms, s);
+            case 28: return launch_win<1, 28, FMT, 0, 0>(P, io, hio, sms, s);
+            default: return launch_win<1, 32, FMT, 0, 0>(P, io, hio, sms, s);
+        }
+    }
+    switch (w0) {
+        case 20: return helpers ? launch_win<1, 20, FMT, LOGAN_HSHAPE(64)>(P, io, hio, sms, s)
+                                : launch_win<1, 20, FMT, 0, 0>(P, io, hio, sms, s);
+        case 24: return helpers ? launch_win<1, 24, FMT, LOGAN_HSHAPE(64)>(P, io, hio, sms, s)
+                                : launch_win<1, 24, FMT, 0, 0>(P, io, hio, sms, s);
+        case 28: return helpers ? launch_win<1, 28, FMT, LOGAN_HSHAPE(64)>(P, io, hio, sms, s)
+                                : launch_win<1, 28, FMT, 0, 0>(P, io, hio, sms, s);
+        default: return helpers ? launch_win<1, 32, FMT, LOGAN_HSHAPE(64)>(P, io, hio, sms, s)
+                                : launch_win<1, 32, FMT, 0, 0>(P, io, hio, sms, s);
+    }
+}
+
+template <int FMT>
+static cudaError_t launch_width(int wi, bool latency, bool helpers, const Params &P, const LevelIO &io,
+                                const LevelIO &hio, int sms, cudaStream_t s, int w0, int w5) {
+    if (wi == 0 && !(latency && w0 == 32)) return launch_first<FMT>(w0, helpers && !latency, P, io, hio, sms, s);
+    constexpr bool HELP = fmt_base(FMT) != FMT_U8S && !fmt_z(FMT);
+    if (HELP && helpers && !latency) {
+        if constexpr (HELP) switch (wi) {
+            case 1: return launch_win<2, 32, FMT, LOGAN_HSHAPE(128)>(P, io, hio, sms, s);
+            case 2: return launch_win<4, 32, FMT, LOGAN_HSHAPE(256)>(P, io, hio, sms, s);
+            case 3: return launch_win<8, 32, FMT, LOGAN_HSHAPE(512)>(P, io, hio, sms, s);
+            case 4:
+                if (w5 == 640) return launch_win<16, 32, FMT, 32, 20>(P, io, hio, sms, s);
+                if (w5 == 768) return launch_win<16, 32, FMT, 32, 24>(P, io, hio, sms, s);
+                if (w5 == 896) return launch_win<16, 32, FMT, 32, 28>(P, io, hio, sms, s);
+                return launch_win<16, 32, FMT, 32, 32>(P, io, hio, sms, s);
+            default: break;
+        }
+    }
+    if (wi == 5) {  // the top window: one warp per task, R = w5 / 32 slots per lane
+        if (w5 == 640) return launch_win<32, 20, FMT, 0, 0>(P, io, hio, sms, s);
+        if (w5 == 768) return launch_win<32, 24, FMT, 0, 0>(P, io, hio, sms, s);
+        if (w5 == 896) return launch_win<32, 28, FMT, 0, 0>(P, io, hio, sms, s);
+    }
+    switch (wi * 2 + (latency ? 1 : 0)) {
+        case 1: return launch_win<32, 1, FMT, 0, 0>(P, io, hio, sms, s);
+        case 2: return launch_win<2, 32, FMT, 0, 0>(P, io, hio, sms, s);
+        case 3: return launch_win<32, 2, FMT, 0, 0>(P, io, hio, sms, s);
+        case 4: return launch_win<4, 32, FMT, 0, 0>(P, io, hio, sms, s);
+        case 5: return launch_win<32, 4, FMT, 0, 0>(P, io, hio, sms, s);
+        case 6: return launch_win<8, 32, FMT, 0, 0>(P, io, hio, sms, s);
+        case 7: return launch_win<32, 8, FMT, 0, 0>(P, io, hio, sms, s);
+        case 8: return launch_win<16, 32, FMT, 0, 0>(P, io, hio, sms, s);
+        case 9: return launch_win<32, 16, FMT, 0, 0>(P, io, hio, sms, s);
+        case 10:
+        case 11: return launch_win<32, 32, FMT, 0, 0>(P, io, hio, sms, s);
+        default: return cudaErrorInvalidValue;
+    }
+}
+
+static int auto_first_level(int32_t xdrop) {
+    // the band of true pairs is about X + a few slots wide
+    if (xdrop <= 20) return 0;   // W = w0 (auto_first_slots)
+    if (xdrop <= 50) return 1;   // W = 64
+    if (xdrop <= 110) return 2;  // W = 128
+    if (xdrop <= 230) return 3;  // W = 256
+    if (xdrop <= 480) return 4;  // W = 512
+    if (xdrop <= 1000) return 5; // W = 1024
+    if (xdrop <= BAND_XMAX) return BAND_LEVEL;  // the band follows the alignment's width
+    return WIDE_LEVEL;           // unbounded CTA level
+}
+
+// Width of the top window level (one warp per task): 640, 768 or 896 slots when
+// X starts tasks there with a band of about X + 8 slots (X in (480, 820]), so
+// the window is not half empty; 1024 otherwise (X near 1000, or bands that
+// escalated from narrower windows, e.g. spurious pairs at small X).
+static int auto_top_width(int32_t xdrop) {
+    if (xdrop <= 480) return 1024;
+    if (xdrop <= 560) return 640;
+    if (xdrop <= 680) return 768;
+    if (xdrop <= 820) return 896;
+    return 1024;
+}
+
+// Slots of the first window: the band of true pairs is about X + 8 slots wide at
+// its widest, and long reads drift more between re-centrings.
+static int auto_first_slots(int32_t xdrop, int64_t max_ext) {
+    if (xdrop <= 12) return 20;
+    if (xdrop <= 16) return 24;
+    if (xdrop <= 20) return max_ext > 6000 ? 32 : 28;
+    return 32;
+}
+
+template <int FMT>
+int run_batch(const Params &P, const logan_options_t *opt, logan_result_t *out, uint64_t *cells,
+                     logan_stats_t *stats, uint8_t *ws, const Layout &L, cudaStream_t s) {
+    TaskRes *tres = (TaskRes *)(ws + L.tres);
+    uint16_t *tbucket = (uint16_t *)(ws + L.tbucket);
+    uint32_t *queue = (uint32_t *)(ws + L.queue);
+    uint32_t *lists[2] = {(uint32_t *)(ws + L.listA), (uint32_t *)(ws + L.listB)};
+    uint32_t *hist = (uint32_t *)(ws + L.hist);
+    uint32_t *cursor_b = (uint32_t *)(ws + L.cursor_b);
+    uint32_t *ctr = (uint32_t *)(ws + L.counters);
+    int32_t *wide = (int32_t *)(ws + L.wide);
+
+    int dev = 0, sms = 148;
+    if (cudaGetDevice(&dev) != cudaSuccess) return LOGAN_ECUDA;
+    if (cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess) return LOGAN_ECUDA;
+
+    if (cudaMemsetAsync(hist, 0, sizeof(uint32_t) * NBUCKET, s) != cudaSuccess) return LOGAN_ECUDA;
+    if (cudaMemsetAsync(ctr, 0, sizeof(uint32_t) * NCTR, s) != cudaSuccess) return LOGAN_ECUDA;
+    if (stats && cudaMemsetAsync(stats, 0, sizeof(logan_stats_t), s) != cudaSuccess) return LOGAN_ECUDA;
+
+    cudaEvent_t const *ev = (opt && opt->timing_events) ? (cudaEvent_t const *)opt->timing_events : nullptr;
+    auto mark = [&](int stage, int which) -> bool {
+        return !ev || cudaEventRecord(ev[2 * stage + which], s) == cudaSuccess;
+    };
+    if (!mark(0, 0)) return LOGAN_ECUDA;
+    const int64_t per_block = SETUP_THREADS;
+    int grid = (int)((P.n_pairs + per_block - 1) / per_block);
+    if (grid > sms * 8) grid = sms * 8;
+    if (grid < 1) grid = 1;
+    k_expand<<<grid, SETUP_THREADS, 0, s>>>(P, tres, tbucket, hist);
+    k_scan<<<1, SETUP_THREADS, 0, s>>>(hist, cursor_b, &ctr[0]);
+    int grid2 = (int)((L.ntask + per_block - 1) / per_block);
+    if (grid2 > sms * 8) grid2 = sms * 8;
+    if (grid2 < 1) grid2 = 1;
+    k_scatter<<<grid2, SETUP_THREADS, 0, s>>>(L.ntask, tbucket, cursor_b, queue);
+    if (cudaGetLastError() != cudaSuccess) return LOGAN_ECUDA;
+    if (!mark(0, 1)) return LOGAN_ECUDA;
+
+    // level choice from the expected band width: about X slots under +1/-1/-1;
+    // with a substitution matrix about X / |gap| (moving one slot off the
+    // alignment's diagonal costs two gaps against at most X of slack)
+    const int32_t xband = fmt_base(FMT) == FMT_U8S ? (P.xdrop + (-P.gap) - 1) / (-P.gap) : P.xdrop;
+    int first = (opt && opt->first_level > 0) ? opt->first_level - 1 : auto_first_level(xband);
+    // no band level for matrices or Z-drop: those tasks go on to the CTA level
+    constexpr bool no_band = fmt_base(FMT) == FMT_U8S || fmt_z(FMT);
+    if (no_band && first == BAND_LEVEL) first = WIDE_LEVEL;
+    if (first < 0 || first > NLEVEL - 1) return LOGAN_EINVAL;
+    uint32_t *recs[2] = {(uint32_t *)(ws + L.recsA), (uint32_t *)(ws + L.recsB)};
+    const int w0 = (opt && opt->first_slots > 0) ? opt->first_slots : auto_first_slots(xband, L.wide_stride - 2);
+    const int w5 = auto_top_width(xband);
+    auto width_of = [&](int lv) { return lv == 0 ? w0 : (lv == NWIDTH - 1 ? w5 : kWidth[lv]); };
+    const uint32_t *in_list = queue;
+    const uint32_t *in_recs = nullptr;
+    const int32_t *rec_in = nullptr;
+    int64_t rec_in_stride = 0;
+    const uint32_t *in_count = &ctr[0];
+    int out_sel = 0;
+    // below this many tasks a level runs in its latency shape (one warp per task)
+    const uint32_t latency_below = (uint32_t)sms * 16u;
+    // the IO of window level lv, given its input list / records
+    auto level_io = [&](int lv, const uint32_t *lst, const uint32_t *cnt, const uint32_t *irecs,
+                        const int32_t *rin, int64_t rin_stride, int osel) {
+        LevelIO io{};
+        io.list = lst;
+        io.count = cnt;
+        io.cursor = &ctr[1 + lv];
+        io.out_list = lists[osel];
+        io.out_count = &ctr[CTR_OUT + lv];
+        io.stats = stats;
+        io.level = lv;
+        io.tres = tres;
+        io.in_recs = irecs;
+        io.rec_in = rin;
+        io.rec_in_stride = rin_stride;
+        io.handover = opt ? opt->handover : 0;
+        io.min_count = 0;
+        io.max_count = 0xffffffffu;
+        if (lv < NWIDTH) {
+            io.out_recs = recs[osel];
+            io.rec_out = (int32_t *)(ws + L.pool[lv]);
+            io.rec_out_stride = rec_ints(width_of(lv));
+            io.rec_out_cap = L.pool_cap[lv];
+            io.rec_out_count = &ctr[CTR_FILL + lv];
+        }
+        return io;
+    };
+    // Few tasks (e.g. long reads spread over many GPUs): the throughput shape
+    // would leave SMs with too few warps to hide the per-antidiagonal latency,
+    // so the first level runs one warp per task instead (measured on C5 with
+    // 2,500 pairs: 260 vs 158 GCUPS).
+    const int64_t groups_needed = L.ntask * (first < NWIDTH ? width_of(first) / 32 : 1) / 32;  // warps
+    const bool few_tasks = first > 0 && first < NWIDTH && groups_needed < (int64_t)sms * 16;
+    const bool latency_first = (opt && (opt->flags & 1)) || few_tasks;
+    for (int lv = first; lv < NLEVEL; ++lv) {
+        // substitution matrices have no band level: tasks that outgrow the widest
+        // window go straight on to the CTA level (which restarts them)
+        if (no_band && lv == BAND_LEVEL) continue;
+        LevelIO io = level_io(lv, in_list, in_count, in_recs, rec_in, rec_in_stride, out_sel);
+        cudaError_t e = cudaSuccess;
+        if (!mark(1 + lv, 0)) return LOGAN_ECUDA;
+        if (lv < NWIDTH) {
+            if (lv == first) {
+                const bool helpers = !latency_first && lv + 1 < NWIDTH;
+                LevelIO hio{};
+                if (helpers) {
+                    // the next level's IO: it reads this level's hand-overs
+                    hio = level_io(lv + 1, lists[out_sel], &ctr[CTR_OUT + lv], recs[out_sel],
+                                   (const int32_t *)(ws + L.pool[lv]), rec_ints(width_of(lv)), out_sel ^ 1);
+                    io.done = &ctr[CTR_DONE];
+                    // entries are published by writing the task id: start from NO_TASK
+                    if (cudaMemsetAsync(lists[out_sel], 0xff, sizeof(uint32_t) * (size_t)L.ntask, s) != cudaSuccess)
+                        return LOGAN_ECUDA;
+                }
+                e = launch_width<FMT>(lv, latency_first, helpers, P, io, hio, sms, s, w0, w5);
+            } else {
+                io.max_count = latency_below;
+                e = launch_width<FMT>(lv, true, false, P, io, io, sms, s, w0, w5);
+                if (e == cudaSuccess) {
+                    io.min_count = latency_below;
+                    io.max_count = 0xffffffffu;
+                    e = launch_width<FMT>(lv, false, false, P, io, io, sms, s, w0, w5);
+                }
+            }
+        } else if (lv == BAND_LEVEL) {
+          if constexpr (!no_band) {
+            const int smem = (int)BandSmem<FMT>::BYTES;
+            e = cudaFuncSetAttribute(k_band<FMT>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+            int per_sm = 0;
+            if (e == cudaSuccess)
+                e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_band<FMT>, BAND_NT, smem);
+            if (e == cudaSuccess) {
+                k_band<FMT><<<sms * (per_sm > 0 ? per_sm : 1), BAND_NT, smem, s>>>(P, io);
+                e = cudaGetLastError();
+            }
+          }
+        } else {
+            if constexpr (fmt_base(FMT) == FMT_U8S)
+                k_wide<FMT, SUBST_THREADS, true><<<WIDE_CTAS, SUBST_THREADS, 0, s>>>(P, io, wide, L.wide_stride);
+            else
+                k_wide<FMT><<<WIDE_CTAS, WIDE_THREADS, 0, s>>>(P, io, wide, L.wide_stride);
+            e = cudaGetLastError();
+        }
+        if (e != cudaSuccess) return LOGAN_ECUDA;
+        if (!mark(1 + lv, 1)) return LOGAN_ECUDA;
+        in_list = lists[out_sel];
+        in_recs = (lv < NWIDTH) ? recs[out_sel] : nullptr;
+        rec_in = (lv < NWIDTH) ? (const int32_t *)(ws + L.pool[lv]) : nullptr;
+        rec_in_stride = (lv < NWIDTH) ? rec_ints(width_of(lv)) : 0;
+        in_count = &ctr[CTR_OUT + lv];
+        out_sel ^= 1;
+    }
+    int grid3 = (int)((P.n_pairs + per_block - 1) / per_block);
+    if (grid3 > sms * 8) grid3 = sms * 8;
+    if (grid3 < 1) grid3 = 1;
+    if (!mark(LOGAN_N_STAGES - 1, 0)) return LOGAN_ECUDA;
+    k_combine<FMT><<<grid3, SETUP_THREADS, 0, s>>>(P, tres, out, cells);
+    if (cudaGetLastError() != cudaSuccess) return LOGAN_ECUDA;
+    if (!mark(LOGAN_N_STAGES - 1, 1)) return LOGAN_ECUDA;
+    return LOGAN_OK;
+}
+
+// explicit instantiations live in logan_fmt*.cu (one format per translation unit)
+#define LOGAN_RUN_BATCH_SIG(F)                                                                   \
+    int run_batch<F>(const Params &P, const logan_options_t *opt, logan_result_t *out, uint64_t *cells, \
+                     logan_stats_t *stats, uint8_t *ws, const Layout &L, cudaStream_t s)
+
+}  // namespace logan
+
