@@ -46,6 +46,8 @@ def parse_args():
                          "substitution matrix (SURVEY §8f row 4)")
     ap.add_argument("--pairs", type=int, default=None, help="pairs per GPU (default: the config's)")
     ap.add_argument("--xdrop", type=int, default=None)
+    ap.add_argument("--zdrop", type=int, default=None,
+                    help="also stop extensions by Z-drop with this Z (DESIGN.md c-amb-19; off by default)")
     ap.add_argument("--fmt", choices=["2bit", "u8"], default="2bit")
     ap.add_argument("--first-level", type=int, default=0)
     ap.add_argument("--latency-first", action="store_true",
@@ -84,10 +86,20 @@ def make_batch(args, w, n, pair_base=0, u8=False, two_bit=True):
     return datagen.generate(w, n_pairs=n, pair_base=pair_base, u8=u8, two_bit=two_bit)
 
 
+ZDROP = None  # set from --zdrop in main / run_reference
+
+
 def run_oracle(batch, w, sl, threads):
     """The oracle on pairs ``sl`` of the batch -> per-pair cells."""
     import oracle
     import datagen
+    if ZDROP is not None:
+        sub = datagen.protein_matrix() if batch.pool_2bit is None else None
+        pool, fmt = (batch.pool_u8, 0) if sub is not None else (batch.pool_2bit, 1)
+        _, cells = oracle.pairs_z(pool, fmt, batch.q_off[sl], batch.q_len[sl], batch.t_off[sl], batch.t_len[sl],
+                                  batch.q_seed[sl], batch.t_seed[sl], w.k, w.match, w.mismatch, w.gap, w.xdrop,
+                                  ZDROP, subst=sub, pool_len=batch.pool_len, n_threads=threads)
+        return cells
     if batch.pool_2bit is None:  # protein codes: the substitution-matrix oracle
         _, cells = oracle.pairs_subst(batch.pool_u8, batch.q_off[sl], batch.q_len[sl], batch.t_off[sl],
                                       batch.t_len[sl], batch.q_seed[sl], batch.t_seed[sl], w.k,
@@ -112,6 +124,8 @@ def config_dict(w, n, fmt, first_level, world):
          "parallelism": f"pairs sharded over {world} GPU(s), no data-path collective"}
     if first_level:
         d["first_level"] = first_level
+    if ZDROP is not None:
+        d["zdrop"] = ZDROP
     return d
 
 
@@ -185,6 +199,8 @@ def oracle_sample(batch, w, seconds, threads):
 
 def run_reference(args):
     """--impl reference: the oracle (the only reference this tier has) on host cores."""
+    global ZDROP
+    ZDROP = args.zdrop
     rank = int(os.environ.get("RANK", "0"))
     if rank != 0:
         return 0
@@ -222,9 +238,11 @@ def run_reference(args):
 
 # --------------------------------------------------------------------------- our arm
 def main():
+    global ZDROP
     args = parse_args()
     if args.impl == "reference":
         return run_reference(args)
+    ZDROP = args.zdrop
 
     import numpy as np
     import torch
@@ -262,7 +280,7 @@ def main():
     def step(events=None, stats=None):
         logan.xdrop_batch(db, w.match, w.mismatch, w.gap, w.xdrop, workspace=ws, out=out, cells=cells,
                           stats=stats, first_level=first, stream=stream, timing_events=events,
-                          latency_first=args.latency_first, subst=subst)
+                          latency_first=args.latency_first, subst=subst, zdrop=args.zdrop)
 
     # one untimed run with device stats: per-level task and cell counts (deterministic)
     st = logan.new_stats(dev)
@@ -387,7 +405,8 @@ def main():
         def e2e_step(s):
             logan.xdrop_batch_host(hp[0], fmt, batch.pool_len, *hp[1:], w.k, w.match, w.mismatch,
                                    w.gap, w.xdrop, arenas[s % 2], out=hout[s % 2], cells=hcells[s % 2],
-                                   first_level=first, stream=streams[s % 2], asynchronous=True, subst=subst)
+                                   first_level=first, stream=streams[s % 2], asynchronous=True, subst=subst,
+                                   zdrop=args.zdrop)
 
         for s_ in range(2):
             e2e_step(s_)

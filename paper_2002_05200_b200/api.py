@@ -172,7 +172,7 @@ def xdrop_batch_host(pool: np.ndarray, fmt: int, pool_len: int, q_off, q_len, t_
                      q_seed, t_seed, k: int, match: int, mismatch: int, gap: int, xdrop: int,
                      arena: HostArena, out: np.ndarray | None = None,
                      cells: np.ndarray | None = None, first_level: int | None = None, stream=None,
-                     asynchronous: bool = False, subst=None):
+                     asynchronous: bool = False, subst=None, zdrop: int | None = None):
     """End-to-end call with HOST buffers (numpy; pinned memory copies fastest).
 
     ``asynchronous=True`` returns right after enqueuing (``logan_xdrop_batch_host_async``):
@@ -194,7 +194,7 @@ def xdrop_batch_host(pool: np.ndarray, fmt: int, pool_len: int, q_off, q_len, t_
     ptr = lambda a: a.ctypes.data
     fn = lib.logan_xdrop_batch_host_async if asynchronous else lib.logan_xdrop_batch_host
     st = fn(ptr(pool), fmt, pool_len, *[ptr(a) for a in arrs], n, k, sc,
-            _opts(first_level, subst=subst), ptr(out), ptr(cells),
+            _opts(first_level, subst=subst, zdrop=zdrop), ptr(out), ptr(cells),
             arena.tensor.data_ptr(), arena.nbytes, stream.cuda_stream)
     _lib.check(st)
     return out, cells
