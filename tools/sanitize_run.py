@@ -22,3 +22,17 @@ for fmt in ((logan.LOGAN_SEQ_2BIT,) if small else (logan.LOGAN_SEQ_2BIT, logan.L
         out, cells = logan.xdrop_batch(db, 1, -1, -1, 50, first_level=lvl, latency_first=lat, handover=ho)
         torch.cuda.synchronize()
         print(fmt, lvl, lat, ho, int(cells.sum()), flush=True)
+
+# substitution matrices and Z-drop (FMT_U8S and FMT | FMT_Z builds)
+M = torch.as_tensor(datagen.protein_matrix()).cuda()
+pb = datagen.protein_pairs(6 if small else 40, len_lo=50, len_hi=400)
+dpb = logan.to_device(pb, logan.LOGAN_SEQ_U8)
+for lvl, z in ((None, None), (1, 10), (3, None), (8, 5)):
+    out, cells = logan.xdrop_batch(dpb, 1, -1, -4, 40, first_level=lvl, subst=M, zdrop=z)
+    torch.cuda.synchronize()
+    print("subst", lvl, z, int(cells.sum()), flush=True)
+db = logan.to_device(b, logan.LOGAN_SEQ_2BIT)
+for lvl, z in ((None, 20), (2, 0), (8, 10)):
+    out, cells = logan.xdrop_batch(db, 1, -1, -1, 50, first_level=lvl, zdrop=z)
+    torch.cuda.synchronize()
+    print("zdrop", lvl, z, int(cells.sum()), flush=True)
