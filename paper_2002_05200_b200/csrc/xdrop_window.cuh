@@ -482,15 +482,14 @@ struct Window {
         const bool h = (lf != INT32_MAX);
 
         // (6) best after the complete antidiagonal; argmax on strict increase
-        if (kmax >= 0) {
+        // V = u + T_d > best_{d-1} = T_d + X  <=>  u > X  <=>  kmax >= (X + 1) * KEYMUL:
+        // the key decode runs only on antidiagonals that raise best
+        if (kmax >= (P.xdrop + 1) * KEYMUL) {
             const int32_t ku = kmax / KEYMUL;
-            const int32_t V = ku + Tc;
-            if (V > st.best) {
-                st.best = V;
-                const int32_t slot = st.S0 + (1023 - (kmax - ku * KEYMUL));
-                st.arg_i = slot + ch;
-                st.arg_j = d - st.arg_i;
-            }
+            st.best = ku + Tc;
+            const int32_t slot = st.S0 + (1023 - (kmax - ku * KEYMUL));
+            st.arg_i = slot + ch;
+            st.arg_j = d - st.arg_i;
         }
         // Z-drop stop (c-amb-19): best - M_d > Z + |gap| * |(i_d - i*) - (j_d - j*)|
         bool zstop = false;
