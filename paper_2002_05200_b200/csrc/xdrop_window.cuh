@@ -345,13 +345,17 @@ struct Window {
         //     Empty antidiagonals carry EMPTY_F / EMPTY_L and drop out of the
         //     min / max; d = 1 clips to an empty band by itself.
         {
-            // columns of slots on d-1 and d-2 (PAR fixes the parity of d)
-            const int32_t c1 = PAR ? (d - 1) >> 1 : d >> 1;
-            const int32_t c2 = PAR ? (d - 1) >> 1 : (d - 2) >> 1;
-            // d-1 has the other parity, d-2 this parity
-            const int32_t lo = max(min(st.sF[1 - PAR] + c1, st.sF[PAR] + c2 + 1), max(1, d - st.n));
-            const int32_t hi = min(max(st.sL[1 - PAR] + c1, st.sL[PAR] + c2) + 1, min(st.m, d - 1));
-            st.cells += (uint32_t)max(hi - lo + 1, 0);
+            // column of slot 0 on d-1 (c1) and d-2 (c2 = c1 - 1 + PAR), so with
+            // c = c1: odd d: lo = max(min(F1, F2 + 1) + c, 1, d-n), hi = min(max(L1, L2) + c + 1, m, d-1);
+            // even d: lo = max(min(F1, F2) + c, 1, d-n), hi = min(max(L1, L2 - 1) + c + 1, m, d-1)
+            // (3-input DPX min / max; d-1 has the other parity, d-2 this parity)
+            const int32_t c = PAR ? (d - 1) >> 1 : d >> 1;
+            const int32_t F1 = st.sF[1 - PAR], F2 = st.sF[PAR], L1 = st.sL[1 - PAR], L2 = st.sL[PAR];
+            const int32_t fmin = PAR ? min(F1, F2 + 1) : min(F1, F2);
+            const int32_t lmax = PAR ? max(L1, L2) : max(L1, L2 - 1);
+            const int32_t lo = __vimax3_s32(fmin + c, 1, d - st.n);
+            const int32_t hi = __vimin3_s32(lmax + c + 1, st.m, d - 1);
+            st.cells += (uint32_t)__vimax_s32_relu(hi - lo + 1, 0);
         }
 
         // (2) bases for antidiagonal d
