@@ -207,7 +207,7 @@ def run_reference(args):
     import datagen
     w, n = workload(args)
     threads = len(os.sched_getaffinity(0))
-    probe = make_batch(args, w, min(n, max(threads * 64, 512)))
+    probe = make_batch(args, w, min(n, max(threads * 1024, 4096)))
     cal = oracle_sample(probe, w, args.ref_step_seconds, threads)
     per_step = cal["pairs"]
     batch = make_batch(args, w, min(n, per_step))
