@@ -462,8 +462,10 @@ struct Window {
             vmask = (rlo <= rhi) ? ((0xffffffffu >> (31 - rhi)) & ~((1u << rlo) - 1u)) : 0u;
         }
         const uint32_t live = ~dead & vmask;
-        int32_t lf = live ? gl * R + __ffs(live) - 1 : INT32_MAX;
-        int32_t ll = live ? gl * R + 31 - __clz(live) : INT32_MIN;
+        // one lane per task: the extremes are only read when live != 0, so no
+        // sentinel selects (a sub-warp or warp group reduces with sentinels)
+        int32_t lf = G == 1 ? __ffs(live) - 1 : (live ? gl * R + __ffs(live) - 1 : INT32_MAX);
+        int32_t ll = G == 1 ? 31 - __clz(live) : (live ? gl * R + 31 - __clz(live) : INT32_MIN);
         kmax = kmax - gl * R;  // key = u*KEYMUL + 1023 - (gl*R + r)
         // Z-drop (c-amb-19) needs the max over in-matrix cells only: cells past
         // the matrix stay below an earlier best (harmless for best) but can top
@@ -483,7 +485,7 @@ struct Window {
             ll = grp_max<G>(ll, gmask);
             if (zon) kz = grp_max<G>(kz, gmask);
         }
-        const bool h = (lf != INT32_MAX);
+        const bool h = G == 1 ? live != 0 : (lf != INT32_MAX);
 
         // (6) best after the complete antidiagonal; argmax on strict increase
         // V = u + T_d > best_{d-1} = T_d + X  <=>  u > X  <=>  kmax >= (X + 1) * KEYMUL:
