@@ -200,6 +200,8 @@ struct Stream {
     uint32_t nxt;        // wp[dir] (prefetched)
     int32_t idx;         // extension index returned by the next next()
     int32_t sh;          // bit offset of that base inside cur
+    int32_t nld;         // words that may still be prefetched beyond wp in direction dir
+                         // (going backwards: the words above the pool start)
 
     __device__ __forceinline__ void seek(const Params &P, int32_t i) {
         idx = i;
@@ -207,19 +209,45 @@ struct Stream {
         const int64_t pos = s.base + (int64_t)s.dir * (c - 1);
         const int64_t wi = pos >> F::LOG_CPW;
         sh = F::BITS * (int32_t)(pos & (CPW - 1));
-        wp = P.pool + (wi < 0 ? 0 : (wi >= P.pool_words ? P.pool_words - 1 : wi));
+        const int64_t wc = wi < 0 ? 0 : (wi >= P.pool_words ? P.pool_words - 1 : wi);
+        wp = P.pool + wc;
+        nld = s.dir < 0 ? (int32_t)(wc < (1 << 30) ? wc : (1 << 30)) : (1 << 30);
         cur = __ldg(wp);
-        nxt = (s.dir < 0 && wp <= P.pool) ? 0u : __ldg(wp + s.dir);
+        nxt = nld > 0 ? __ldg(wp + s.dir) : 0u;
     }
 
     // word boundary crossed: shift the prefetched word in, prefetch the next one
+    // (going backwards, one crossing past the last base can put wp on the word
+    // before the pool: never prefetch below the pool start)
     __device__ __forceinline__ void refill(const Params &P) {
         sh -= s.dir * 32;
         wp += s.dir;
         cur = nxt;
-        // going backwards, one crossing past the last base can put wp on the word
-        // before the pool: never prefetch below the pool start
-        nxt = (s.dir < 0 && wp <= P.pool) ? 0u : __ldg(wp + s.dir);
+        --nld;
+        nxt = nld > 0 ? __ldg(wp + s.dir) : 0u;
+    }
+
+    // next() for the hot loop: the same result and state, with the refill
+    // predicated instead of branched (in a warp of independent tasks some lane
+    // crosses a word boundary on most steps, so the branch was nearly always
+    // taken by the warp) and the sentinel chosen by a select.
+    __device__ __forceinline__ uint32_t next_fast(uint32_t sent) {
+        const int32_t i = idx++;
+        const bool in = (uint32_t)(i - 1) < (uint32_t)s.len;  // 1 <= i <= len
+        const uint32_t c = (cur >> sh) & F::MASK;
+        const int32_t nsh = sh + (in ? s.dir * F::BITS : 0);
+        const bool need = (uint32_t)nsh >= 32u;
+        sh = nsh & 31;
+        const uint32_t *wn = wp + (need ? s.dir : 0);
+        cur = need ? nxt : cur;
+        nld -= need ? 1 : 0;
+        const uint32_t ld = (need && nld > 0) ? 1u : 0u;
+        uint32_t v = need ? 0u : nxt;
+        asm volatile("{\n\t.reg .pred p;\n\tsetp.ne.u32 p, %2, 0;\n\t@p ld.global.nc.u32 %0, [%1];\n\t}"
+                     : "+r"(v) : "l"(wn + s.dir), "r"(ld));
+        nxt = v;
+        wp = wn;
+        return in ? c : sent;
     }
 
     __device__ __forceinline__ uint32_t next(const Params &P, uint32_t sent) {
