@@ -362,12 +362,14 @@ struct Window {
         if (PAR == 1) {  // i advances: A fields move down one slot
             uint32_t in = 0;
             if (G > 1) in = __shfl_down_sync(gmask, Aw[0], 1, G) & FM;
-            if (gl == G - 1) in = RF::fa(st.sa.next_fast(RF::SA));
+            // one or two lanes per task: many lanes of the warp read a stream, so its
+            // refill is predicated; wider groups have few readers per warp: branch
+            if (gl == G - 1) in = RF::fa(G <= 2 ? st.sa.next_fast(RF::SA) : st.sa.next(P, RF::SA));
             shift_down(Aw, in);
         } else {         // j advances: B fields move up one slot
             uint32_t in = 0;
             if (G > 1) in = __shfl_up_sync(gmask, top_field(Bw), 1, G);
-            if (gl == 0) in = RF::fb(st.sb.next_fast(RF::SB));
+            if (gl == 0) in = RF::fb(G <= 2 ? st.sb.next_fast(RF::SB) : st.sb.next(P, RF::SB));
             shift_up(Bw, in);
         }
 
