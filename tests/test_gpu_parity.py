@@ -565,3 +565,29 @@ def test_zdrop_with_substitution_matrix():
         for lvl in (None, 1, 3, 8):
             got = _subst_run(b, M, -4, X, first_level=lvl, zdrop=Z)
             assert_same(*got, *ref, what=f"zdrop+subst X={X} Z={Z} level {lvl}")
+
+
+def test_config7_and_zdrop_full_size_sampled():
+    """Full-size runs of the f-4 modes in bench.py's launch configuration:
+    config 7 (100K protein-like pairs, substitution matrix) and C2 with
+    Z-drop; sampled pairs against the oracle, the cell totals against the
+    per-pair sums, and Z-drop never exceeding the plain X-drop values."""
+    M = datagen.protein_matrix()
+    pb = datagen.protein_pairs(100_000)
+    o, c = _subst_run(pb, M, -4, 50)
+    idx = np.arange(0, pb.n_pairs, 97)
+    ref = oracle.pairs_subst(pb.pool_u8, pb.q_off[idx], pb.q_len[idx], pb.t_off[idx], pb.t_len[idx],
+                             pb.q_seed[idx], pb.t_seed[idx], pb.workload.k, M, -4, 50, pool_len=pb.pool_len)
+    assert_same(o[idx], c[idx], *ref, what="C7 sample")
+    w = datagen.CONFIGS[2]
+    b = datagen.generate(w)
+    db = logan.to_device(b, logan.LOGAN_SEQ_2BIT)
+    out, cells = logan.xdrop_batch(db, 1, -1, -1, w.xdrop, zdrop=5)
+    torch.cuda.synchronize()
+    oz, cz = out.cpu().numpy(), cells.cpu().numpy().view(np.uint64)
+    idx = np.arange(0, b.n_pairs, 97)
+    refz = oracle.pairs_z(b.pool_u8, 0, b.q_off[idx], b.q_len[idx], b.t_off[idx], b.t_len[idx], b.q_seed[idx],
+                          b.t_seed[idx], w.k, 1, -1, -1, w.xdrop, 5, pool_len=b.pool_len)
+    assert_same(oz[idx], cz[idx], *refz, what="C2 Z-drop sample")
+    plain = gpu_run(b, w.xdrop)
+    assert (cz <= plain[1]).all() and (oz[:, 0] <= plain[0][:, 0]).all()
