@@ -62,6 +62,10 @@ constexpr int32_t KEYMUL = 1027;
 #define LOGAN_L0_MINB 1
 #endif
 
+#ifndef LOGAN_NCHAIN
+#define LOGAN_NCHAIN 4
+#endif
+
 #ifndef LOGAN_MASK_FMA_CHAINS
 #define LOGAN_MASK_FMA_CHAINS 0
 #endif
@@ -389,9 +393,10 @@ struct Window {
         for (int q = 0; q < NW; ++q) X[q] = SUB ? Aw[q] + Bw[q] : Aw[q] ^ Bw[q];  // SUB: two table indices
 
         // (4) cells
-        int32_t kq[4];
-        uint32_t dq[4];
-        constexpr int RQ = (R + 3) / 4;
+        constexpr int NCH = LOGAN_NCHAIN;  // independent key / dead-mask chains per lane
+        int32_t kq[NCH];
+        uint32_t dq[NCH];
+        constexpr int RQ = (R + NCH - 1) / NCH;
         if (PAR == 1) {
             int32_t nb = DEAD;  // E[R] of this lane = E[0] of the next lane
             if (G > 1) {
@@ -445,11 +450,11 @@ struct Window {
         }
         int32_t kmax = kq[0];
 #pragma unroll
-        for (int c = 1; c < 4; ++c)
+        for (int c = 1; c < NCH; ++c)
             if (c * RQ < R) kmax = max(kmax, kq[c]);
         uint32_t dead = 0;
 #pragma unroll
-        for (int c = 0; c < 4; ++c)
+        for (int c = 0; c < NCH; ++c)
             if (c * RQ < R) dead |= dq[c] << (c * RQ);
 
         // (5) validity of slots for this lane: cells with i < 0 or j < 0 are dead
