@@ -505,8 +505,11 @@ struct Window {
             st.arg_j = d - st.arg_i;
         }
         // Z-drop stop (c-amb-19): best - M_d > Z + |gap| * |(i_d - i*) - (j_d - j*)|
+        // Every live u is >= 0 and best >= T_d + X, so a stop needs u_max < X - Z on
+        // this antidiagonal: key below (X - Z) * KEYMUL (cheap test first; an
+        // antidiagonal that raised best has u_max > X and never stops)
         bool zstop = false;
-        if (zon && kz >= 0) {
+        if (zon && kz >= 0 && kz < (P.xdrop - P.zdrop) * KEYMUL) {
             const int32_t kzu = kz / KEYMUL;
             const int32_t zi = st.S0 + (1023 - (kz - kzu * KEYMUL)) + ch;
             const int32_t off = abs((zi - st.arg_i) - ((d - zi) - st.arg_j));
