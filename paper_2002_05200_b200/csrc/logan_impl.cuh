@@ -234,14 +234,6 @@ static cudaError_t launch_first(int w0, bool helpers, const Params &P, const Lev
 #ifdef LOGAN_L0_R
     w0 = LOGAN_L0_R;
 #endif
-    if constexpr (fmt_base(FMT) == FMT_U8S) {  // substitution matrices: no in-kernel helpers
-        switch (w0) {
-            case 20: return launch_win<1, 20, FMT, 0, 0>(P, io, hio, sms, s);
-            case 24: return launch_win<1, 24, FMT, 0, 0>(P, io, hio, sms, s);
-            case 28: return launch_win<1, 28, FMT, 0, 0>(P, io, hio, sms, s);
-            default: return launch_win<1, 32, FMT, 0, 0>(P, io, hio, sms, s);
-        }
-    }
     switch (w0) {
         case 20: return helpers ? launch_win<1, 20, FMT, LOGAN_HSHAPE(64)>(P, io, hio, sms, s)
                                 : launch_win<1, 20, FMT, 0, 0>(P, io, hio, sms, s);
@@ -258,7 +250,7 @@ template <int FMT>
 static cudaError_t launch_width(int wi, bool latency, bool helpers, const Params &P, const LevelIO &io,
                                 const LevelIO &hio, int sms, cudaStream_t s, int w0, int w5) {
     if (wi == 0 && !(latency && w0 == 32)) return launch_first<FMT>(w0, helpers && !latency, P, io, hio, sms, s);
-    constexpr bool HELP = fmt_base(FMT) != FMT_U8S;
+    constexpr bool HELP = true;
     if (HELP && helpers && !latency) {
         if constexpr (HELP) switch (wi) {
             case 1: return launch_win<2, 32, FMT, LOGAN_HSHAPE(128)>(P, io, hio, sms, s);

@@ -707,7 +707,7 @@ __device__ __forceinline__ void run_group(Win &w, const Params &P, const LevelIO
 // forming a serial tail after it. What the helpers do not take, the next
 // level's own launch does (it shares their cursor).
 template <int G, int R, int FMT, int HG, int HR>
-__global__ void __launch_bounds__(128, (G == 1 ? (fmt_z(FMT) ? 3 : LOGAN_L0_MINB) : 1))
+__global__ void __launch_bounds__(128, (G == 1 ? ((fmt_z(FMT) || fmt_base(FMT) == FMT_U8S) ? 3 : LOGAN_L0_MINB) : 1))
     k_window(const Params P, const LevelIO io, const LevelIO hio) {
     const uint32_t count = *io.count;
     const uint32_t taken = *io.cursor;  // entries already taken (by in-kernel helpers)
