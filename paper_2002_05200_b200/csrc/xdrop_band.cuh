@@ -439,15 +439,12 @@ struct BandCta {
             if (lane == 0) red(PAR)[warp] = make_int4(K, (int32_t)FC, LC, 0);
         }
         __syncthreads();
-        int32_t K = INT32_MIN, LC = -1;
-        uint32_t FC = 0xffffffffu;
-#pragma unroll
-        for (int w = 0; w < BAND_NW; ++w) {
-            const int4 r = red(PAR)[w];
-            K = max(K, r.x);
-            FC = min(FC, (uint32_t)r.y);
-            LC = max(LC, r.z);
-        }
+        // fold the NW partials: lane w reads warp w's (one LDS), CREDUX combines
+        int4 r = make_int4(INT32_MIN, -1, -1, 0);
+        if (lane < BAND_NW) r = red(PAR)[lane];
+        const int32_t K = __reduce_max_sync(0xffffffffu, r.x);
+        const uint32_t FC = __reduce_min_sync(0xffffffffu, (uint32_t)r.y);
+        const int32_t LC = __reduce_max_sync(0xffffffffu, r.z);
         const bool h = LC >= 0;
 
         // (6) best after the complete antidiagonal, strict increase;
