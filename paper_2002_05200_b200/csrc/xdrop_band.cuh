@@ -67,6 +67,7 @@ constexpr uint32_t D16X2 = 0xC000C000u;       // two dead slots (-16384 each)
 #endif
 constexpr int BAND_NT = LOGAN_BAND_NT;        // threads per task (= per block)
 constexpr int BAND_NW = BAND_NT / 32;
+constexpr int BAND_ARG_WARP = BAND_NW > 1 ? 1 : 0;  // the warp that keeps the argmax
 
 template <int FMT> struct BandFmt;
 template <> struct BandFmt<LOGAN_SEQ_2BIT> { static constexpr int CB = 4; };  // one nibble per base
@@ -455,7 +456,7 @@ struct BandCta {
             const int32_t V = M + Tc;
             if (V > t.best) {
                 t.best = V;
-                if (warp == 0) {
+                if (warp == BAND_ARG_WARP) {  // (warp 0 has the exact extents and the cell count)
                     const int32_t c = hbase + 8 * (1023 - (K & 1023));
                     const uint4 w = *(const uint4 *)(cur + ((c >> 1) & (BAND_WORDS - 1)));
                     const uint32_t W4[4] = {w.x, w.y, w.z, w.w};
@@ -506,6 +507,7 @@ struct BandCta {
 template <int FMT>
 __global__ void __launch_bounds__(BAND_NT) k_band(const Params P, const LevelIO io) {
     __shared__ uint32_t s_pos;
+    __shared__ int32_t s_arg[2];  // the argmax warp's result, for the writer (thread 0)
     BandCta<FMT> c;
     c.tid = threadIdx.x;
     c.lane = threadIdx.x & 31;
@@ -529,12 +531,14 @@ __global__ void __launch_bounds__(BAND_NT) k_band(const Params P, const LevelIO 
                 rc = (c.t.d & 1) ? c.template step<0>(P) : c.template step<1>(P);
             } while (rc == 0);
         }
+        if (c.tid == 32 * BAND_ARG_WARP) { s_arg[0] = c.t.arg_i; s_arg[1] = c.t.arg_j; }
+        __syncthreads();
         if (c.tid == 0) {
             if (rc == 1) {
                 TaskRes tr;
                 tr.best = c.t.best;
-                tr.i = c.t.arg_i;
-                tr.j = c.t.arg_j;
+                tr.i = s_arg[0];
+                tr.j = s_arg[1];
                 tr.flags = 0;
                 tr.cells = c.t.cells;
                 io.tres[task] = tr;
