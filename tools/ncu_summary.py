@@ -18,6 +18,9 @@ KEYS = [
     ("smsp__warps_eligible.avg.per_cycle_active", "eligible warps / SMSP"),
     ("launch__registers_per_thread", "registers / thread"),
     ("launch__occupancy_limit_registers", "blocks / SM (reg limit)"),
+    ("l1tex__data_pipe_lsu_wavefronts_mem_shared.sum.pct_of_peak_sustained_elapsed", "shared-memory wavefronts % of peak"),
+    ("memory_l1_wavefronts_shared", "shared wavefronts"),
+    ("memory_l1_wavefronts_shared_ideal", "shared wavefronts (ideal, no bank conflicts)"),
     ("smsp__inst_executed.sum", "warp instructions"),
     ("smsp__thread_inst_executed_per_inst_executed.ratio", "active lanes / instruction"),
     ("dram__bytes_read.sum", "DRAM read"),
