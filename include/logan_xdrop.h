@@ -98,7 +98,7 @@ enum {
  *                  code buffers with garbage before each task, so the tests
  *                  see the worst case of stale shared memory. Results never
  *                  depend on it.
- *  first_slots   : 0 = automatic; 20, 24, 28 or 32 force the width of the
+ *  first_slots   : 0 = automatic; 16, 20, 24, 28 or 32 force the width of the
  *                  first window (one lane per task) when the first level is
  *                  level 1. Results never depend on it.
  *  handover      : test knob, 0 = off. If > 0, every task at a register
@@ -249,7 +249,7 @@ int logan_abi_version(void);
 /* Diagnostics (host only, no GPU needed): the diagonal-slot width of the
  * register window that level `level` (1..6) would run in a call with this
  * xdrop, max_ext_len (as for logan_workspace_bytes) and options.first_slots
- * (0 = automatic): level 1 is 20, 24, 28 or 32 slots, levels 2..5 are 64,
+ * (0 = automatic): level 1 is 16, 20, 24, 28 or 32 slots, levels 2..5 are 64,
  * 128, 256 and 512, level 6 is 640, 768, 896 or 1024. Returns 0 for levels
  * that are not register windows (7 = band level, 8 = CTA level) or out of
  * range. Results never depend on the widths; bench.py uses this to name the

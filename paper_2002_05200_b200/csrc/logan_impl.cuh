@@ -235,6 +235,8 @@ static cudaError_t launch_first(int w0, bool helpers, const Params &P, const Lev
     w0 = LOGAN_L0_R;
 #endif
     switch (w0) {
+        case 16: return helpers ? launch_win<1, 16, FMT, LOGAN_HSHAPE(64)>(P, io, hio, sms, s)
+                                : launch_win<1, 16, FMT, 0, 0>(P, io, hio, sms, s);
         case 20: return helpers ? launch_win<1, 20, FMT, LOGAN_HSHAPE(64)>(P, io, hio, sms, s)
                                 : launch_win<1, 20, FMT, 0, 0>(P, io, hio, sms, s);
         case 24: return helpers ? launch_win<1, 24, FMT, LOGAN_HSHAPE(64)>(P, io, hio, sms, s)
@@ -311,8 +313,12 @@ static int auto_top_width(int32_t xdrop) {
 
 // Slots of the first window: the band of true pairs is about X + 8 slots wide at
 // its widest, and long reads drift more between re-centrings.
+// Measured on C6 / C3 (profiles/r01_ab_first_slots_small_x.txt): X = 5: 16 slots
+// 617 GCUPS vs 20: 555; X = 8: 20 754 vs 16: 614 (2% of tasks overflow); X = 10:
+// 20 ~ 24 on 2.5-7.5 kb reads, 24 +10% on 10 kb reads; X = 12: 24 881 vs 20: 730.
 static int auto_first_slots(int32_t xdrop, int64_t max_ext) {
-    if (xdrop <= 12) return 20;
+    if (xdrop <= 5) return 16;
+    if (xdrop <= 10) return max_ext > 9000 ? 24 : 20;
     if (xdrop <= 16) return 24;
     if (xdrop <= 20) return max_ext > 6000 ? 32 : 28;
     return 32;

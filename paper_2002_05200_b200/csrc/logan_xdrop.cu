@@ -70,7 +70,7 @@ static int check_args(const uint8_t *seq_pool, int32_t seq_fmt, int64_t pool_len
     if (sc.gap >= 0 || sc.gap < -127 || sc.xdrop < 0 || sc.xdrop > (1 << 19)) return LOGAN_EINVAL;
     if (opt && (opt->flags & 4) && (opt->zdrop < 0 || opt->zdrop > (1 << 19))) return LOGAN_EINVAL;
     if (opt && (opt->first_level < 0 || opt->first_level > NLEVEL)) return LOGAN_EINVAL;
-    if (opt && opt->first_slots != 0 && opt->first_slots != 20 && opt->first_slots != 24 &&
+    if (opt && opt->first_slots != 0 && opt->first_slots != 16 && opt->first_slots != 20 && opt->first_slots != 24 &&
         opt->first_slots != 28 && opt->first_slots != 32)
         return LOGAN_EINVAL;
     if (n_pairs == 0) return LOGAN_OK;

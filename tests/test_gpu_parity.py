@@ -366,7 +366,7 @@ def test_cta_level_extension_equal_to_workspace_bound():
         assert_same(*got, *ref, what=f"bound level={lvl}")
 
 
-@pytest.mark.parametrize("slots", [20, 24, 28, 32])
+@pytest.mark.parametrize("slots", [16, 20, 24, 28, 32])
 def test_first_window_widths(slots):
     """Every compiled first-window width (one lane per task) is exact, including
     the overflow hand-over to the next level."""
