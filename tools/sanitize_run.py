@@ -36,3 +36,9 @@ for lvl, z in ((None, 20), (2, 0), (8, 10)):
     out, cells = logan.xdrop_batch(db, 1, -1, -1, 50, first_level=lvl, zdrop=z)
     torch.cuda.synchronize()
     print("zdrop", lvl, z, int(cells.sum()), flush=True)
+# first-window widths (one lane per task), with the overflow hand-over to level 2
+for fs in (16, 20):
+    for X in (5, 50):
+        out, cells = logan.xdrop_batch(db, 1, -1, -1, X, first_level=1, first_slots=fs)
+        torch.cuda.synchronize()
+        print("slots", fs, X, int(cells.sum()), flush=True)
