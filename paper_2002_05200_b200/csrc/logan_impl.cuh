@@ -315,12 +315,14 @@ static int auto_top_width(int32_t xdrop) {
 // its widest, and long reads drift more between re-centrings.
 // Measured on C6 / C3 (profiles/r01_ab_first_slots_small_x.txt): X = 5: 16 slots
 // 617 GCUPS vs 20: 555; X = 8: 20 754 vs 16: 614 (2% of tasks overflow); X = 10:
-// 20 ~ 24 on 2.5-7.5 kb reads, 24 +10% on 10 kb reads; X = 12: 24 881 vs 20: 730.
+// 20 ~ 24 on 2.5-7.5 kb reads, 24 +10% on 10 kb reads; X = 12: 24 881 vs 20: 730;
+// X = 14, 16: 24 best; X = 18, 20: 28 best on 2.5-7.5 kb reads (C6 X = 20: 1168 vs
+// 32: 1109), 32 on 10 kb reads (profiles/r01_ab_first_slots_mid_x.txt).
 static int auto_first_slots(int32_t xdrop, int64_t max_ext) {
     if (xdrop <= 5) return 16;
     if (xdrop <= 10) return max_ext > 9000 ? 24 : 20;
     if (xdrop <= 16) return 24;
-    if (xdrop <= 20) return max_ext > 6000 ? 32 : 28;
+    if (xdrop <= 20) return max_ext > 9000 ? 32 : 28;
     return 32;
 }
 

@@ -55,7 +55,8 @@ def test_library_is_sm100a(lib):
 def test_host_side_checks_without_gpu(lib):
     assert lib.logan_abi_version() == 1
     # window widths by level (diagnostics; results never depend on them)
-    assert lib.logan_level_width(1, 20, 2500, 0) == 28 and lib.logan_level_width(1, 20, 9000, 0) == 32
+    assert lib.logan_level_width(1, 20, 2500, 0) == 28 and lib.logan_level_width(1, 20, 10000, 0) == 32
+    assert lib.logan_level_width(1, 20, 7700, 0) == 28 and lib.logan_level_width(1, 18, 7700, 0) == 28
     assert lib.logan_level_width(1, 10, 2500, 0) == 20 and lib.logan_level_width(1, 20, 2500, 24) == 24
     assert [lib.logan_level_width(1, x, 2500, 0) for x in (0, 5, 6, 10, 11, 12, 16)] == [16, 16, 20, 20, 24, 24, 24]
     assert lib.logan_level_width(1, 10, 10000, 0) == 24 and lib.logan_level_width(1, 20, 2500, 16) == 16
