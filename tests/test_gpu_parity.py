@@ -174,6 +174,24 @@ def test_config2_full_size_sampled():
     assert (got[1] > 0).all()
 
 
+@pytest.mark.parametrize("X", [5, 12, 18])
+def test_config2_small_x_auto_widths_sampled(X):
+    """Full C2 batch at the X values whose automatic first window is 16, 24 and
+    28 slots, in the throughput shape with in-kernel helpers:
+    every 100th pair against the oracle, and every pair equal to a run with
+    the 32-slot first window (results never depend on the width)."""
+    w = datagen.CONFIGS[2]
+    b = datagen.generate(w)
+    got = gpu_run(b, X)
+    idx = np.arange(0, b.n_pairs, 100)
+    ref = oracle_run(b, X, idx=idx)
+    assert_same(got[0][idx], got[1][idx], *ref, what=f"C2 X={X} sample")
+    db = logan.to_device(b, logan.LOGAN_SEQ_2BIT)
+    out, cells = logan.xdrop_batch(db, 1, -1, -1, X, first_slots=32)
+    torch.cuda.synchronize()
+    assert (out.cpu().numpy() == got[0]).all() and (cells.cpu().numpy().view(np.uint64) == got[1]).all()
+
+
 @pytest.mark.parametrize("X", [10, 20, 50, 100])
 def test_config3_x_sweep_sampled(X):
     w = datagen.CONFIGS[3]
