@@ -94,6 +94,8 @@ enum {
  *  flags         : bit 0 = run the first level in its latency shape (one
  *                  warp per task) instead of its throughput shape.
  *                  bit 2 = Z-drop on, threshold `zdrop` (0 <= zdrop <= 2^19).
+ *                  bit 3 = run the first level in its throughput shape even
+ *                  when the batch has few tasks (test / tuning knob; bit 0 wins).
  *                  bit 1 = test knob: the band level fills its shared-memory
  *                  code buffers with garbage before each task, so the tests
  *                  see the worst case of stale shared memory. Results never

@@ -415,10 +415,12 @@ int run_batch(const Params &P, const logan_options_t *opt, logan_result_t *out, 
     // Few tasks (e.g. long reads spread over many GPUs): the throughput shape
     // would leave SMs with too few warps to hide the per-antidiagonal latency,
     // so the first level runs one warp per task instead (measured on C5 with
-    // 2,500 pairs: 260 vs 158 GCUPS).
+    // 2,500 pairs: 260 vs 158 GCUPS at 4.2 throughput-shape warps per SM; C3 at
+    // X = 50 with 12,500 pairs, 10.6 warps per SM, prefers the throughput shape:
+    // 487 vs 300 GCUPS, profiles/r01_ab_few_tasks.txt).
     const int64_t groups_needed = L.ntask * (first < NWIDTH ? width_of(first) / 32 : 1) / 32;  // warps
-    const bool few_tasks = first > 0 && first < NWIDTH && groups_needed < (int64_t)sms * 16;
-    const bool latency_first = (opt && (opt->flags & 1)) || few_tasks;
+    const bool few_tasks = first > 0 && first < NWIDTH && groups_needed < (int64_t)sms * 8;
+    const bool latency_first = (opt && (opt->flags & 1)) || (few_tasks && !(opt && (opt->flags & 8)));
     for (int lv = first; lv < NLEVEL; ++lv) {
         // substitution matrices have no band level: tasks that outgrow the widest
         // window go straight on to the CTA level (which restarts them)
