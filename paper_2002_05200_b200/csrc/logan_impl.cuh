@@ -419,7 +419,12 @@ int run_batch(const Params &P, const logan_options_t *opt, logan_result_t *out, 
     // X = 50 with 12,500 pairs, 10.6 warps per SM, prefers the throughput shape:
     // 487 vs 300 GCUPS, profiles/r01_ab_few_tasks.txt).
     const int64_t groups_needed = L.ntask * (first < NWIDTH ? width_of(first) / 32 : 1) / 32;  // warps
-    const bool few_tasks = first > 0 && first < NWIDTH && groups_needed < (int64_t)sms * 8;
+    // Level 1 (one lane per task) keeps its throughput shape down to 2 warps per SM;
+    // its latency shape exists for the 32-slot window only (C3, X = 20: 3,000 pairs,
+    // 1.3 warps/SM: 128 vs 95 GCUPS for latency; 6,250 pairs: 171 vs 121 for
+    // throughput; profiles/r01_ab_l1_latency.txt).
+    const bool few_tasks = (first > 0 && first < NWIDTH && groups_needed < (int64_t)sms * 8) ||
+                           (first == 0 && w0 == 32 && groups_needed < (int64_t)sms * 2);
     const bool latency_first = (opt && (opt->flags & 1)) || (few_tasks && !(opt && (opt->flags & 8)));
     for (int lv = first; lv < NLEVEL; ++lv) {
         // substitution matrices have no band level: tasks that outgrow the widest
