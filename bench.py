@@ -2,23 +2,34 @@
 """Benchmark of the B200 X-drop hot path (LOGAN, arXiv 2002.05200).
 
     python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+                    [--config C] [--xdrop X] [--share r/N]
 
 One step = one pass of the whole hot path (task expansion + LPT bucketing +
 all sweep levels + combine) over one batch of synthetic pairs already resident
-in HBM.  Default workload: BASELINE.json configs[1] = 100K pairs of 2.5 kb
-reads, 15% error, k = 17, X = 20, +1/-1/-1 (``datagen.CONFIGS[2]``); under
-torchrun every rank processes its own 100K pairs (weak scaling, no data-path
-collective; results are gathered once after the timed region).
+in HBM.  Default workload: BASELINE.json configs[2] = 100K pairs of 10 kb reads,
+15% error, k = 17, X = 20, +1/-1/-1 (``datagen.CONFIGS[3]``), the config the
+metric is quoted on "at 1/2/4/8 B200"; ``--config 2`` is configs[1] (2.5 kb).
+
+Multi-GPU (torchrun, N ranks): the config's ONE batch is split across the
+ranks by a static cell-count-balanced LPT partition (paper P:223-225,
+``multi.partition_lpt`` over ``multi.pair_costs``) -- strong scaling, no
+collective on the data path; after the timed region the per-pair results are
+gathered once to rank 0 and compared with a 1-GPU run of the whole batch.
+``--share r/N`` runs rank r's share of an N-way split on one GPU (per-share
+times project the N-GPU makespan without an N-GPU box).
 
 Metric: GCUPS = band cells (the oracle's definition, c-amb-14) / device time,
-aggregated over all ranks with the max-over-ranks time.  Prints ONE JSON line
-on rank 0.  DESIGN.md §7 documents every key.
+aggregated over all ranks with the max-over-ranks time.  The timed output is
+checked element by element against the oracle on a sample ("parity"); any
+mismatch exits non-zero.  Prints ONE JSON line on rank 0.
+documents every key.
 """
 from __future__ import annotations
 
 import argparse
 import json
 import os
+import platform
 import statistics
 import subprocess
 import sys
@@ -30,21 +41,23 @@ if ROOT not in sys.path:
 
 METRIC = "GCUPS (computed cells/s, device-timed) at 1/2/4/8 B200 vs int roofline"
 UNIT = "GCUPS"
-N_REF_OPS_PER_CELL = 6       # DESIGN.md §7: algorithmic int32 ops per cell (SURVEY §8d convention)
-ALU_LANES_PER_SM_CLK = 64    # 4 SMSPs x 16 int32 ALU lanes (B300_MICROARCH: alu pipe rt_SMSP = 2)
+N_REF_OPS_PER_CELL = 6       # DESIGN.md §6.2: algorithmic int32 ops per cell (SURVEY §8d convention)
 B200_SMS = 148
+DEFAULT_CONFIG = 3
+PEAK_FILE = os.path.join(ROOT, "profiles", "int_peak.json")      # tools/int_peak.py (microbenchmark)
+NCU_FILE = os.path.join(ROOT, "profiles", "ncu_metrics.json")    # tools/ncu_metrics.py (ncu --set full)
 
 
-def parse_args():
+def parse_args(argv=None):
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=30)
+    ap.add_argument("--steps", type=int, default=20)
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
-    ap.add_argument("--config", type=int, default=2,
+    ap.add_argument("--config", type=int, default=DEFAULT_CONFIG,
                     help="datagen.CONFIGS key (BASELINE configs[c-1]); 7 = protein-like pairs scored with a "
                          "substitution matrix (SURVEY §8f row 4)")
-    ap.add_argument("--pairs", type=int, default=None, help="pairs per GPU (default: the config's)")
+    ap.add_argument("--pairs", type=int, default=None, help="pairs of the whole batch (default: the config's)")
     ap.add_argument("--xdrop", type=int, default=None)
     ap.add_argument("--zdrop", type=int, default=None,
                     help="also stop extensions by Z-drop with this Z (DESIGN.md c-amb-19; off by default)")
@@ -52,14 +65,19 @@ def parse_args():
     ap.add_argument("--first-level", type=int, default=0)
     ap.add_argument("--latency-first", action="store_true",
                     help="run the first level in its latency shape (one warp per task)")
+    ap.add_argument("--share", default=None,
+                    help="r/N: run only rank r's share of an N-way split of the batch, on one GPU")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-verify", action="store_true", help="N > 1: skip the gathered-vs-1-GPU check")
     ap.add_argument("--cpu-seconds", type=float, default=12.0,
                     help="target host seconds of the oracle sample (cpu_baseline)")
+    ap.add_argument("--parity-seconds", type=float, default=4.0,
+                    help="target host seconds of the oracle parity sample when cpu_baseline does not run")
     ap.add_argument("--ref-step-seconds", type=float, default=2.0,
                     help="target host seconds per step of --impl reference")
     ap.add_argument("--stats", action="store_true", help="print per-level stats to stderr")
-    return ap.parse_args()
+    return ap.parse_args(argv)
 
 
 PROTEIN_CONFIG = 7  # not a BASELINE config: SURVEY §8f row 4 (substitution matrices)
@@ -79,41 +97,60 @@ def workload(args):
     return w, n
 
 
-def make_batch(args, w, n, pair_base=0, u8=False, two_bit=True):
+def shard_of(args, w, n, world, rank):
+    """Global pair indices of rank ``rank``'s share of the n-pair batch (all of
+    it at world 1) and the partition (None at world 1)."""
+    import numpy as np
+    if world == 1:
+        return np.arange(n, dtype=np.int64), None
+    if args.config == PROTEIN_CONFIG:  # no length pass for the numpy protein generator: even ranges
+        bounds = [n * r // world for r in range(world + 1)]
+        parts = [np.arange(bounds[r], bounds[r + 1], dtype=np.int64) for r in range(world)]
+        return parts[rank], parts
     import datagen
+    from paper_2002_05200_b200 import multi
+    ql, tl, qs, ts = datagen.lengths(w, n)
+    parts = multi.partition_lpt(multi.pair_costs(ql, tl, qs, ts, w.k, w.xdrop, w.gap), world)
+    return parts[rank], parts
+
+
+def make_batch(args, w, idx, u8=False):
+    """The pairs ``idx`` (global indices, ascending) of the workload."""
+    import datagen
+    n = len(idx)
     if args.config == PROTEIN_CONFIG:
-        return datagen.protein_pairs(n, pair_base=pair_base, xdrop=w.xdrop, gap=w.gap)
-    return datagen.generate(w, n_pairs=n, pair_base=pair_base, u8=u8, two_bit=two_bit)
+        base = int(idx[0]) if n else 0
+        return datagen.protein_pairs(n, pair_base=base, xdrop=w.xdrop, gap=w.gap)
+    if n and int(idx[-1]) - int(idx[0]) + 1 == n:  # a contiguous range
+        return datagen.generate(w, n_pairs=n, pair_base=int(idx[0]), u8=u8, two_bit=True)
+    return datagen.generate(w, indices=idx, u8=u8, two_bit=True)
 
 
 ZDROP = None  # set from --zdrop in main / run_reference
 
 
 def run_oracle(batch, w, sl, threads):
-    """The oracle on pairs ``sl`` of the batch -> per-pair cells."""
+    """The oracle on pairs ``sl`` of the batch -> (int32[n,5] results, uint64[n] cells)."""
     import oracle
     import datagen
     if ZDROP is not None:
         sub = datagen.protein_matrix() if batch.pool_2bit is None else None
         pool, fmt = (batch.pool_u8, 0) if sub is not None else (batch.pool_2bit, 1)
-        _, cells = oracle.pairs_z(pool, fmt, batch.q_off[sl], batch.q_len[sl], batch.t_off[sl], batch.t_len[sl],
-                                  batch.q_seed[sl], batch.t_seed[sl], w.k, w.match, w.mismatch, w.gap, w.xdrop,
-                                  ZDROP, subst=sub, pool_len=batch.pool_len, n_threads=threads)
-        return cells
+        return oracle.pairs_z(pool, fmt, batch.q_off[sl], batch.q_len[sl], batch.t_off[sl], batch.t_len[sl],
+                              batch.q_seed[sl], batch.t_seed[sl], w.k, w.match, w.mismatch, w.gap, w.xdrop,
+                              ZDROP, subst=sub, pool_len=batch.pool_len, n_threads=threads)
     if batch.pool_2bit is None:  # protein codes: the substitution-matrix oracle
-        _, cells = oracle.pairs_subst(batch.pool_u8, batch.q_off[sl], batch.q_len[sl], batch.t_off[sl],
-                                      batch.t_len[sl], batch.q_seed[sl], batch.t_seed[sl], w.k,
-                                      datagen.protein_matrix(), w.gap, w.xdrop, pool_len=batch.pool_len,
-                                      n_threads=threads)
-        return cells
-    _, cells = oracle.pairs(batch.pool_2bit, 1, batch.q_off[sl], batch.q_len[sl], batch.t_off[sl],
-                            batch.t_len[sl], batch.q_seed[sl], batch.t_seed[sl], w.k, w.match,
-                            w.mismatch, w.gap, w.xdrop, pool_len=batch.pool_len, n_threads=threads)
-    return cells
+        return oracle.pairs_subst(batch.pool_u8, batch.q_off[sl], batch.q_len[sl], batch.t_off[sl],
+                                  batch.t_len[sl], batch.q_seed[sl], batch.t_seed[sl], w.k,
+                                  datagen.protein_matrix(), w.gap, w.xdrop, pool_len=batch.pool_len,
+                                  n_threads=threads)
+    return oracle.pairs(batch.pool_2bit, 1, batch.q_off[sl], batch.q_len[sl], batch.t_off[sl],
+                        batch.t_len[sl], batch.q_seed[sl], batch.t_seed[sl], w.k, w.match,
+                        w.mismatch, w.gap, w.xdrop, pool_len=batch.pool_len, n_threads=threads)
 
 
-def config_dict(w, n, fmt, first_level, world):
-    d = {"workload": w.name, "pairs_per_gpu": n, "total_pairs": n * world,
+def config_dict(w, n, fmt, first_level, world, share=None):
+    d = {"workload": w.name, "total_pairs": n,
          "read_len": (f"{w.tlen_min}-{w.tlen_max} residues" if w.name.startswith("protein") else
                       w.tlen_max if w.mode == 0 else f"{w.len_lo}-{w.len_hi}"),
          "error": w.err, "k": w.k, "X": w.xdrop,
@@ -121,7 +158,12 @@ def config_dict(w, n, fmt, first_level, world):
                      if w.name.startswith("protein") else f"{w.match:+d}/{w.mismatch:+d}/{w.gap:+d}"),
          "fmt": fmt,
          "seed": w.seed, "l2": "flushed between timed steps (256 MiB write)",
-         "parallelism": f"pairs sharded over {world} GPU(s), no data-path collective"}
+         "parallelism": (f"one batch split over {world} GPU(s) by a static cell-count-balanced LPT partition "
+                         "(multi.pair_costs); no data-path collective, one gather after the timed region")}
+    if share is not None:
+        d["share"] = f"{share[0]}/{share[1]}"
+        d["parallelism"] = (f"share {share[0]} of a {share[1]}-way LPT split of the batch, run alone on one GPU "
+                            "(projects the per-GPU time of an N-GPU run)")
     if first_level:
         d["first_level"] = first_level
     if ZDROP is not None:
@@ -177,24 +219,52 @@ class ClockSampler:
 
 
 # --------------------------------------------------------------------------- oracle legs
-def oracle_sample(batch, w, seconds, threads):
-    """Time the oracle as it stands on a bounded prefix of the batch."""
+def cpu_model() -> str:
+    try:
+        out = subprocess.run(["lscpu"], capture_output=True, text=True, timeout=10).stdout
+        for line in out.splitlines():
+            if line.startswith("Model name:"):
+                return line.split(":", 1)[1].strip()
+    except (OSError, subprocess.TimeoutExpired):
+        pass
+    return platform.processor() or "unknown"
+
+
+def oracle_sample(batch, w, seconds, threads, idx_pool=None):
+    """Time the oracle as it stands on a bounded sample of the batch: pairs
+    ``idx_pool[:k]`` (default: the batch order), k grown to about ``seconds``."""
     import numpy as np
     import oracle
     oracle.build()
+    if idx_pool is None:
+        idx_pool = np.arange(batch.n_pairs)
 
     def run(k):
-        sl = slice(0, k)
+        sl = idx_pool[:k]
         t0 = time.perf_counter()
-        cells = run_oracle(batch, w, sl, threads)
-        return time.perf_counter() - t0, int(np.asarray(cells, dtype=np.uint64).sum())
+        o, c = run_oracle(batch, w, sl, threads)
+        return time.perf_counter() - t0, o, c
 
-    k = min(batch.n_pairs, max(threads * 4, 64))
-    dt, cells = run(k)
-    if dt < seconds * 0.5 and k < batch.n_pairs:
-        k = min(batch.n_pairs, max(k + 1, int(k * seconds / max(dt, 1e-3))))
-        dt, cells = run(k)
-    return {"pairs": k, "seconds": dt, "cells": cells}
+    k = min(len(idx_pool), max(threads * 4, 64))
+    dt, o, c = run(k)
+    if dt < seconds * 0.5 and k < len(idx_pool):
+        k = min(len(idx_pool), max(k + 1, int(k * seconds / max(dt, 1e-3))))
+        dt, o, c = run(k)
+    return {"idx": idx_pool[:k], "seconds": dt, "out": o, "cells": c,
+            "cell_sum": int(np.asarray(c, dtype=np.uint64).sum())}
+
+
+def single_thread_c1():
+    """The oracle on BASELINE configs[0] (C1, 1,000 pairs) on ONE host thread."""
+    import datagen
+    import numpy as np
+    w = datagen.CONFIGS[1]
+    b = datagen.generate(w, u8=False)
+    t0 = time.perf_counter()
+    _, c = run_oracle(b, w, slice(0, b.n_pairs), 1)
+    dt = time.perf_counter() - t0
+    return {"value": int(np.asarray(c, np.uint64).sum()) / dt / 1e9, "unit": UNIT,
+            "workload": f"{w.name} ({b.n_pairs} pairs, 1 thread, {dt:.2f} s)"}
 
 
 def run_reference(args):
@@ -204,18 +274,17 @@ def run_reference(args):
     rank = int(os.environ.get("RANK", "0"))
     if rank != 0:
         return 0
-    import datagen
+    import numpy as np
     w, n = workload(args)
     threads = len(os.sched_getaffinity(0))
-    probe = make_batch(args, w, min(n, max(threads * 1024, 4096)))
+    probe = make_batch(args, w, np.arange(min(n, max(threads * 1024, 4096))))
     cal = oracle_sample(probe, w, args.ref_step_seconds, threads)
-    per_step = cal["pairs"]
-    batch = make_batch(args, w, min(n, per_step))
+    per_step = len(cal["idx"])
+    batch = make_batch(args, w, np.arange(min(n, per_step)))
     times, cells = [], 0
     for s in range(args.warmup + args.steps):
-        import numpy as np
         t0 = time.perf_counter()
-        c = run_oracle(batch, w, slice(0, batch.n_pairs), threads)
+        _, c = run_oracle(batch, w, slice(0, batch.n_pairs), threads)
         dt = time.perf_counter() - t0
         if s >= args.warmup:
             times.append(dt)
@@ -223,23 +292,51 @@ def run_reference(args):
     total = sum(times)
     value = cells * len(times) / total / 1e9
     sample = (f"first {batch.n_pairs} of the {n} pairs of {w.name} per step "
-              f"({cells} cells/step), oracle_pairs on {threads} host threads")
+              f"({cells} cells/step), oracle_pairs on {threads} host threads ({cpu_model()})")
     line = {"impl": "reference", "metric": METRIC, "value": value, "unit": UNIT,
             "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
-            "ms_per_step": 1e3 * total / len(times), "higher_is_better": True, "scaling": "weak",
+            "ms_per_step": 1e3 * total / len(times), "higher_is_better": True, "scaling": "strong",
             "vs_baseline": None, "dtype": "int64", "data": "synthetic",
             "config": config_dict(w, n, "u8" if args.config == PROTEIN_CONFIG else "2bit", 0, 1),
             "cpu_baseline": {"value": value, "unit": UNIT, "cores": threads, "kind": "oracle",
-                             "sample": sample},
+                             "sample": sample, "cpu_model": cpu_model()},
             "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
     return 0
 
 
+# --------------------------------------------------------------------------- roofline inputs
+def int_peak(sm_max_mhz):
+    """Peak int32 ALU-pipe ops/s of the B200: the measured per-SM per-clock
+    throughput of the cell's ALU-pipe instructions (tools/int_peak.py,
+    profiles/int_peak.json) x 148 SMs x the max SM clock; without the file, the
+    guide's ALU pipe rate (16 lanes per SMSP, 64 per SM)."""
+    try:
+        pk = json.load(open(PEAK_FILE))
+        lanes = float(pk["alu_int32_ops_per_clk_per_sm"])
+        how = (f"{B200_SMS} SMs x {lanes:.1f} int32 ALU ops/clk/SM (measured: {pk.get('source', PEAK_FILE)}) "
+               f"x {sm_max_mhz:.0f} MHz")
+        extra = {k: pk[k] for k in ("s16x2_ops_per_clk_per_sm", "issue_inst_per_clk_per_sm") if k in pk}
+    except (OSError, ValueError, KeyError):
+        lanes = 64.0
+        how = f"{B200_SMS} SMs x 64 int32 lanes/clk (derived: 4 SMSPs x 16-lane ALU pipe) x {sm_max_mhz:.0f} MHz"
+        extra = {}
+    return B200_SMS * lanes * sm_max_mhz * 1e6 / 1e12, how, extra
+
+
+def ncu_evidence(key):
+    """Per-launch ncu counters of the dominant kernel for this workload (committed
+    under profiles/ by tools/ncu_metrics.py from an `ncu --set full` capture)."""
+    try:
+        return json.load(open(NCU_FILE)).get(key)
+    except (OSError, ValueError):
+        return None
+
+
 # --------------------------------------------------------------------------- our arm
-def main():
+def main(argv=None):
     global ZDROP
-    args = parse_args()
+    args = parse_args(argv)
     if args.impl == "reference":
         return run_reference(args)
     ZDROP = args.zdrop
@@ -262,18 +359,29 @@ def main():
     dev = torch.device("cuda", local)
     if world > 1:
         dist.init_process_group("nccl", device_id=dev)
+    share = None
+    if args.share:
+        if world > 1:
+            raise SystemExit("--share runs one share on one GPU (no torchrun)")
+        r, nsh = (int(x) for x in args.share.split("/"))
+        share = (r, nsh)
 
     w, n = workload(args)
     protein = args.config == PROTEIN_CONFIG
     if protein:
         args.fmt = "u8"
     fmt = logan.LOGAN_SEQ_2BIT if args.fmt == "2bit" else logan.LOGAN_SEQ_U8
-    batch = make_batch(args, w, n, pair_base=rank * n, u8=(args.fmt == "u8"), two_bit=True)
+    if share is not None:
+        idx, parts = shard_of(args, w, n, share[1], share[0])
+    else:
+        idx, parts = shard_of(args, w, n, world, rank)
+    batch = make_batch(args, w, idx, u8=(args.fmt == "u8"))
+    n_local = batch.n_pairs
     subst = torch.as_tensor(datagen.protein_matrix()).to(dev) if protein else None
     db = logan.to_device(batch, fmt, device=dev)
-    ws = logan.make_workspace(n, db.max_ext_len, dev)
-    out = torch.empty((n, 5), dtype=torch.int32, device=dev)
-    cells = torch.empty(n, dtype=torch.int64, device=dev)
+    ws = logan.make_workspace(n_local, db.max_ext_len, dev)
+    out = torch.empty((n_local, 5), dtype=torch.int32, device=dev)
+    cells = torch.empty(n_local, dtype=torch.int64, device=dev)
     stream = torch.cuda.current_stream(dev)
     first = args.first_level or None
 
@@ -344,18 +452,8 @@ def main():
     total_ms_max = float(t.item())
     cells_all = int(c.item())
     value = cells_all * args.steps / (total_ms_max / 1e3) / 1e9
-
-    # gather of per-pair results to rank 0 (outside the timed steps, reported separately)
-    gather_ms = None
-    if world > 1:
-        g0, g1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        res = torch.cat([out.view(torch.int32), cells.view(torch.int32).view(n, 2)], dim=1).contiguous()
-        allres = torch.empty((world * n, 7), dtype=torch.int32, device=dev)
-        g0.record(stream)
-        dist.all_gather_into_tensor(allres, res)
-        g1.record(stream)
-        torch.cuda.synchronize()
-        gather_ms = g0.elapsed_time(g1)
+    out_h = out.cpu().numpy()
+    cells_h = cells.cpu().numpy().view(np.uint64)
 
     # dominant kernel and its roofline (bound: int32 ALU)
     dom_stage = max((s for s in stage_ms if 1 <= s <= nst - 2), key=lambda s: stage_ms[s])
@@ -363,28 +461,26 @@ def main():
     dom_ms = stage_ms[dom_stage] / args.steps
     dom_cells = stats["cells_per_level"][dom_level]
     sm_max = clocks.get("sm_max_mhz") or 1965.0
-    peak_tops = B200_SMS * ALU_LANES_PER_SM_CLK * sm_max * 1e6 / 1e12
+    peak_tops, peak_how, peak_extra = int_peak(sm_max)
     achieved_tops = N_REF_OPS_PER_CELL * dom_cells / (dom_ms / 1e3) / 1e12
-    traffic = None
-    tfile = os.path.join(ROOT, "profiles", "traffic.json")
-    if os.path.exists(tfile):
-        try:
-            tj = json.load(open(tfile))
-            key = f"{w.name}/{args.fmt}/level{dom_level + 1}"
-            traffic = tj.get(key)
-        except (OSError, ValueError):
-            traffic = None
     # the library picks window widths from X (from ceil(X / |gap|) with a substitution matrix)
     xband = -(-w.xdrop // -w.gap) if subst is not None else w.xdrop
     level_names = [f"window{logan._lib.load().logan_level_width(lv + 1, xband, db.max_ext_len, 0)}"
                    for lv in range(6)] + ["band8192", "wide_cta"]
+    ncu_key = f"{w.name}/{args.fmt}/level{dom_level + 1}"
+    ev_ncu = ncu_evidence(ncu_key)
     roofline = {"bound": "alu", "achieved": achieved_tops, "peak": peak_tops, "unit": "TOP/s",
-                "frac": achieved_tops / peak_tops, "traffic": traffic,
+                "frac": achieved_tops / peak_tops,
+                "traffic": ev_ncu.get("dram_bytes") if ev_ncu else None,
                 "kernel": f"{'k_window' if dom_level < 6 else ('k_band' if dom_level == 6 else 'k_wide')} "
                           f"level {dom_level + 1} ({level_names[dom_level]})",
                 "kernel_ms": dom_ms, "kernel_share_of_step": dom_ms / (total_ms / args.steps),
-                "ops_per_cell": N_REF_OPS_PER_CELL,
-                "peak_derivation": f"{B200_SMS} SMs x {ALU_LANES_PER_SM_CLK} int32 lanes/clk x {sm_max:.0f} MHz"}
+                "ops_per_cell": N_REF_OPS_PER_CELL, "cells_per_launch": dom_cells,
+                "peak_derivation": peak_how, **peak_extra}
+    if ev_ncu:
+        roofline["ncu"] = {k: ev_ncu[k] for k in ("sass_thread_inst_per_cell", "int_thread_inst_per_cell",
+                                                  "int_warp_gips", "alu_pipe_pct", "fma_pipe_pct", "issue_pct",
+                                                  "source") if k in ev_ncu}
 
     # End-to-end through the host-buffer C-ABI entry point, from pinned host memory:
     # every step copies its inputs in (H2D) and its results out (D2H) inside the timed
@@ -396,9 +492,9 @@ def main():
         pin = lambda a: torch.from_numpy(np.ascontiguousarray(a)).pin_memory().numpy()
         hp = [pin(x) for x in (pool_np, batch.q_off, batch.q_len, batch.t_off, batch.t_len,
                                batch.q_seed, batch.t_seed)]
-        hout = [torch.empty((n, 5), dtype=torch.int32).pin_memory().numpy() for _ in range(2)]
-        hcells = [torch.empty(n, dtype=torch.int64).pin_memory().numpy().view(np.uint64) for _ in range(2)]
-        arenas = [logan.HostArena(n, batch.pool_len, fmt, db.max_ext_len, device=dev) for _ in range(2)]
+        hout = [torch.empty((n_local, 5), dtype=torch.int32).pin_memory().numpy() for _ in range(2)]
+        hcells = [torch.empty(n_local, dtype=torch.int64).pin_memory().numpy().view(np.uint64) for _ in range(2)]
+        arenas = [logan.HostArena(n_local, batch.pool_len, fmt, db.max_ext_len, device=dev) for _ in range(2)]
         streams = [torch.cuda.Stream(dev) for _ in range(2)]
         pool_bytes = (batch.pool_len + 3) // 4 if fmt == logan.LOGAN_SEQ_2BIT else batch.pool_len
 
@@ -425,49 +521,106 @@ def main():
             e2e_step(s_)
         ends = []
         for st_ in streams:
-            ev = torch.cuda.Event(enable_timing=True)
-            ev.record(st_)
-            ends.append(ev)
+            evx = torch.cuda.Event(enable_timing=True)
+            evx.record(st_)
+            ends.append(evx)
         torch.cuda.synchronize()
-        e2e_ms = max(a0.elapsed_time(ev) for ev in ends)
+        e2e_ms = max(a0.elapsed_time(evx) for evx in ends)
         te = torch.tensor([e2e_ms], dtype=torch.float64, device=dev)
         if world > 1:
             dist.all_reduce(te, op=dist.ReduceOp.MAX)
-        for hc in hcells:
-            assert int(hc.sum()) == cells_step
+        for k_ in range(2):
+            assert int(hcells[k_].sum()) == cells_step
+            assert (hout[k_] == out_h).all()  # the host entry point gives the device entry point's results
         e2e = {"value": cells_all * ke / (float(te.item()) / 1e3) / 1e9, "unit": UNIT,
-               "h2d_bytes_per_step": int(pool_bytes + 32 * n), "d2h_bytes_per_step": int(28 * n),
+               "h2d_bytes_per_step": int(pool_bytes + 32 * n_local), "d2h_bytes_per_step": int(28 * n_local),
                "steps": ke, "api": "logan_xdrop_batch_host_async (2 arenas / 2 streams, pinned)"}
 
-    # CPU baseline: the oracle on this host's cores, rank 0 at N = 1 only
+    # CPU baseline (rank 0 at N = 1 only) and the parity sample: the oracle on this
+    # host's cores over a bounded sample of this rank's pairs, compared element by
+    # element with the timed run's output
     cpu = None
-    if rank == 0 and world == 1 and not args.no_cpu_baseline:
-        threads = len(os.sched_getaffinity(0))
-        r = oracle_sample(batch, w, args.cpu_seconds, threads)
-        cpu = {"value": r["cells"] / r["seconds"] / 1e9, "unit": UNIT, "cores": threads,
-               "kind": "oracle",
-               "sample": f"first {r['pairs']} of the {n} pairs ({r['cells']} cells) in "
-                         f"{r['seconds']:.1f} s, oracle_pairs on {threads} host threads"}
+    parity = None
+    threads = len(os.sched_getaffinity(0))
+    if rank == 0:
+        rng = np.random.default_rng(2002052000)
+        sample_order = rng.permutation(n_local)  # a uniform sample of the pairs, not a prefix
+        if world == 1 and share is None and not args.no_cpu_baseline:
+            r = oracle_sample(batch, w, args.cpu_seconds, threads, sample_order)
+            cpu = {"value": r["cell_sum"] / r["seconds"] / 1e9, "unit": UNIT, "cores": threads,
+                   "kind": "oracle", "cpu_model": cpu_model(),
+                   "sample": f"{len(r['idx'])} uniformly sampled of the {n_local} pairs ({r['cell_sum']} cells) "
+                             f"in {r['seconds']:.1f} s, oracle_pairs on {threads} host threads",
+                   "single_thread_c1": single_thread_c1()}
+        else:
+            r = oracle_sample(batch, w, args.parity_seconds, threads, sample_order)
+        sel = r["idx"]
+        bad = int(((out_h[sel] != r["out"]).any(axis=1) | (cells_h[sel] != r["cells"])).sum())
+        parity = {"pairs": int(len(sel)), "mismatches": bad, "vs": "oracle",
+                  "outputs": "score, q_begin, q_end, t_begin, t_end, cells (bit-exact)",
+                  "sample": f"uniform sample of {'rank 0' if world > 1 else 'the'} pairs"}
+
+    # N > 1: one gather of the per-pair results to rank 0 (outside the timed region),
+    # then rank 0 runs the whole batch alone and compares (partition independence)
+    gather_ms = None
+    if world > 1:
+        cap = max(len(p) for p in parts)
+        rec = torch.zeros((cap, 8), dtype=torch.int32, device=dev)
+        rec[:n_local, 0:5] = out
+        rec[:n_local, 5:7] = cells.view(torch.int32).view(n_local, 2)
+        allrec = torch.empty((world * cap, 8), dtype=torch.int32, device=dev)
+        g0, g1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        g0.record(stream)
+        dist.all_gather_into_tensor(allrec, rec)
+        g1.record(stream)
+        torch.cuda.synchronize()
+        gather_ms = g0.elapsed_time(g1)
+        if rank == 0 and not args.no_verify:
+            g = allrec.cpu().numpy().reshape(world, cap, 8)
+            full_o = np.zeros((n, 5), np.int32)
+            full_c = np.zeros(n, np.uint64)
+            for r_, p in enumerate(parts):
+                full_o[p] = g[r_, :len(p), 0:5]
+                full_c[p] = np.ascontiguousarray(g[r_, :len(p), 5:7]).view(np.uint64).reshape(-1)
+            whole = make_batch(args, w, np.arange(n, dtype=np.int64), u8=(args.fmt == "u8"))
+            dbw = logan.to_device(whole, fmt, device=dev)
+            o1, c1 = logan.xdrop_batch(dbw, w.match, w.mismatch, w.gap, w.xdrop, subst=subst, zdrop=args.zdrop)
+            torch.cuda.synchronize()
+            o1, c1 = o1.cpu().numpy(), c1.cpu().numpy().view(np.uint64)
+            parity["gathered_vs_1gpu"] = {"pairs": n, "mismatches": int(((full_o != o1).any(axis=1) |
+                                                                          (full_c != c1)).sum())}
+            del dbw
 
     if rank == 0:
         line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
                 "warmup": args.warmup, "ms_per_step": total_ms_max / args.steps,
-                "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "int32",
+                "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "int32",
                 "data": "synthetic (datagen, seeded; DESIGN.md §5)",
-                "config": config_dict(w, n, args.fmt, args.first_level, world),
-                "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e,
+                "config": config_dict(w, n, args.fmt, args.first_level, world, share),
+                "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e, "parity": parity,
                 "gpu_launches": launches_per_step * args.steps, "clocks": clocks,
-                "cells_per_step": cells_all,
+                "cells_per_step": cells_all, "pairs_this_gpu": n_local,
                 "stage_ms_per_step": {str(k): v / args.steps for k, v in stage_ms.items()},
-                "levels": {"tasks_started": stats["tasks_started"],
+                "levels": {"first": [stats["first_level"], stats["first_width"], stats["first_shape"],
+                                     stats["first_helpers"]],
+                           "tasks_started": stats["tasks_started"],
                            "tasks_finished": stats["tasks_finished"],
+                           "helper_tasks": stats["helper_tasks"],
                            "cells_per_level": stats["cells_per_level"],
                            "window_shifts": stats["window_shifts"]}}
         if gather_ms is not None:
             line["gather_ms"] = gather_ms
         print(json.dumps(line), flush=True)
+    ok = parity is None or (parity["mismatches"] == 0 and
+                            parity.get("gathered_vs_1gpu", {"mismatches": 0})["mismatches"] == 0)
     if world > 1:
+        flag = torch.tensor([0 if ok else 1], device=dev)
+        dist.all_reduce(flag, op=dist.ReduceOp.MAX)
+        ok = int(flag.item()) == 0
         dist.destroy_process_group()
+    if not ok:
+        print("bench.py: the timed output differs from the oracle / the 1-GPU run", file=sys.stderr)
+        return 3
     return 0
 
 

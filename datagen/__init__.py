@@ -56,6 +56,11 @@ def _load():
         lib.gen_bases.argtypes = [P(_Cfg), P(ctypes.c_int64), P(ctypes.c_uint8),
                                   P(ctypes.c_uint8), ctypes.c_int]
         lib.gen_bases.restype = ctypes.c_int
+        lib.gen_lengths_idx.argtypes = [P(_Cfg), P(ctypes.c_int64)] + [P(ctypes.c_int32)] * 4 + [ctypes.c_int]
+        lib.gen_lengths_idx.restype = ctypes.c_int
+        lib.gen_bases_idx.argtypes = [P(_Cfg), P(ctypes.c_int64), P(ctypes.c_int64), P(ctypes.c_uint8),
+                                      P(ctypes.c_uint8), ctypes.c_int]
+        lib.gen_bases_idx.restype = ctypes.c_int
         _lib = lib
     return _lib
 
@@ -145,13 +150,15 @@ def _pad16(n: int) -> int:
 
 
 def generate(w: Workload, n_pairs: int | None = None, pair_base: int = 0, u8: bool = True,
-             two_bit: bool = True, n_threads: int | None = None) -> Batch:
-    """Generate pairs ``[pair_base, pair_base + n_pairs)`` of workload ``w``.
+             two_bit: bool = True, n_threads: int | None = None, indices=None) -> Batch:
+    """Generate pairs ``[pair_base, pair_base + n_pairs)`` of workload ``w``, or
+    the global pairs ``indices`` (any order; a shard of a partitioned batch).
 
     The pools are padded with zero bytes to a multiple of 16 bytes + 16 (the
     library reads whole words).
     """
-    n = w.n_pairs if n_pairs is None else int(n_pairs)
+    idx = None if indices is None else np.ascontiguousarray(indices, np.int64)
+    n = (w.n_pairs if n_pairs is None else int(n_pairs)) if idx is None else len(idx)
     if n_threads is None:
         n_threads = len(os.sched_getaffinity(0))
     cfg = _Cfg(w.seed, n, pair_base, w.mode, w.tlen_min, w.tlen_max, w.err, w.k, w.spurious,
@@ -160,10 +167,11 @@ def generate(w: Workload, n_pairs: int | None = None, pair_base: int = 0, u8: bo
     ql = np.zeros(n, np.int32); tl = np.zeros(n, np.int32)
     qs = np.zeros(n, np.int32); ts = np.zeros(n, np.int32)
     lib = _load()
+    ip = idx.ctypes.data_as(P(ctypes.c_int64)) if idx is not None else None
     if n > 0:
-        st = lib.gen_lengths(ctypes.byref(cfg), ql.ctypes.data_as(P(ctypes.c_int32)),
-                             tl.ctypes.data_as(P(ctypes.c_int32)), qs.ctypes.data_as(P(ctypes.c_int32)),
-                             ts.ctypes.data_as(P(ctypes.c_int32)), n_threads)
+        lens = [a.ctypes.data_as(P(ctypes.c_int32)) for a in (ql, tl, qs, ts)]
+        st = (lib.gen_lengths(ctypes.byref(cfg), *lens, n_threads) if idx is None else
+              lib.gen_lengths_idx(ctypes.byref(cfg), ip, *lens, n_threads))
         if st != 0:
             raise RuntimeError("gen_lengths failed")
     region = (ql.astype(np.int64) + tl + 3) // 4 * 4
@@ -174,12 +182,34 @@ def generate(w: Workload, n_pairs: int | None = None, pair_base: int = 0, u8: bo
     pu8 = np.zeros(_pad16(pool_len) + 16, np.uint8) if u8 else None
     p2 = np.zeros(_pad16((pool_len + 3) // 4) + 16, np.uint8) if two_bit else None
     if n > 0 and (u8 or two_bit):
-        st = lib.gen_bases(ctypes.byref(cfg), off.ctypes.data_as(P(ctypes.c_int64)),
-                           pu8.ctypes.data_as(P(ctypes.c_uint8)) if u8 else None,
-                           p2.ctypes.data_as(P(ctypes.c_uint8)) if two_bit else None, n_threads)
+        args = (off.ctypes.data_as(P(ctypes.c_int64)), pu8.ctypes.data_as(P(ctypes.c_uint8)) if u8 else None,
+                p2.ctypes.data_as(P(ctypes.c_uint8)) if two_bit else None, n_threads)
+        st = (lib.gen_bases(ctypes.byref(cfg), *args) if idx is None else
+              lib.gen_bases_idx(ctypes.byref(cfg), ip, *args))
         if st != 0:
             raise RuntimeError("gen_bases failed")
-    return Batch(w, pair_base, off, ql, off + ql, tl, qs, ts, pool_len, pu8, p2)
+    b = Batch(w, pair_base, off, ql, off + ql, tl, qs, ts, pool_len, pu8, p2)
+    if idx is not None:
+        b.meta["indices"] = idx
+    return b
+
+
+def lengths(w: Workload, n_pairs: int | None = None, pair_base: int = 0, n_threads: int | None = None):
+    """(q_len, t_len, q_seed, t_seed) of pairs [pair_base, pair_base + n_pairs)
+    without the pools (pass 1 only: what a partitioner needs)."""
+    n = w.n_pairs if n_pairs is None else int(n_pairs)
+    if n_threads is None:
+        n_threads = len(os.sched_getaffinity(0))
+    cfg = _Cfg(w.seed, n, pair_base, w.mode, w.tlen_min, w.tlen_max, w.err, w.k, w.spurious,
+               w.len_lo, w.len_hi, w.burst)
+    out = [np.zeros(n, np.int32) for _ in range(4)]
+    if n > 0:
+        P = ctypes.POINTER
+        st = _load().gen_lengths(ctypes.byref(cfg), *[a.ctypes.data_as(P(ctypes.c_int32)) for a in out],
+                                 n_threads)
+        if st != 0:
+            raise RuntimeError("gen_lengths failed")
+    return tuple(out)
 
 
 def decode_2bit(pool: np.ndarray, start: int, length: int) -> bytes:

@@ -228,6 +228,7 @@ typedef struct {
     const int64_t *off; /* pass 2: pair region start (bases) */
     uint8_t *u8;        /* may be NULL */
     uint8_t *b2;        /* may be NULL */
+    const int64_t *idx; /* NULL: local pair p is global pair_base + p; else global idx[p] */
     int64_t next;
     pthread_mutex_t mu;
     int pass;
@@ -255,7 +256,7 @@ static void *worker(void *arg) {
         int64_t e = b + 16 < j->cfg->n_pairs ? b + 16 : j->cfg->n_pairs;
         for (int64_t p = b; p < e; ++p) {
             int32_t ql, tl, qs, ts;
-            gen_pair(j->cfg, j->cfg->pair_base + p, &s, &ql, &tl, &qs, &ts);
+            gen_pair(j->cfg, j->idx ? j->idx[p] : j->cfg->pair_base + p, &s, &ql, &tl, &qs, &ts);
             if (j->pass == 1) {
                 j->qlen[p] = ql; j->tlen[p] = tl; j->qs[p] = qs; j->ts[p] = ts;
             } else {
@@ -286,7 +287,15 @@ static int run(job_t *j, int n_threads) {
 /* Pass 1: lengths and seeds. */
 int gen_lengths(const gen_cfg_t *cfg, int32_t *qlen, int32_t *tlen, int32_t *qs, int32_t *ts,
                 int n_threads) {
-    job_t j = {cfg, qlen, tlen, qs, ts, NULL, NULL, NULL, 0, PTHREAD_MUTEX_INITIALIZER, 1, 0};
+    job_t j = {cfg, qlen, tlen, qs, ts, NULL, NULL, NULL, NULL, 0, PTHREAD_MUTEX_INITIALIZER, 1, 0};
+    return run(&j, n_threads);
+}
+
+/* Pass 1 for an arbitrary set of global pair indices idx[0 .. cfg->n_pairs)
+ * (a shard of a partitioned batch; pair_base is ignored). */
+int gen_lengths_idx(const gen_cfg_t *cfg, const int64_t *idx, int32_t *qlen, int32_t *tlen, int32_t *qs,
+                    int32_t *ts, int n_threads) {
+    job_t j = {cfg, qlen, tlen, qs, ts, NULL, NULL, NULL, idx, 0, PTHREAD_MUTEX_INITIALIZER, 1, 0};
     return run(&j, n_threads);
 }
 
@@ -295,6 +304,13 @@ int gen_lengths(const gen_cfg_t *cfg, int32_t *qlen, int32_t *tlen, int32_t *qs,
  * that threads never share a 2-bit byte. u8 / b2 must be zero-initialised
  * (b2 is OR-ed into). */
 int gen_bases(const gen_cfg_t *cfg, const int64_t *off, uint8_t *u8, uint8_t *b2, int n_threads) {
-    job_t j = {cfg, NULL, NULL, NULL, NULL, off, u8, b2, 0, PTHREAD_MUTEX_INITIALIZER, 2, 0};
+    job_t j = {cfg, NULL, NULL, NULL, NULL, off, u8, b2, NULL, 0, PTHREAD_MUTEX_INITIALIZER, 2, 0};
+    return run(&j, n_threads);
+}
+
+/* Pass 2 for global pair indices idx[0 .. cfg->n_pairs) (see gen_lengths_idx). */
+int gen_bases_idx(const gen_cfg_t *cfg, const int64_t *idx, const int64_t *off, uint8_t *u8, uint8_t *b2,
+                  int n_threads) {
+    job_t j = {cfg, NULL, NULL, NULL, NULL, off, u8, b2, idx, 0, PTHREAD_MUTEX_INITIALIZER, 2, 0};
     return run(&j, n_threads);
 }

@@ -37,11 +37,17 @@
 extern "C" {
 #endif
 
-#define LOGAN_ABI_VERSION 1
+#define LOGAN_ABI_VERSION 2
 
 /* Linear scoring scheme (eq. P:85, read with signed addends, c-amb-2).
  * Requirements: 0 < match <= 127, -127 <= mismatch < 0, -127 <= gap < 0,
- * 0 <= xdrop <= 2^19 (X >= (m+n)*127 disables pruning: "X = infinity"). */
+ * 0 <= xdrop <= 2^28. No cell of an extension with m + n bases
+ * can ever drop once X >= 2 (m+n) w, w = max(match, -mismatch, -gap) (127 with
+ * a substitution matrix): |S| <= (m+n) w and best <= (m+n) w, so best - X <= S.
+ * The library therefore runs every call with X' = min(X, 4 max_ext_len w),
+ * which gives results identical to X ("X = infinity" is any X >= that bound);
+ * the register windows hold X' <= 2^19 (their argmax key u * 1027 + slot must
+ * stay below 2^31), larger X' runs on the CTA level (int32 absolute scores). */
 typedef struct {
     int32_t match;
     int32_t mismatch;
@@ -92,8 +98,12 @@ enum {
  *                  LPT bucketing), stages 1..8 = levels 1..8, stage 9 =
  *                  combine. Stages not launched leave their events untouched.
  *  flags         : bit 0 = run the first level in its latency shape (one
- *                  warp per task) instead of its throughput shape.
- *                  bit 2 = Z-drop on, threshold `zdrop` (0 <= zdrop <= 2^19).
+ *                  warp per task) instead of its throughput shape; at level 1
+ *                  this sets the first window to 32 slots (the only width
+ *                  with a latency shape) unless first_slots forces another
+ *                  width, in which case level 1 runs its one-lane shape
+ *                  without in-kernel helpers.
+ *                  bit 2 = Z-drop on, threshold `zdrop` (0 <= zdrop <= 2^28).
  *                  bit 3 = run the first level in its throughput shape even
  *                  when the batch has few tasks (test / tuning knob; bit 0 wins).
  *                  bit 1 = test knob: the band level fills its shared-memory
@@ -112,7 +122,10 @@ enum {
  *                  antidiagonal d, an extension ends if best - M_d > zdrop +
  *                  |gap| * |(i_d - i*) - (j_d - j*)|, M_d the largest live
  *                  score on d at (i_d, j_d) (smallest i), (i*, j*) the argmax
- *                  so far. X-drop pruning still applies. Tasks with Z-drop
+ *                  so far. X-drop pruning still applies. On an antidiagonal
+ *                  with a live cell best - M_d <= X, so a Z >= X' never
+ *                  fires and the library runs such calls without Z-drop
+ *                  (identical results). Tasks with Z-drop
  *                  skip the band level (bands wider than the widest window
  *                  restart on the CTA level).
  *  subst, alphabet : substitution-matrix scoring (the
@@ -149,13 +162,21 @@ typedef struct {
 /* Per-call device-side statistics (optional output in DEVICE memory, may be
  * NULL; filled once the stream syncs): per level, the tasks that started
  * there, the tasks that finished there and their band cells; window shifts
- * summed over all tasks. */
+ * summed over all tasks; the invalid pairs; and which kernel shape the first
+ * level ran (diagnostics: tests assert which instantiation they exercised). */
 typedef struct {
     uint64_t tasks_started[8];   /* entry l-1 = level l (1..8) */
     uint64_t tasks_finished[8];
     uint64_t cells_per_level[8];
     uint64_t window_shifts;
     uint64_t cells_total;
+    uint64_t pairs_invalid;      /* pairs rejected by validation (see logan_xdrop_batch) */
+    uint64_t helper_tasks;       /* tasks the first level's in-kernel helpers took */
+    uint32_t first_level;        /* the level the call started on (1..8) */
+    uint32_t first_width;        /* its register-window width in slots (0 for levels 7, 8) */
+    uint32_t first_shape;        /* 0 = throughput shape (one lane or W/32 lanes per task), 1 = latency
+                                    shape (one warp per task) */
+    uint32_t first_helpers;      /* 1 if the first level ran in-kernel escalation helpers */
 } logan_stats_t;
 
 /* Bytes of device workspace a call with n_pairs pairs needs.
@@ -178,6 +199,12 @@ size_t logan_workspace_bytes(int64_t n_pairs, int64_t max_ext_len);
  *               (reads may be shared between pairs).
  *  q_len,t_len: int32[n_pairs] read lengths (bases), 0 <= len < 2^30.
  *  q_seed,t_seed: int32[n_pairs] seed start inside query / target read.
+ *  max_ext_len: the caller's bound on every extension length (bases) of the
+ *               batch: max over pairs of max(qs, ts, M-qs-k, N-ts-k), or any
+ *               larger value, 0 <= max_ext_len < 2^30. It sizes the workspace
+ *               (see logan_workspace_bytes) and picks the first window width;
+ *               a pair with an extension longer than it is an INVALID pair
+ *               (below), never a silently wrong result.
  *  k          : seed length (>= 0; k = 0 is a point seed).
  *  sc         : scoring and X.
  *  opt        : may be NULL (automatic).
@@ -187,19 +214,23 @@ size_t logan_workspace_bytes(int64_t n_pairs, int64_t max_ext_len);
  *  workspace  : device buffer of >= logan_workspace_bytes(n_pairs, max_ext_len)
  *               bytes, 256-byte aligned. Its contents are scratch.
  *
- * Errors: invalid scalars / NULL required pointers -> LOGAN_EINVAL and a too
- * small workspace -> LOGAN_ENOSPC, both returned synchronously with nothing
- * launched. A pair whose ranges are invalid (q_seed < 0, q_seed + k > q_len,
- * likewise for t, or a read outside [0, pool_len)) gets the invalid result and
- * cells = 0; the rest of the batch is unaffected. A launch failure returns
- * LOGAN_ECUDA. n_pairs = 0 is a no-op returning LOGAN_OK.
+ * Errors: invalid scalars / NULL required pointers -> LOGAN_EINVAL and a
+ * workspace smaller than logan_workspace_bytes(n_pairs, max_ext_len) ->
+ * LOGAN_ENOSPC, both returned synchronously with nothing launched. A pair
+ * whose ranges are invalid (q_seed < 0, q_seed + k > q_len, likewise for t, a
+ * read outside [0, pool_len), or an extension longer than max_ext_len) gets
+ * the invalid result {INT32_MIN, -1, -1, -1, -1} and cells = 0, and is counted
+ * in stats->pairs_invalid; the rest of the batch is unaffected (device-side
+ * validation cannot fail the call synchronously). A valid pair always gets its
+ * exact result. A launch failure returns LOGAN_ECUDA. n_pairs = 0 is a no-op
+ * returning LOGAN_OK.
  * Results are valid once `stream` has been synchronised.
  */
 int logan_xdrop_batch(const uint8_t *seq_pool, int32_t seq_fmt, int64_t pool_len,
                       const int64_t *q_off, const int32_t *q_len,
                       const int64_t *t_off, const int32_t *t_len,
                       const int32_t *q_seed, const int32_t *t_seed,
-                      int64_t n_pairs, int32_t k, logan_scoring_t sc,
+                      int64_t n_pairs, int64_t max_ext_len, int32_t k, logan_scoring_t sc,
                       const logan_options_t *opt,
                       logan_result_t *out, uint64_t *cells, logan_stats_t *stats,
                       void *workspace, size_t workspace_bytes, void *stream);
@@ -211,8 +242,12 @@ int logan_xdrop_batch(const uint8_t *seq_pool, int32_t seq_fmt, int64_t pool_len
  * logan_host_arena_bytes(...) bytes; the call copies the inputs into it
  * (host->device), runs logan_xdrop_batch on `stream`, copies `out` (and
  * `cells` if non-NULL) back (device->host) and synchronises `stream` before
- * returning. Same error behaviour as logan_xdrop_batch; additionally returns
- * LOGAN_ECUDA if a copy or the final synchronisation fails.
+ * returning. The extension bound is computed here from the host descriptors
+ * (over the valid pairs), so no valid pair is ever rejected: an arena sized
+ * for a smaller max_ext_len than the batch needs returns LOGAN_ENOSPC with
+ * nothing launched. Same error behaviour as logan_xdrop_batch otherwise;
+ * additionally returns LOGAN_ECUDA if a copy or the final synchronisation
+ * fails.
  */
 size_t logan_host_arena_bytes(int64_t n_pairs, int64_t pool_len, int32_t seq_fmt,
                               int64_t max_ext_len);

@@ -15,6 +15,7 @@ LIB_PATH = os.path.join(PKG, "liblogan_xdrop.so")
 LOGAN_SEQ_U8 = 0
 LOGAN_SEQ_2BIT = 1
 LOGAN_OK, LOGAN_EINVAL, LOGAN_ECUDA, LOGAN_ENOSPC = 0, 1, 2, 3
+ABI_VERSION = 2  # LOGAN_ABI_VERSION this binding marshals for
 
 #: every symbol include/logan_xdrop.h declares
 EXPORTS = ("logan_workspace_bytes", "logan_xdrop_batch", "logan_host_arena_bytes",
@@ -45,7 +46,10 @@ class Result(ctypes.Structure):
 class Stats(ctypes.Structure):
     _fields_ = [("tasks_started", ctypes.c_uint64 * 8), ("tasks_finished", ctypes.c_uint64 * 8),
                 ("cells_per_level", ctypes.c_uint64 * 8), ("window_shifts", ctypes.c_uint64),
-                ("cells_total", ctypes.c_uint64)]
+                ("cells_total", ctypes.c_uint64), ("pairs_invalid", ctypes.c_uint64),
+                ("helper_tasks", ctypes.c_uint64), ("first_level", ctypes.c_uint32),
+                ("first_width", ctypes.c_uint32), ("first_shape", ctypes.c_uint32),
+                ("first_helpers", ctypes.c_uint32)]
 
 
 class LoganError(RuntimeError):
@@ -70,7 +74,7 @@ def load(path: str | None = None) -> ctypes.CDLL:
     lib.logan_workspace_bytes.restype = sz
     lib.logan_host_arena_bytes.argtypes = [i64, i64, i32, i64]
     lib.logan_host_arena_bytes.restype = sz
-    lib.logan_xdrop_batch.argtypes = [vp, i32, i64, vp, vp, vp, vp, vp, vp, i64, i32, Scoring,
+    lib.logan_xdrop_batch.argtypes = [vp, i32, i64, vp, vp, vp, vp, vp, vp, i64, i64, i32, Scoring,
                                       ctypes.POINTER(Options), vp, vp, vp, vp, sz, vp]
     lib.logan_xdrop_batch.restype = ctypes.c_int
     lib.logan_xdrop_batch_host.argtypes = [vp, i32, i64, vp, vp, vp, vp, vp, vp, i64, i32, Scoring,
@@ -84,6 +88,9 @@ def load(path: str | None = None) -> ctypes.CDLL:
     lib.logan_abi_version.restype = ctypes.c_int
     lib.logan_level_width.argtypes = [i32, i32, i64, i32]
     lib.logan_level_width.restype = ctypes.c_int
+    if lib.logan_abi_version() != ABI_VERSION:
+        raise LoganError(f"{path}: ABI version {lib.logan_abi_version()}, binding expects {ABI_VERSION} "
+                         "(rebuild with `python -m paper_2002_05200_b200.build`)")
     _lib = lib
     return lib
 

@@ -126,24 +126,31 @@ def xdrop_batch(db: DeviceBatch, match: int, mismatch: int, gap: int, xdrop: int
     lib = _lib.load()
     n = db.n_pairs
     dev = db.q_len.device
-    if out is None:
-        out = torch.empty((n, 5), dtype=torch.int32, device=dev)
-    if cells is None:
-        cells = torch.empty(n, dtype=torch.int64, device=dev)
-    if workspace is None or workspace.n_pairs < n or workspace.max_ext_len < db.max_ext_len:
-        workspace = make_workspace(n, db.max_ext_len, dev)
     if stream is None:
         stream = torch.cuda.current_stream(dev)
-    sc = _lib.Scoring(match, mismatch, gap, xdrop)
-    st = lib.logan_xdrop_batch(
-        db.pool.data_ptr(), db.fmt, db.pool_len, db.q_off.data_ptr(), db.q_len.data_ptr(),
-        db.t_off.data_ptr(), db.t_len.data_ptr(), db.q_seed.data_ptr(), db.t_seed.data_ptr(),
-        n, db.k, sc, _opts(first_level, timing_events, latency_first, handover, first_slots, poison, subst, zdrop,
-              throughput_first),
-        out.data_ptr(),
-        cells.data_ptr(),
-        stats.data_ptr() if stats is not None else None,
-        workspace.ptr(), workspace.nbytes, stream.cuda_stream)
+    # the library launches on the current device: make it db's (multi-GPU callers)
+    with torch.cuda.device(dev):
+        if out is None:
+            out = torch.empty((n, 5), dtype=torch.int32, device=dev)
+        if cells is None:
+            cells = torch.empty(n, dtype=torch.int64, device=dev)
+        if workspace is None or workspace.n_pairs < n or workspace.max_ext_len < db.max_ext_len:
+            workspace = make_workspace(n, db.max_ext_len, dev)
+        # the kernels run asynchronously on `stream`: keep the caching allocator from
+        # handing these blocks to another stream's allocation before they finish
+        for t in (out, cells, workspace.tensor):
+            t.record_stream(stream)
+        sc = _lib.Scoring(match, mismatch, gap, xdrop)
+        st = lib.logan_xdrop_batch(
+            db.pool.data_ptr(), db.fmt, db.pool_len, db.q_off.data_ptr(), db.q_len.data_ptr(),
+            db.t_off.data_ptr(), db.t_len.data_ptr(), db.q_seed.data_ptr(), db.t_seed.data_ptr(),
+            n, db.max_ext_len, db.k, sc,
+            _opts(first_level, timing_events, latency_first, handover, first_slots, poison, subst, zdrop,
+                  throughput_first),
+            out.data_ptr(),
+            cells.data_ptr(),
+            stats.data_ptr() if stats is not None else None,
+            workspace.ptr(), workspace.nbytes, stream.cuda_stream)
     _lib.check(st)
     return out, cells
 
@@ -156,7 +163,9 @@ def new_stats(device=None):
 def stats_dict(stats_tensor) -> dict:
     v = [int(x) for x in stats_tensor.cpu().tolist()]
     return {"tasks_started": v[0:8], "tasks_finished": v[8:16], "cells_per_level": v[16:24],
-            "window_shifts": v[24], "cells_total": v[25]}
+            "window_shifts": v[24], "cells_total": v[25], "pairs_invalid": v[26], "helper_tasks": v[27],
+            "first_level": v[28] & 0xffffffff, "first_width": v[28] >> 32,
+            "first_shape": "latency" if v[29] & 0xffffffff else "throughput", "first_helpers": bool(v[29] >> 32)}
 
 
 class HostArena:
@@ -191,13 +200,15 @@ def xdrop_batch_host(pool: np.ndarray, fmt: int, pool_len: int, q_off, q_len, t_
     arrs = [np.ascontiguousarray(a) for a in (q_off, q_len, t_off, t_len, q_seed, t_seed)]
     if asynchronous and any(a is not b for a, b in zip(arrs, (q_off, q_len, t_off, t_len, q_seed, t_seed))):
         raise ValueError("asynchronous host calls need C-contiguous numpy inputs (they must outlive the call)")
+    dev = arena.tensor.device
     if stream is None:
-        stream = torch.cuda.current_stream()
+        stream = torch.cuda.current_stream(dev)
     sc = _lib.Scoring(match, mismatch, gap, xdrop)
     ptr = lambda a: a.ctypes.data
     fn = lib.logan_xdrop_batch_host_async if asynchronous else lib.logan_xdrop_batch_host
-    st = fn(ptr(pool), fmt, pool_len, *[ptr(a) for a in arrs], n, k, sc,
-            _opts(first_level, subst=subst, zdrop=zdrop), ptr(out), ptr(cells),
-            arena.tensor.data_ptr(), arena.nbytes, stream.cuda_stream)
+    with torch.cuda.device(dev):
+        st = fn(ptr(pool), fmt, pool_len, *[ptr(a) for a in arrs], n, k, sc,
+                _opts(first_level, subst=subst, zdrop=zdrop), ptr(out), ptr(cells),
+                arena.tensor.data_ptr(), arena.nbytes, stream.cuda_stream)
     _lib.check(st)
     return out, cells

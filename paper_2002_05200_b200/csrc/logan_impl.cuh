@@ -17,6 +17,8 @@ constexpr int NBUCKET = 2048;
 constexpr int NLEVEL = 8;  // 6 window levels + the band level + the CTA level
 constexpr int BAND_LEVEL = 6, WIDE_LEVEL = 7;
 constexpr int SETUP_THREADS = 256;
+constexpr int32_t XDROP_MAX = 1 << 28;   // ABI limit on X and Z
+constexpr int32_t WINDOW_XMAX = 1 << 19; // register windows: (X + 2*127) * KEYMUL < 2^31
 
 __device__ __forceinline__ uint32_t cost_bucket(uint32_t c) {
     // monotone log-linear bucket: 32 octaves x 64 sub-buckets (c >= 1)
@@ -28,7 +30,7 @@ __device__ __forceinline__ uint32_t cost_bucket(uint32_t c) {
 // Workspace layout (each region 256-byte aligned).
 // First-level window: one lane per task x w0 slots, w0 in {20, 24, 28, 32}
 // chosen at run time from X and the read lengths (auto_first_slots), or forced
-// by options.first_slots. LOGAN_L0_R (build knob) restricts it to one value.
+// by options.first_slots.
 constexpr int NWIDTH = 6;  // register-window widths w0, 64, 128, 256, 512, 1024
 static const int kWidth[NWIDTH] = {32, 64, 128, 256, 512, 1024};  // [0]: the largest w0 (pool sizing)
 
@@ -82,9 +84,11 @@ static __global__ void k_expand(const Params P, TaskRes *tres, uint16_t *tbucket
     __shared__ uint32_t sh[NBUCKET];
     for (int b = threadIdx.x; b < NBUCKET; b += blockDim.x) sh[b] = 0;
     __syncthreads();
+    uint32_t n_bad = 0;
     for (int64_t p = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; p < P.n_pairs;
          p += (int64_t)gridDim.x * blockDim.x) {
         const bool ok = pair_valid(P, p);
+        n_bad += ok ? 0u : 1u;
 #pragma unroll
         for (int side = 0; side < 2; ++side) {
             const uint32_t task = (uint32_t)(2 * p + side);
@@ -105,6 +109,13 @@ static __global__ void k_expand(const Params P, TaskRes *tres, uint16_t *tbucket
             }
             tbucket[task] = bk;
         }
+    }
+    if (P.stats && n_bad) atomicAdd((unsigned long long *)&P.stats->pairs_invalid, (unsigned long long)n_bad);
+    if (P.stats && blockIdx.x == 0 && threadIdx.x == 0) {
+        P.stats->first_level = P.info[0];
+        P.stats->first_width = P.info[1];
+        P.stats->first_shape = P.info[2];
+        P.stats->first_helpers = P.info[3];
     }
     __syncthreads();
     for (int b = threadIdx.x; b < NBUCKET; b += blockDim.x)
@@ -158,7 +169,8 @@ static __global__ void k_combine(const Params P, const TaskRes *tres, logan_resu
          p += (int64_t)gridDim.x * blockDim.x) {
         const TaskRes L = tres[2 * p], R = tres[2 * p + 1];
         logan_result_t r;
-        if ((L.flags | R.flags) & 3) {  // invalid pair, or wide scratch too small (max_ext_len)
+        if ((L.flags | R.flags) & 3) {  // invalid pair (flags 2, the CTA level's scratch guard, cannot occur:
+                                         // pair_valid rejects extensions above the bound that sizes it)
             r = {INT32_MIN, -1, -1, -1, -1};
             if (cells) cells[p] = 0;
         } else {
@@ -231,9 +243,6 @@ static cudaError_t launch_win(const Params &P, const LevelIO &io_in, const Level
 template <int FMT>
 static cudaError_t launch_first(int w0, bool helpers, const Params &P, const LevelIO &io, const LevelIO &hio,
                                 int sms, cudaStream_t s) {
-#ifdef LOGAN_L0_R
-    w0 = LOGAN_L0_R;
-#endif
     switch (w0) {
         case 16: return helpers ? launch_win<1, 16, FMT, LOGAN_HSHAPE(64)>(P, io, hio, sms, s)
                                 : launch_win<1, 16, FMT, 0, 0>(P, io, hio, sms, s);
@@ -327,7 +336,7 @@ static int auto_first_slots(int32_t xdrop, int64_t max_ext) {
 }
 
 template <int FMT>
-int run_batch(const Params &P, const logan_options_t *opt, logan_result_t *out, uint64_t *cells,
+int run_batch(const Params &P, const logan_options_t *opt, bool wide_only, logan_result_t *out, uint64_t *cells,
                      logan_stats_t *stats, uint8_t *ws, const Layout &L, cudaStream_t s) {
     TaskRes *tres = (TaskRes *)(ws + L.tres);
     uint16_t *tbucket = (uint16_t *)(ws + L.tbucket);
@@ -350,31 +359,20 @@ int run_batch(const Params &P, const logan_options_t *opt, logan_result_t *out, 
     auto mark = [&](int stage, int which) -> bool {
         return !ev || cudaEventRecord(ev[2 * stage + which], s) == cudaSuccess;
     };
-    if (!mark(0, 0)) return LOGAN_ECUDA;
-    const int64_t per_block = SETUP_THREADS;
-    int grid = (int)((P.n_pairs + per_block - 1) / per_block);
-    if (grid > sms * 8) grid = sms * 8;
-    if (grid < 1) grid = 1;
-    k_expand<<<grid, SETUP_THREADS, 0, s>>>(P, tres, tbucket, hist);
-    k_scan<<<1, SETUP_THREADS, 0, s>>>(hist, cursor_b, &ctr[0]);
-    int grid2 = (int)((L.ntask + per_block - 1) / per_block);
-    if (grid2 > sms * 8) grid2 = sms * 8;
-    if (grid2 < 1) grid2 = 1;
-    k_scatter<<<grid2, SETUP_THREADS, 0, s>>>(L.ntask, tbucket, cursor_b, queue);
-    if (cudaGetLastError() != cudaSuccess) return LOGAN_ECUDA;
-    if (!mark(0, 1)) return LOGAN_ECUDA;
-
     // level choice from the expected band width: about X slots under +1/-1/-1;
     // with a substitution matrix about X / |gap| (moving one slot off the
     // alignment's diagonal costs two gaps against at most X of slack)
     const int32_t xband = fmt_base(FMT) == FMT_U8S ? (P.xdrop + (-P.gap) - 1) / (-P.gap) : P.xdrop;
     int first = (opt && opt->first_level > 0) ? opt->first_level - 1 : auto_first_level(xband);
+    if (wide_only) first = WIDE_LEVEL;  // X' > 2^19: beyond the windows' key range (header)
     // no band level for matrices or Z-drop: those tasks go on to the CTA level
     constexpr bool no_band = fmt_base(FMT) == FMT_U8S || fmt_z(FMT);
     if (no_band && first == BAND_LEVEL) first = WIDE_LEVEL;
     if (first < 0 || first > NLEVEL - 1) return LOGAN_EINVAL;
     uint32_t *recs[2] = {(uint32_t *)(ws + L.recsA), (uint32_t *)(ws + L.recsB)};
-    const int w0 = (opt && opt->first_slots > 0) ? opt->first_slots : auto_first_slots(xband, L.wide_stride - 2);
+    // flags bit 0 at level 1: the 32-slot window, the only one with a latency shape
+    const int w0 = (opt && opt->first_slots > 0) ? opt->first_slots
+                   : ((opt && (opt->flags & 1)) ? 32 : auto_first_slots(xband, P.max_ext));
     const int w5 = auto_top_width(xband);
     auto width_of = [&](int lv) { return lv == 0 ? w0 : (lv == NWIDTH - 1 ? w5 : kWidth[lv]); };
     const uint32_t *in_list = queue;
@@ -426,6 +424,29 @@ int run_batch(const Params &P, const logan_options_t *opt, logan_result_t *out, 
     const bool few_tasks = (first > 0 && first < NWIDTH && groups_needed < (int64_t)sms * 8) ||
                            (first == 0 && w0 == 32 && groups_needed < (int64_t)sms * 2);
     const bool latency_first = (opt && (opt->flags & 1)) || (few_tasks && !(opt && (opt->flags & 8)));
+    // the first level's launch, recorded in stats (diagnostics: which kernel ran)
+    Params Pe = P;
+    if (stats) {
+        const bool shape_lat = latency_first && !(first == 0 && w0 != 32);
+        Pe.info[0] = (uint32_t)(first + 1);
+        Pe.info[1] = first < NWIDTH ? (uint32_t)width_of(first) : 0u;
+        Pe.info[2] = first < NWIDTH && shape_lat ? 1u : 0u;
+        Pe.info[3] = first < NWIDTH - 1 && !latency_first ? 1u : 0u;
+    }
+    if (!mark(0, 0)) return LOGAN_ECUDA;
+    const int64_t per_block = SETUP_THREADS;
+    int grid = (int)((P.n_pairs + per_block - 1) / per_block);
+    if (grid > sms * 8) grid = sms * 8;
+    if (grid < 1) grid = 1;
+    k_expand<<<grid, SETUP_THREADS, 0, s>>>(Pe, tres, tbucket, hist);
+    k_scan<<<1, SETUP_THREADS, 0, s>>>(hist, cursor_b, &ctr[0]);
+    int grid2 = (int)((L.ntask + per_block - 1) / per_block);
+    if (grid2 > sms * 8) grid2 = sms * 8;
+    if (grid2 < 1) grid2 = 1;
+    k_scatter<<<grid2, SETUP_THREADS, 0, s>>>(L.ntask, tbucket, cursor_b, queue);
+    if (cudaGetLastError() != cudaSuccess) return LOGAN_ECUDA;
+    if (!mark(0, 1)) return LOGAN_ECUDA;
+
     for (int lv = first; lv < NLEVEL; ++lv) {
         // substitution matrices have no band level: tasks that outgrow the widest
         // window go straight on to the CTA level (which restarts them)
@@ -441,6 +462,7 @@ int run_batch(const Params &P, const logan_options_t *opt, logan_result_t *out, 
                     // the next level's IO: it reads this level's hand-overs
                     hio = level_io(lv + 1, lists[out_sel], &ctr[CTR_OUT + lv], recs[out_sel],
                                    (const int32_t *)(ws + L.pool[lv]), rec_ints(width_of(lv)), out_sel ^ 1);
+                    hio.is_helper = 1;
                     io.done = &ctr[CTR_DONE];
                     // entries are published by writing the task id: start from NO_TASK
                     if (cudaMemsetAsync(lists[out_sel], 0xff, sizeof(uint32_t) * (size_t)L.ntask, s) != cudaSuccess)
@@ -496,8 +518,8 @@ int run_batch(const Params &P, const logan_options_t *opt, logan_result_t *out, 
 
 // explicit instantiations live in logan_fmt*.cu (one format per translation unit)
 #define LOGAN_RUN_BATCH_SIG(F)                                                                   \
-    int run_batch<F>(const Params &P, const logan_options_t *opt, logan_result_t *out, uint64_t *cells, \
-                     logan_stats_t *stats, uint8_t *ws, const Layout &L, cudaStream_t s)
+    int run_batch<F>(const Params &P, const logan_options_t *opt, bool wide_only, logan_result_t *out, \
+                     uint64_t *cells, logan_stats_t *stats, uint8_t *ws, const Layout &L, cudaStream_t s)
 
 }  // namespace logan
 

@@ -15,6 +15,8 @@
 //                   shared-memory ring of 8192 slots (wide bands: large X)
 //   6. level 8    : k_wide, one CTA per task, unbounded band (restart)
 //   7. k_combine  : seed score + L + R -> logan_result_t, cells (c-amb-8/10)
+#include <algorithm>
+
 #include "logan_impl.cuh"
 
 namespace logan {
@@ -67,8 +69,8 @@ static int check_args(const uint8_t *seq_pool, int32_t seq_fmt, int64_t pool_len
         return LOGAN_EINVAL;
     if (!subst && (sc.match <= 0 || sc.match > 127 || sc.mismatch >= 0 || sc.mismatch < -127))
         return LOGAN_EINVAL;
-    if (sc.gap >= 0 || sc.gap < -127 || sc.xdrop < 0 || sc.xdrop > (1 << 19)) return LOGAN_EINVAL;
-    if (opt && (opt->flags & 4) && (opt->zdrop < 0 || opt->zdrop > (1 << 19))) return LOGAN_EINVAL;
+    if (sc.gap >= 0 || sc.gap < -127 || sc.xdrop < 0 || sc.xdrop > XDROP_MAX) return LOGAN_EINVAL;
+    if (opt && (opt->flags & 4) && (opt->zdrop < 0 || opt->zdrop > XDROP_MAX)) return LOGAN_EINVAL;
     if (opt && (opt->first_level < 0 || opt->first_level > NLEVEL)) return LOGAN_EINVAL;
     if (opt && opt->first_slots != 0 && opt->first_slots != 16 && opt->first_slots != 20 && opt->first_slots != 24 &&
         opt->first_slots != 28 && opt->first_slots != 32)
@@ -81,25 +83,18 @@ static int check_args(const uint8_t *seq_pool, int32_t seq_fmt, int64_t pool_len
 
 int logan_xdrop_batch(const uint8_t *seq_pool, int32_t seq_fmt, int64_t pool_len, const int64_t *q_off,
                       const int32_t *q_len, const int64_t *t_off, const int32_t *t_len, const int32_t *q_seed,
-                      const int32_t *t_seed, int64_t n_pairs, int32_t k, logan_scoring_t sc,
+                      const int32_t *t_seed, int64_t n_pairs, int64_t max_ext_len, int32_t k, logan_scoring_t sc,
                       const logan_options_t *opt, logan_result_t *out, uint64_t *cells, logan_stats_t *stats,
                       void *workspace, size_t workspace_bytes, void *stream) {
     int st = check_args(seq_pool, seq_fmt, pool_len, q_off, q_len, t_off, t_len, q_seed, t_seed, n_pairs, k,
                         sc, opt, out);
     if (st != LOGAN_OK) return st;
+    if (max_ext_len < 0 || max_ext_len >= ((int64_t)1 << 30)) return LOGAN_EINVAL;
     if (n_pairs == 0) return LOGAN_OK;
     if (!workspace || ((uintptr_t)workspace & 255) != 0) return LOGAN_EINVAL;
-    // the wide level's scratch is sized by the caller's bound on extension lengths:
-    // recover it from the workspace size (largest stride that fits)
-    const Layout base = make_layout(n_pairs, 0);
-    if (workspace_bytes < base.total) return LOGAN_ENOSPC;
-    const size_t per_col = sizeof(int32_t) * 3 * WIDE_CTAS;
-    int64_t max_ext = (int64_t)((workspace_bytes - base.total) / per_col);
-    // alignment padding makes the estimate approximate: take the largest bound that fits
-    while (make_layout(n_pairs, max_ext + 1).total <= workspace_bytes) ++max_ext;
-    while (max_ext > 0 && make_layout(n_pairs, max_ext).total > workspace_bytes) --max_ext;
-    Layout L = make_layout(n_pairs, max_ext);
-    if (L.total > workspace_bytes) return LOGAN_ENOSPC;
+    // the caller's extension bound sizes the workspace (the CTA level's scratch)
+    const Layout L = make_layout(n_pairs, max_ext_len);
+    if (workspace_bytes < L.total) return LOGAN_ENOSPC;
 
     Params P;
     P.pool = (const uint32_t *)seq_pool;
@@ -110,26 +105,36 @@ int logan_xdrop_batch(const uint8_t *seq_pool, int32_t seq_fmt, int64_t pool_len
     P.q_off = q_off; P.q_len = q_len; P.t_off = t_off; P.t_len = t_len;
     P.q_seed = q_seed; P.t_seed = t_seed;
     P.n_pairs = n_pairs;
+    P.max_ext = max_ext_len;
     P.k = k;
-    P.match = sc.match; P.mismatch = sc.mismatch; P.gap = sc.gap; P.xdrop = sc.xdrop;
+    P.match = sc.match; P.mismatch = sc.mismatch; P.gap = sc.gap;
     P.one = 1;
     P.poison = (opt && (opt->flags & 2)) ? 1 : 0;
     P.subst = opt ? opt->subst : nullptr;
     P.alphabet = (opt && opt->subst) ? opt->alphabet : 0;
-    P.zdrop = (opt && (opt->flags & 4)) ? opt->zdrop : -1;
+    P.stats = stats;
+    P.info[0] = P.info[1] = P.info[2] = P.info[3] = 0;
+    // X' = min(X, 4 max_ext w): no cell of any extension of the batch can drop
+    // at or above that bound, so the results equal those at X (header, scoring)
+    const int64_t w = P.subst ? 127 : std::max<int64_t>(sc.match, std::max<int64_t>(-sc.mismatch, -sc.gap));
+    const int64_t xnp = 4 * std::max<int64_t>(max_ext_len, 1) * w;
+    P.xdrop = (int32_t)std::min<int64_t>(sc.xdrop, xnp);
+    // Z-drop fires only if best - M_d > Z, and best - M_d <= X' on any antidiagonal
+    // with a live cell: Z >= X' is the same as no Z-drop (header, zdrop)
+    P.zdrop = (opt && (opt->flags & 4) && opt->zdrop < P.xdrop) ? opt->zdrop : -1;
+    // register windows keep X' <= 2^19 (argmax key range); beyond, the CTA level
+    const bool wide_only = P.xdrop > WINDOW_XMAX;
 
-    // extension lengths beyond the wide scratch would overflow it: such pairs
-    // are rejected up front by the caller-side bound (documented in the header)
     cudaStream_t s = (cudaStream_t)stream;
     uint8_t *ws = (uint8_t *)workspace;
     if (P.zdrop >= 0) {  // the Z-drop builds of the kernels (FMT | FMT_Z)
-        if (P.subst) return run_batch<FMT_U8S | FMT_Z>(P, opt, out, cells, stats, ws, L, s);
-        if (seq_fmt == LOGAN_SEQ_2BIT) return run_batch<LOGAN_SEQ_2BIT | FMT_Z>(P, opt, out, cells, stats, ws, L, s);
-        return run_batch<LOGAN_SEQ_U8 | FMT_Z>(P, opt, out, cells, stats, ws, L, s);
+        if (P.subst) return run_batch<FMT_U8S | FMT_Z>(P, opt, wide_only, out, cells, stats, ws, L, s);
+        if (seq_fmt == LOGAN_SEQ_2BIT) return run_batch<LOGAN_SEQ_2BIT | FMT_Z>(P, opt, wide_only, out, cells, stats, ws, L, s);
+        return run_batch<LOGAN_SEQ_U8 | FMT_Z>(P, opt, wide_only, out, cells, stats, ws, L, s);
     }
-    if (P.subst) return run_batch<FMT_U8S>(P, opt, out, cells, stats, ws, L, s);
-    if (seq_fmt == LOGAN_SEQ_2BIT) return run_batch<LOGAN_SEQ_2BIT>(P, opt, out, cells, stats, ws, L, s);
-    return run_batch<LOGAN_SEQ_U8>(P, opt, out, cells, stats, ws, L, s);
+    if (P.subst) return run_batch<FMT_U8S>(P, opt, wide_only, out, cells, stats, ws, L, s);
+    if (seq_fmt == LOGAN_SEQ_2BIT) return run_batch<LOGAN_SEQ_2BIT>(P, opt, wide_only, out, cells, stats, ws, L, s);
+    return run_batch<LOGAN_SEQ_U8>(P, opt, wide_only, out, cells, stats, ws, L, s);
 }
 
 size_t logan_host_arena_bytes(int64_t n_pairs, int64_t pool_len, int32_t seq_fmt, int64_t max_ext_len) {
@@ -182,6 +187,16 @@ static int host_batch(const uint8_t *seq_pool, int32_t seq_fmt, int64_t pool_len
     if (st != LOGAN_OK) return st;
     if (n_pairs == 0) return LOGAN_OK;
     if (!device_arena || ((uintptr_t)device_arena & 255) != 0) return LOGAN_EINVAL;
+    // the extension bound over the valid pairs (the same validation as the device's
+    // k_expand; invalid pairs are rejected there whatever their lengths)
+    int64_t max_ext = 0;
+    for (int64_t p = 0; p < n_pairs; ++p) {
+        const int64_t ql = q_len[p], tl = t_len[p], qs = q_seed[p], ts = t_seed[p];
+        if (ql < 0 || tl < 0 || ql >= (1 << 30) || tl >= (1 << 30)) continue;
+        if (qs < 0 || ts < 0 || qs + k > ql || ts + k > tl) continue;
+        if (q_off[p] < 0 || t_off[p] < 0 || q_off[p] + ql > pool_len || t_off[p] + tl > pool_len) continue;
+        max_ext = std::max(max_ext, std::max(std::max(qs, ts), std::max(ql - qs - k, tl - ts - k)));
+    }
     const int64_t pool_bytes = seq_fmt == LOGAN_SEQ_2BIT ? (pool_len + 3) / 4 : pool_len;
     uint8_t *a = (uint8_t *)device_arena;
     size_t o = 0;
@@ -206,8 +221,9 @@ static int host_batch(const uint8_t *seq_pool, int32_t seq_fmt, int64_t pool_len
         cudaMemcpyAsync(d_qs, q_seed, n4, cudaMemcpyHostToDevice, s) != cudaSuccess ||
         cudaMemcpyAsync(d_ts, t_seed, n4, cudaMemcpyHostToDevice, s) != cudaSuccess)
         return LOGAN_ECUDA;
-    st = logan_xdrop_batch(d_pool, seq_fmt, pool_len, d_qoff, d_qlen, d_toff, d_tlen, d_qs, d_ts, n_pairs, k, sc,
-                           opt, d_out, d_cells, nullptr, a + o, arena_bytes - o, stream);
+    if (o + logan_workspace_bytes(n_pairs, max_ext) > arena_bytes) return LOGAN_ENOSPC;
+    st = logan_xdrop_batch(d_pool, seq_fmt, pool_len, d_qoff, d_qlen, d_toff, d_tlen, d_qs, d_ts, n_pairs, max_ext,
+                           k, sc, opt, d_out, d_cells, nullptr, a + o, arena_bytes - o, stream);
     if (st != LOGAN_OK) return st;
     if (cudaMemcpyAsync(out, d_out, sizeof(logan_result_t) * (size_t)n_pairs, cudaMemcpyDeviceToHost, s) !=
         cudaSuccess)

@@ -25,6 +25,8 @@ struct Params {
     const int32_t *q_seed;
     const int32_t *t_seed;
     int64_t n_pairs;
+    int64_t max_ext;        // the caller's bound on extension lengths (longer: invalid pair)
+    logan_stats_t *stats;   // NULL or the caller's device statistics
     int32_t k;
     int32_t match, mismatch, gap, xdrop;
     int32_t one;  // = 1 at run time; opaque to the compiler (see Window::cell)
@@ -32,6 +34,7 @@ struct Params {
     const int8_t *subst;  // NULL, or an alphabet x alphabet substitution matrix (device memory)
     int32_t alphabet;
     int32_t zdrop;        // Z-drop threshold (c-amb-19), < 0 = off
+    uint32_t info[4];     // the first level's launch (k_expand copies it into stats)
 };
 
 // Result of one extension task (L or R of one pair), 24 bytes.
@@ -69,6 +72,7 @@ struct LevelIO {
     int32_t helpers;             // blocks whose last warp is a helper
     uint32_t workers;            // producer groups (non-helper groups) in the launch
     uint32_t *done;              // producer groups that finished
+    int32_t is_helper;           // this IO drives in-kernel helpers (stats.helper_tasks)
 };
 
 constexpr uint32_t NO_TASK = 0xffffffffu;
@@ -89,6 +93,9 @@ struct TaskDesc {
     bool valid;    // pair passed validation
 };
 
+// A pair is valid iff its seed and reads lie inside the reads / pool and both
+// extensions are at most the caller's declared bound max_ext long (header,
+// logan_xdrop_batch); invalid pairs get the invalid result.
 __device__ __forceinline__ bool pair_valid(const Params &P, int64_t p) {
     const int64_t qo = P.q_off[p], to = P.t_off[p];
     const int32_t ql = P.q_len[p], tl = P.t_len[p], qs = P.q_seed[p], ts = P.t_seed[p];
@@ -96,6 +103,7 @@ __device__ __forceinline__ bool pair_valid(const Params &P, int64_t p) {
     if (ql < 0 || tl < 0 || ql >= (1 << 30) || tl >= (1 << 30)) return false;
     if (qs < 0 || ts < 0 || qs + k > ql || ts + k > tl) return false;
     if (qo < 0 || to < 0 || qo + ql > P.pool_len || to + tl > P.pool_len) return false;
+    if (qs > P.max_ext || ts > P.max_ext || ql - qs - k > P.max_ext || tl - ts - k > P.max_ext) return false;
     return true;
 }
 

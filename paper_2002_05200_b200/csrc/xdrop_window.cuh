@@ -630,8 +630,10 @@ __device__ __forceinline__ void run_group(Win &w, const Params &P, const LevelIO
         const uint32_t rec = io.in_recs ? io.in_recs[pos] : NO_REC;
         if (rec != NO_REC) w.resume(P, io.rec_in + (size_t)rec * io.rec_in_stride);
         else w.init(P, task);
-        if (io.stats && w.gl == 0)
+        if (io.stats && w.gl == 0) {
             atomicAdd((unsigned long long *)&io.stats->tasks_started[io.level], 1ull);
+            if (io.is_helper) atomicAdd((unsigned long long *)&io.stats->helper_tasks, 1ull);
+        }
         if (w.st.d & 1) rc = w.template step<0>(P);
         return true;
     };

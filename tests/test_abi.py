@@ -53,7 +53,7 @@ def test_library_is_sm100a(lib):
 
 
 def test_host_side_checks_without_gpu(lib):
-    assert lib.logan_abi_version() == 1
+    assert lib.logan_abi_version() == 2
     # window widths by level (diagnostics; results never depend on them)
     assert lib.logan_level_width(1, 20, 2500, 0) == 28 and lib.logan_level_width(1, 20, 10000, 0) == 32
     assert lib.logan_level_width(1, 20, 7700, 0) == 28 and lib.logan_level_width(1, 18, 7700, 0) == 28
@@ -69,31 +69,58 @@ def test_host_side_checks_without_gpu(lib):
     assert 0 < small < big
     assert lib.logan_workspace_bytes(10, 1000) > small  # wide-level scratch grows with length
     sc_bad = _lib.Scoring(1, 1, -1, 10)  # mismatch must be < 0
-    st = lib.logan_xdrop_batch(None, 1, 0, None, None, None, None, None, None, 5, 17, sc_bad,
+    st = lib.logan_xdrop_batch(None, 1, 0, None, None, None, None, None, None, 5, 0, 17, sc_bad,
                                None, None, None, None, None, 0, None)
     assert st == _lib.LOGAN_EINVAL
     sc = _lib.Scoring(1, -1, -1, 10)
-    st = lib.logan_xdrop_batch(None, 7, 0, None, None, None, None, None, None, 5, 17, sc,
+    st = lib.logan_xdrop_batch(None, 7, 0, None, None, None, None, None, None, 5, 0, 17, sc,
                                None, None, None, None, None, 0, None)
     assert st == _lib.LOGAN_EINVAL  # unknown format
-    st = lib.logan_xdrop_batch(None, 1, 0, None, None, None, None, None, None, 0, 17, sc,
+    st = lib.logan_xdrop_batch(None, 1, 0, None, None, None, None, None, None, 0, 0, 17, sc,
                                None, None, None, None, None, 0, None)
     assert st == _lib.LOGAN_OK  # n_pairs = 0: no-op, nothing launched
-    st = lib.logan_xdrop_batch(None, 1, 0, None, None, None, None, None, None, 3, 17, sc,
+    st = lib.logan_xdrop_batch(None, 1, 0, None, None, None, None, None, None, 3, 0, 17, sc,
                                None, None, None, None, None, 0, None)
     assert st == _lib.LOGAN_EINVAL  # NULL device pointers
     # substitution matrices: u8 pool only, 1 <= alphabet <= 32 (checked before any launch)
     opt = _lib.Options()
     opt.subst = 0x1000
     opt.alphabet = 20
-    st = lib.logan_xdrop_batch(None, 1, 0, None, None, None, None, None, None, 3, 17, sc,
+    st = lib.logan_xdrop_batch(None, 1, 0, None, None, None, None, None, None, 3, 0, 17, sc,
                                ctypes.byref(opt), None, None, None, None, 0, None)
     assert st == _lib.LOGAN_EINVAL  # 2-bit pool with a matrix
     opt.alphabet = 33
-    st = lib.logan_xdrop_batch(None, 0, 0, None, None, None, None, None, None, 3, 17, sc,
+    st = lib.logan_xdrop_batch(None, 0, 0, None, None, None, None, None, None, 3, 0, 17, sc,
                                ctypes.byref(opt), None, None, None, None, 0, None)
     assert st == _lib.LOGAN_EINVAL  # alphabet too large
     assert ctypes.sizeof(_lib.Options) == 64  # layout of logan_options_t
+
+
+def test_workspace_and_bounds_checked_before_launch(lib):
+    """ABI v2: the workspace must hold logan_workspace_bytes(n_pairs, max_ext_len)
+    (else LOGAN_ENOSPC, synchronously, nothing launched); X and Z up to 2^28 are
+    accepted, beyond is LOGAN_EINVAL; max_ext_len must be in [0, 2^30). The fake
+    device pointers below are never dereferenced: every check returns first."""
+    sc = _lib.Scoring(1, -1, -1, 20)
+    fake = 0x100000  # 256-byte aligned, non-NULL
+    args = lambda n, ext, sc_, ws_bytes, opt=None: (fake, 1, 1000, fake, fake, fake, fake, fake, fake, n, ext, 17,
+                                                    sc_, opt, fake, None, None, fake, ws_bytes, None)
+    need = lib.logan_workspace_bytes(100, 5000)
+    assert lib.logan_xdrop_batch(*args(100, 5000, sc, need - 1)) == _lib.LOGAN_ENOSPC
+    # a workspace sized for shorter extensions than the declared bound is refused
+    assert lib.logan_xdrop_batch(*args(100, 5000, sc, lib.logan_workspace_bytes(100, 100))) == _lib.LOGAN_ENOSPC
+    assert lib.logan_xdrop_batch(*args(100, -1, sc, need)) == _lib.LOGAN_EINVAL
+    assert lib.logan_xdrop_batch(*args(100, 1 << 30, sc, need)) == _lib.LOGAN_EINVAL
+    assert lib.logan_xdrop_batch(*args(100, 5000, _lib.Scoring(1, -1, -1, (1 << 28) + 1), need)) == _lib.LOGAN_EINVAL
+    assert lib.logan_xdrop_batch(*args(100, 5000, _lib.Scoring(1, -1, -1, -1), need)) == _lib.LOGAN_EINVAL
+    opt = _lib.Options()
+    opt.flags = 4
+    opt.zdrop = (1 << 28) + 1
+    assert lib.logan_xdrop_batch(*args(100, 5000, sc, need, ctypes.byref(opt))) == _lib.LOGAN_EINVAL
+    # the host entry point: an arena smaller than the copies it needs
+    st = lib.logan_xdrop_batch_host(fake, 1, 1000, fake, fake, fake, fake, fake, fake, 0, 17, sc, None, fake,
+                                    None, fake, 0, None)
+    assert st == _lib.LOGAN_OK  # n_pairs = 0: no-op
 
 
 def test_product_path_does_not_import_oracle():

@@ -270,14 +270,18 @@ def _mixed_pairs(seed, n=300, maxlen=300):
 
 @pytest.mark.parametrize("lvl", [1, 2, 3, 4, 5, 6])
 def test_latency_shapes_as_first_level(lvl):
-    """Every level's latency shape (one warp per task), forced as the first level."""
+    """Every level's latency shape (one warp per task), forced as the first level
+    (at level 1 flags bit 0 selects the 32-slot window, the width that has one)."""
     b = _mixed_pairs(lvl)
     for X in (0, 3, 10, 30, 80):
         ref = oracle_run(b, X)
         for fmt in FMTS:
             db = logan.to_device(b, fmt)
-            out, cells = logan.xdrop_batch(db, 1, -1, -1, X, first_level=lvl, latency_first=True)
+            st = logan.new_stats()
+            out, cells = logan.xdrop_batch(db, 1, -1, -1, X, first_level=lvl, latency_first=True, stats=st)
             torch.cuda.synchronize()
+            s = logan.stats_dict(st)
+            assert (s["first_level"], s["first_shape"], s["first_helpers"]) == (lvl, "latency", False), s
             assert_same(out.cpu().numpy(), cells.cpu().numpy().view(np.uint64), *ref,
                         what=f"latency level {lvl} X={X} fmt={fmt}")
 
@@ -337,17 +341,21 @@ def test_top_window_widths(X):
 
 def test_mass_overflow_with_helpers():
     """Most tasks overflow the first window (X far above its width): helpers take
-    what they can while level 1 runs, the next launch takes the rest; results exact."""
+    what they can while level 1 runs (its throughput shape forced with
+    options.flags bit 3: 8,000 tasks would otherwise take the latency shape),
+    the next launch takes the rest; results exact."""
     w = datagen.CONFIGS[2].with_(xdrop=60)
     b = datagen.generate(w, n_pairs=4000)
     idx = np.arange(0, b.n_pairs, 10)
     ref = oracle_run(b, 60, idx=idx)
     st = logan.new_stats()
     db = logan.to_device(b, logan.LOGAN_SEQ_2BIT)
-    out, cells = logan.xdrop_batch(db, 1, -1, -1, 60, first_level=1, stats=st)
+    out, cells = logan.xdrop_batch(db, 1, -1, -1, 60, first_level=1, stats=st, throughput_first=True)
     torch.cuda.synchronize()
     s = logan.stats_dict(st)
+    assert (s["first_level"], s["first_shape"], s["first_helpers"]) == (1, "throughput", True), s
     assert s["tasks_started"][1] > 1000  # mass hand-over to the W=64 level
+    assert s["helper_tasks"] > 0
     o, c = out.cpu().numpy(), cells.cpu().numpy().view(np.uint64)
     assert_same(o[idx], c[idx], *ref, what="mass overflow")
 
@@ -387,15 +395,24 @@ def test_cta_level_extension_equal_to_workspace_bound():
 @pytest.mark.parametrize("slots", [16, 20, 24, 28, 32])
 def test_first_window_widths(slots):
     """Every compiled first-window width (one lane per task) is exact, including
-    the overflow hand-over to the next level."""
+    the overflow hand-over to the next level: in the one-lane throughput shape
+    with in-kernel helpers (forced: 300 pairs would pick the latency shape at 32
+    slots) and in the automatic choice."""
     b = _mixed_pairs(300 + slots)
     for X in (0, 5, 12, 20):
         ref = oracle_run(b, X)
-        db = logan.to_device(b, logan.LOGAN_SEQ_2BIT)
-        out, cells = logan.xdrop_batch(db, 1, -1, -1, X, first_level=1, first_slots=slots)
-        torch.cuda.synchronize()
-        assert_same(out.cpu().numpy(), cells.cpu().numpy().view(np.uint64), *ref,
-                    what=f"first window {slots} X={X}")
+        for tp in (True, False):
+            db = logan.to_device(b, logan.LOGAN_SEQ_2BIT)
+            st = logan.new_stats()
+            out, cells = logan.xdrop_batch(db, 1, -1, -1, X, first_level=1, first_slots=slots, stats=st,
+                                           throughput_first=tp)
+            torch.cuda.synchronize()
+            s = logan.stats_dict(st)
+            assert s["first_width"] == slots
+            if tp:
+                assert (s["first_shape"], s["first_helpers"]) == ("throughput", True), s
+            assert_same(out.cpu().numpy(), cells.cpu().numpy().view(np.uint64), *ref,
+                        what=f"first window {slots} X={X} throughput_first={tp}")
 
 
 # --------------------------------------------------------------------------
@@ -609,3 +626,67 @@ def test_config7_and_zdrop_full_size_sampled():
     assert_same(oz[idx], cz[idx], *refz, what="C2 Z-drop sample")
     plain = gpu_run(b, w.xdrop)
     assert (cz <= plain[1]).all() and (oz[:, 0] <= plain[0][:, 0]).all()
+
+
+# --------------------------------------------------------------------------
+# Boundary (ABI v2): the declared extension bound, X up to 2^28, Z >= X
+
+def test_declared_extension_bound_rejects_longer_pairs_only():
+    """A pair with an extension longer than the declared max_ext_len is an
+    invalid pair (invalid result, 0 cells, counted in stats.pairs_invalid);
+    every other pair keeps its exact result. Never a wrong result with OK."""
+    import dataclasses
+    w = datagen.CONFIGS[1]
+    b = datagen.generate(w, n_pairs=200)
+    ref_o, ref_c = oracle_run(b, w.xdrop)
+    db = logan.to_device(b, logan.LOGAN_SEQ_2BIT)
+    bound = 700
+    ext = np.maximum(np.maximum(b.q_seed, b.t_seed),
+                     np.maximum(b.q_len - b.q_seed - w.k, b.t_len - b.t_seed - w.k))
+    over = ext > bound
+    assert 0 < over.sum() < b.n_pairs
+    st = logan.new_stats()
+    out, cells = logan.xdrop_batch(dataclasses.replace(db, max_ext_len=bound), 1, -1, -1, w.xdrop, stats=st)
+    torch.cuda.synchronize()
+    o, c = out.cpu().numpy(), cells.cpu().numpy().view(np.uint64)
+    assert logan.stats_dict(st)["pairs_invalid"] == int(over.sum())
+    assert (o[over] == np.array([-2 ** 31, -1, -1, -1, -1])).all() and (c[over] == 0).all()
+    assert (o[~over] == ref_o[~over]).all() and (c[~over] == ref_c[~over]).all()
+
+
+def test_huge_x_runs_exactly():
+    """X up to 2^28: X' = min(X, 4 max_ext w) gives the X = inf
+    results; when X' > 2^19 (long extensions, large |w|) only the CTA level can
+    hold it and the call runs there. Z >= X' is the same as no Z-drop."""
+    w = datagen.CONFIGS[1]
+    b = datagen.generate(w, n_pairs=40)
+    for (ma, mi, g) in ((1, -1, -1), (100, -127, -127)):
+        ref = oracle_run(b, 2 ** 28, ma, mi, g)
+        st = logan.new_stats()
+        got = gpu_run(b, 2 ** 28, ma, mi, g, stats=st)
+        assert_same(*got, *ref, what=f"X=2^28 scoring {(ma, mi, g)}")
+        s = logan.stats_dict(st)
+        if 4 * b.max_ext_len() * max(ma, -mi, -g) > 2 ** 19:
+            assert s["first_level"] == 8, s
+        assert_same(*gpu_run(b, 2 ** 19, ma, mi, g), *ref, what="X=2^19 == X=2^28 here")
+    db = logan.to_device(b, logan.LOGAN_SEQ_2BIT)
+    ref = oracle_run(b, 30)
+    out, cells = logan.xdrop_batch(db, 1, -1, -1, 30, zdrop=30)
+    torch.cuda.synchronize()
+    assert_same(out.cpu().numpy(), cells.cpu().numpy().view(np.uint64), *ref, what="Z >= X")
+
+
+def test_partition_independence_multi_device_wrapper():
+    """P4 partition independence: the single-process multi-device
+    wrapper (multi.xdrop_multi) with G = 1, 2, 4, 8 parts -- all on cuda:0 here
+    (this box has one GPU; the partition and gather logic is the same) --
+    returns exactly the one-call results, pair by pair, for C1 and a BELLA-like
+    C4 sample (dovetails + spurious pairs: the cost model's hard case)."""
+    from paper_2002_05200_b200 import multi
+    for cfg, n in ((1, 1000), (4, 600)):
+        w = datagen.CONFIGS[cfg]
+        b = datagen.generate(w, n_pairs=n, u8=False)
+        ref = gpu_run(b, w.xdrop)
+        for g in (1, 2, 4, 8):
+            o, c = multi.xdrop_multi(b, w, ["cuda:0"] * g)
+            assert_same(o, c, *ref, what=f"xdrop_multi config {cfg} G={g}")

@@ -1,4 +1,4 @@
-"""Multi-process host logic at world size 2 on CPU (gloo): partition + gather.
+"""Multi-process host logic at world sizes 2 and 4 on CPU (gloo): partition + gather.
 
 The per-rank compute is injected (the oracle stands in for the GPU here, as
 the tests may use it); the CUDA path is the default compute on GPU boxes.
@@ -7,6 +7,7 @@ import os
 import socket
 
 import numpy as np
+import pytest
 import torch.multiprocessing as mp
 
 import datagen
@@ -34,6 +35,23 @@ def test_partition_is_a_balanced_permutation():
         assert multi.partition_lpt(costs, g)[0].tolist() == parts[0].tolist()  # deterministic
 
 
+def test_cost_model_follows_the_overlap():
+    """A dovetail pair is costed by its overlap (the sweep ends about X/|gap|
+    antidiagonals past the shorter sequence), not by its read lengths; equal
+    extensions cost antidiagonals x band; invalid pairs cost 0."""
+    k, X = 17, 50
+    # seed in the middle of a 1 kb read against a 30 kb read: each side min 500
+    c = multi.pair_costs([1000, 30000, 1000, 10], [30000, 30000, 1000, 10], [491, 15000, 491, 5],
+                         [15000, 15000, 491, 20], k, X, -1)
+    assert c[3] == 0
+    # pair 0, left: min(491, 15000) = 491 -> min(15491, 2*491 + 2*50) = 1082 antidiagonals x 58;
+    # right: min(492, 14983) = 492 -> 1084 x 58
+    assert c[0] == 1082 * 58 + 1084 * 58
+    # pair 2 (1 kb x 1 kb): the whole matrix, 982 and 984 antidiagonals x 58
+    assert c[2] == 982 * 58 + 984 * 58
+    assert c[0] < c[1] / 10  # the 1 kb x 30 kb pair is not costed like two 30 kb reads
+
+
 def _oracle_compute(sub, w):
     import oracle
     return oracle.pairs(sub.pool_u8, 0, sub.q_off, sub.q_len, sub.t_off, sub.t_len, sub.q_seed,
@@ -41,25 +59,25 @@ def _oracle_compute(sub, w):
                         n_threads=2)
 
 
-def _worker(rank, world, port, ret):
+def _worker(rank, world, port, ret, cfg, n):
     import torch.distributed as dist
     os.environ["MASTER_ADDR"] = "127.0.0.1"
     os.environ["MASTER_PORT"] = str(port)
     dist.init_process_group("gloo", rank=rank, world_size=world)
-    w = datagen.CONFIGS[1]
-    b = datagen.generate(w, n_pairs=120)
+    w = datagen.CONFIGS[cfg]
+    b = datagen.generate(w, n_pairs=n)
     out, cells = multi.run_sharded(b, w, compute=_oracle_compute)
     ret[rank] = (out.copy(), cells.copy())
     dist.destroy_process_group()
 
 
-def test_sharded_gather_equals_single_process():
-    world = 2
+@pytest.mark.parametrize("world,cfg,n", [(2, 1, 120), (4, 1, 90), (4, 4, 24)])
+def test_sharded_gather_equals_single_process(world, cfg, n):
     mgr = mp.Manager()
     ret = mgr.dict()
-    mp.spawn(_worker, args=(world, _free_port(), ret), nprocs=world, join=True)
-    w = datagen.CONFIGS[1]
-    b = datagen.generate(w, n_pairs=120)
+    mp.spawn(_worker, args=(world, _free_port(), ret, cfg, n), nprocs=world, join=True)
+    w = datagen.CONFIGS[cfg]
+    b = datagen.generate(w, n_pairs=n)
     ref = _oracle_compute(b, w)
     for r in range(world):
         out, cells = ret[r]

@@ -176,9 +176,14 @@ def test_larger_x_can_lower_the_score():
     (c-amb-16): a larger X lets an early branch raise best and kill the branch
     that would score higher.  Cross-checked against the dict oracle."""
     A, B = "AATCACCCTTGGCCCT", "ACTATCTGCCCCT"
-    got = [oracle.extend(A, B, X).best for X in (1, 2, 3)]
-    assert got == [4, 3, 4]
-    assert [xdrop_dict(A, B, X)[0] for X in (1, 2, 3)] == got
+    got = [oracle.extend(A, B, X) for X in (1, 2, 3)]
+    assert [r.best for r in got] == [4, 3, 4]
+    assert [xdrop_dict(A, B, X)[0] for X in (1, 2, 3)] == [4, 3, 4]
+    # argmax and cells of SURVEY.md §8c c-amb-16's table (16 x 13: full DP 4 at (16,13), 208 cells)
+    assert [(r.i, r.j, r.cells) for r in got] == [(16, 13, 64), (8, 11, 89), (16, 13, 123)]
+    full = oracle.extend(A, B, INF)
+    assert (full.best, full.i, full.j, full.cells) == (4, 16, 13, 208)
+    assert full_dp_best(A, B, 1, -1, -1) == (4, 16, 13)
 
 
 # ------------------------------------------------------------- pair level --
