@@ -20,26 +20,32 @@
 //    odd d: up = E[s+1], left = E[s], diag = O[s]. Each step overwrites the
 //    array of its parity in place; only the lane-boundary value crosses lanes
 //    (one SHFL per step).
-//  * Scores are stored RELATIVE to the kill threshold T_d = best_{d-1} - X:
-//    u = S - T_d, live <=> u >= 0. The per-step rebase folds into the two
-//    scoring constants (gap' = gap - (T_d - T_{d-1}), s' = s - (T_d - T_{d-2}))
-//    so the cell is three DPX VIADDMNMX plus one VIMNMX.U32:
-//        u = max(max(up, left, DEAD - gap') + gap', diag + s');  u = min_u32(u, DEAD)
-//    (VIMNMX3, an add, VIADDMNMX, VIMNMX.U32), which maps every negative u to
-//    exactly DEAD = -2^20 (an exact, absorbing kill: a dead value can never
-//    climb back within 2^20 / match steps, far more than any task's
-//    antidiagonal count at the ABI's limits).
+//  * Scores are stored RELATIVE to a kill threshold T_e = best_{e-1} - X, and
+//    the kill is applied ONE ANTIDIAGONAL LATE ("kill on read"): step e first
+//    kills antidiagonal e-1 with T_{e-1} (one VIADDMNMX.U32 per slot, which also
+//    rebases it: u = min_u32(u' - (T_{e-1} - T_{e-2}), DEAD)), then computes the
+//    RAW cells of e from the killed e-1 and e-2 (relative to T_{e-1}):
+//        u' = max(max(up, left, DEAD - gap) + gap, diag + s - (T_{e-1} - T_{e-2}))
+//    (VIMNMX3, an FMA-pipe IMAD for diag + s', VIADDMNMX). best_e is the max
+//    over raw e (a raw value above best_{e-1} is >= T_e, i.e. live), so the
+//    reduction of e's maximum only has to finish by step e + 2: it overlaps
+//    step e + 1 instead of sitting on the per-antidiagonal critical path
+//    (for a warp per task: CREDUX ~23 cycles, measured in tools/lat_probe.cu).
+//    Every negative value after the kill is dead, and DEAD - 3*127 <= dead
+//    values <= DEAD (the floor keeps raw values >= DEAD): exact and absorbing.
 //  * Bases sit in registers, 4-bit fields (2-bit pool) or 16-bit fields (u8
 //    pool), one per slot; positions past an extension's end hold sentinels
 //    that match nothing, so cells outside the matrix (i > m or j > n) can only
 //    hold values below an earlier best and are excluded from the band
 //    bookkeeping by a per-lane validity mask -- no per-cell masking.
 //  * Per antidiagonal the max and its slot come from one packed key
-//    (u * 1027 + 1023 - slot, an IMAD) reduced with VIMNMX3 inside the lane and SHFL
-//    butterflies across the G lanes; the live extremes from a funnel-shifted
-//    sign mask + FLO. Ties go to the smallest slot = smallest i (c-amb-9).
+//    (u' * 1027 + 1023 - slot, an IMAD) reduced with VIMNMX3 inside the lane and
+//    CREDUX / SHFL butterflies across the G lanes; it is decoded only when it
+//    raises best. The live extremes come from a funnel-shifted sign mask + FLO.
+//    Ties go to the smallest slot = smallest i (c-amb-9).
 //  * The window re-centres by one slot when the band touches an edge; if the
-//    band is wider than W - 2 slots the task is handed to the next level.
+//    band is wider than W - 2 slots the task is handed to the next level in the
+//    canonical (un-pipelined) state after an even antidiagonal.
 #pragma once
 
 #include "xdrop_common.cuh"
@@ -51,11 +57,10 @@ constexpr uint32_t DEADU = 0xFFF00000u;  // (uint32_t)DEAD
 // Argmax key of a cell: u * KEYMUL + (1023 - slot). KEYMUL > 1023 keeps the
 // order (value, then smallest slot); it is not a power of two so the key is
 // one IMAD on the FMA pipe (the ALU pipe is the kernel's bottleneck).
-// |DEAD| * KEYMUL < 2^31 and (X + 2*127) * KEYMUL < 2^31 for X <= 2^19.
+// |DEAD - 1024| * KEYMUL < 2^31 and (X + 3*127) * KEYMUL < 2^31 for X <= 2^19.
 constexpr int32_t KEYMUL = 1027;
+constexpr int32_t KNONE = INT32_MIN;  // "no pending maximum" (below every raise threshold)
 
-// How many of the 4 sign-mask chains run on the FMA pipe (the rest use SHF on
-// the ALU pipe): balances the two pipes (tuned by measurement).
 // Minimum resident blocks per SM requested for the one-lane-per-task kernels
 // (caps registers; tuned by measurement).
 #ifndef LOGAN_L0_MINB
@@ -64,10 +69,6 @@ constexpr int32_t KEYMUL = 1027;
 
 #ifndef LOGAN_NCHAIN
 #define LOGAN_NCHAIN 4
-#endif
-
-#ifndef LOGAN_MASK_FMA_CHAINS
-#define LOGAN_MASK_FMA_CHAINS 0
 #endif
 
 template <int FMT> struct RegFmt;
@@ -97,7 +98,16 @@ template <> struct RegFmt<LOGAN_SEQ_2BIT | FMT_Z> : RegFmt<LOGAN_SEQ_2BIT> {};
 template <> struct RegFmt<LOGAN_SEQ_U8 | FMT_Z> : RegFmt<LOGAN_SEQ_U8> {};
 template <> struct RegFmt<FMT_U8S | FMT_Z> : RegFmt<FMT_U8S> {};
 
-// Group-uniform state of one task (replicated in each lane of the group).
+// Group-uniform state of one task (replicated in each lane of the group), in
+// the PIPELINED form of the sweep (header, "kill one antidiagonal late"). At
+// the start of step e (computing antidiagonal e; d = e - 1):
+//   - array of parity (e-1)&1: RAW values of e-1, relative to T_{e-2};
+//   - array of parity e&1:     KILLED values of e-2, relative to T_{e-2};
+//   - best / arg: folded through antidiagonal e-3 (best_{e-3});
+//   - Tq[(e-2)&1] = T_{e-2}; Tq[(e-1)&1] = T_{e-3};
+//   - K[(e-2)&1], K[(e-1)&1]: the pending maxima (keys) of raw e-2 and e-1
+//     (KNONE once folded), relative to T_{e-3} and T_{e-2};
+//   - sF / sL[(e-2)&1]: live slot extremes of e-2; [(e-1)&1] of e-3 (stale).
 template <int FMT>
 struct WinState {
     // sa feeds the top slot (read by lane G-1; sa.idx = S0 + W + ceil(d/2)),
@@ -105,17 +115,15 @@ struct WinState {
     Stream<FMT> sa, sb;
     uint32_t task;
     int32_t m, n;
-    int32_t d;             // last antidiagonal computed
+    int32_t d;             // last antidiagonal whose raw values are computed
     int32_t S0;            // slot of the window's first register
     int32_t best, arg_i, arg_j;
-    // thresholds: Tn = T_{d+1}; Tq[p] = the last T_e with e of parity p
-    // (after antidiagonal d: Tq[d&1] = T_d, Tq[(d-1)&1] = T_{d-1}). Indexing by
-    // parity (a compile-time constant inside a step) means nothing rotates.
-    int32_t Tn, Tq[2];
-    // live slot extremes of the last antidiagonal of each parity (sF[d&1] is
-    // antidiagonal d, sF[(d-1)&1] is d-1); an antidiagonal without a (valid)
-    // live cell has sF = EMPTY_F, sL = EMPTY_L, which makes every min / max
-    // below ignore it without a branch
+    int32_t Tq[2];
+    int32_t K[2];
+    int32_t KZ[2];         // Z-drop builds: pending in-matrix maxima (keys)
+    uint32_t dc[2];        // Z-drop builds: band cells added for the last antidiagonal of each parity
+    // an antidiagonal without a (valid) live cell has sF = EMPTY_F, sL =
+    // EMPTY_L, which makes every min / max below ignore it without a branch
     int32_t sF[2], sL[2];
     uint64_t cells;
     uint64_t cells_entry;  // cells already counted when the task entered this level
@@ -123,6 +131,8 @@ struct WinState {
 };
 
 // Hand-over record between levels: REC_HDR ints of scalars, then E[W], O[W].
+// The record holds the CANONICAL state after antidiagonal d (both d and d-1
+// killed; best = best_d), the format every level reads.
 constexpr int REC_HDR = 32;
 __host__ __device__ constexpr int rec_ints(int W) { return REC_HDR + 2 * W; }
 constexpr uint32_t NO_REC = 0xffffffffu;
@@ -145,6 +155,9 @@ __device__ __forceinline__ int32_t grp_min(int32_t v, unsigned gmask) {
     return v;
 }
 
+// min_u32(a + b, c): VIADDMNMX.U32 (the late kill, one DPX op)
+__device__ __forceinline__ uint32_t addmin_u32(uint32_t a, uint32_t b, uint32_t c) { return __viaddmin_u32(a, b, c); }
+
 template <int G, int R, int FMT>
 struct Window {
     using RF = RegFmt<FMT>;
@@ -155,6 +168,7 @@ struct Window {
     static constexpr int W = G * R;
     static constexpr int GG = G;
     static constexpr uint32_t FM = (1u << CB) - 1u;
+    static constexpr bool ZON = fmt_z(FMT);
     static_assert(R >= 1 && R <= 32 && W <= 1024 && (G & (G - 1)) == 0, "window shape");
 
     int32_t E[R], O[R];
@@ -163,22 +177,23 @@ struct Window {
     int gl;            // lane within group
     unsigned gmask;
 
-    // One cell (eq. P:85 + the drop rule P:89) on threshold-relative values:
-    //   u = max(max(up, left, fg) + gap', diag + s'), then the exact kill
-    //   min_u32(u, DEAD): every negative u becomes DEAD, live values stay.
-    // The kernel is bound by the ALU pipe (VIMNMX3, VIADDMNMX, VIMNMX.U32 and
-    // the mismatch test live there), so diag + s' is computed on the FMA pipe:
-    // an IMAD by an opaque run-time 1 for the match case, overwritten by a
-    // predicated IMAD for a mismatch -- no SEL, no IADD3.
+    // RAW cell (eq. P:85) on values relative to T_{e-1}: up / left are killed
+    // values of e-1 (relative to T_{e-1}), diag a killed value of e-2; the
+    // diagonal term carries the rebase T_{e-2} - T_{e-1} inside sma / smi.
+    //   u' = max(max(up, left, fg) + gap, diag + s')   (fg = DEAD - gap: a floor)
+    // The kill is applied one antidiagonal later (kill_u).
     // Substitution-matrix cell: s = the table entry, sr = the diagonal rebase.
     __device__ __forceinline__ static int32_t cell_s(int32_t up, int32_t left, int32_t diag, int32_t s,
                                                      int32_t gp, int32_t fg, int32_t sr) {
         const int32_t t0 = __vimax3_s32(up, left, fg);
-        const int32_t u = __viaddmax_s32(t0, gp, diag + s + sr);
-        return (int32_t)min((uint32_t)u, DEADU);
+        return __viaddmax_s32(t0, gp, diag + s + sr);
     }
     const int8_t *tab;  // FMT_U8S: the substitution table in shared memory
 
+    // The kernel is bound by the ALU pipe (VIMNMX3, VIADDMNMX and the kill live
+    // there), so diag + s' is computed on the FMA pipe: an IMAD by an opaque
+    // run-time 1 for the match case, overwritten by a predicated IMAD for a
+    // mismatch -- no SEL, no IADD3.
     __device__ __forceinline__ static int32_t cell(int32_t up, int32_t left, int32_t diag, bool mis,
                                                    int32_t gp, int32_t fg, int32_t sma, int32_t smi,
                                                    int32_t one) {
@@ -187,8 +202,14 @@ struct Window {
         asm("mad.lo.s32 %0, %1, %2, %3;" : "=r"(dps) : "r"(diag), "r"(one), "r"(sma));
         asm("{\n\t.reg .pred q;\n\tsetp.ne.u32 q, %1, 0;\n\t@q mad.lo.s32 %0, %2, %3, %4;\n\t}"
             : "+r"(dps) : "r"((uint32_t)mis), "r"(diag), "r"(one), "r"(smi));
-        const int32_t u = __viaddmax_s32(t0, gp, dps);
-        return (int32_t)min((uint32_t)u, DEADU);
+        return __viaddmax_s32(t0, gp, dps);
+    }
+    // The late kill: a raw value of e relative to T_{e-1} becomes a killed value
+    // relative to T_e (dl = T_e - T_{e-1} >= 0): u = u' - dl if u' - dl >= 0,
+    // else a dead value in [DEAD - 3*127, DEAD] (every negative u' - dl >= DEAD
+    // maps to exactly DEAD; the floor fg keeps raw values >= DEAD).
+    __device__ __forceinline__ static int32_t kill_u(int32_t u, int32_t ndl) {
+        return (int32_t)addmin_u32((uint32_t)u, (uint32_t)ndl, DEADU);
     }
 
     // per-thread shared-memory slice used only by the (rare) window shifts
@@ -220,11 +241,14 @@ struct Window {
     __device__ __forceinline__ static void shift_up(uint32_t (&w)[NW], uint32_t in) {
 #pragma unroll
         for (int q = NW - 1; q > 0; --q) w[q] = __funnelshift_l(w[q - 1], w[q], CB);
-        w[0] = (NW == 1 ? (w[0] << CB) : (w[0] << CB)) | in;
-        if (RL < FPW) w[NW - 1] &= (1u << (CB * RL)) - 1u;
+        w[0] = (w[0] << CB) | in;
+        if (RL < FPW) w[NW - 1] &= (1u << (CB * (RL < FPW ? RL : 0))) - 1u;
     }
 
     // ---- task start -----------------------------------------------------------
+    // Pipelined state before step e = 1: raw antidiagonal 0 (the origin,
+    // relative to T_{-1} = -X: u' = X), killed antidiagonal -1 (all dead),
+    // nothing pending.
     __device__ __forceinline__ void init(const Params &P, uint32_t task) {
         const TaskDesc td = task_desc(P, task);
         st.task = task;
@@ -232,17 +256,18 @@ struct Window {
         st.n = td.b.len;
         st.d = 0;
         st.S0 = -(W / 2);
-        st.best = 0;
+        st.best = 0;  // best_{-2} := 0
         st.arg_i = st.arg_j = 0;
-        st.Tq[0] = -P.xdrop;  // T_0 = best_{-1} - X with best_{-1} := 0
-        st.Tq[1] = -P.xdrop;  // T_{-1}
-        st.Tn = -P.xdrop;     // T_1 = best_0 - X
-        st.sF[0] = st.sL[0] = 0;  // antidiagonal 0: the origin (slot 0)
-        st.sF[1] = EMPTY_F;       // antidiagonal -1: empty
+        st.Tq[0] = st.Tq[1] = -P.xdrop;  // T_{-1} = T_{-2} = 0 - X
+        st.K[0] = st.K[1] = KNONE;
+        st.KZ[0] = st.KZ[1] = KNONE;
+        st.dc[0] = st.dc[1] = 0;
+        st.sF[1] = EMPTY_F;  // antidiagonal -1: empty
         st.sL[1] = EMPTY_L;
+        st.sF[0] = EMPTY_F;  // antidiagonal 0: set by step 1's kill
+        st.sL[0] = EMPTY_L;
         st.cells = 0;
         st.shifts = 0;
-        // values: origin S(0,0) = 0 -> u = 0 - T_0 = X; everything else dead
         const int32_t s0 = st.S0 + gl * R;
 #pragma unroll
         for (int r = 0; r < R; ++r) {
@@ -273,33 +298,69 @@ struct Window {
         if (gl == 0) st.sb.seek(P, fh - st.S0 + 1);      // sb.idx = floor(d/2) - S0 + 1
     }
 
+    // ---- pending maxima -------------------------------------------------------
+    // Fold the pending key k of raw antidiagonal a (relative to threshold T, with
+    // the window base S0) into best: V = ku + T, a raise only on a strict
+    // increase, argmax = that slot (c-amb-8/9).
+    __device__ __forceinline__ void fold(int32_t k, int32_t T, int32_t a) {
+        if (k >= (st.best - T + 1) * KEYMUL) {  // the decode runs only on antidiagonals that raise best
+            const int32_t ku = k / KEYMUL;
+            st.best = ku + T;
+            st.arg_i = st.S0 + (1023 - (k - ku * KEYMUL)) + ceil_half(a);
+            st.arg_j = a - st.arg_i;
+        }
+    }
+    // Z-drop test (c-amb-19) of antidiagonal a with best = best_a already
+    // folded: kz = the pending in-matrix key of raw a (relative to T), live iff
+    // its value is >= Ta; stop if best - M_a > Z + |gap| * |(i_a - i*) - (j_a - j*)|.
+    // Every live M_a is >= Ta = best_{a-1} - X, so a stop needs M_a < best - Z
+    // (cheap pre-test first).
+    __device__ __forceinline__ bool zstop(const Params &P, int32_t kz, int32_t T, int32_t Ta, int32_t a) const {
+        if (kz < (Ta - T) * KEYMUL || kz >= (st.best - P.zdrop - T) * KEYMUL) return false;
+        const int32_t kzu = kz / KEYMUL;
+        const int32_t zi = st.S0 + (1023 - (kz - kzu * KEYMUL)) + ceil_half(a);
+        const int32_t off = abs((zi - st.arg_i) - ((a - zi) - st.arg_j));
+        return st.best - (kzu + T) > P.zdrop - P.gap * off;
+    }
+
     // ---- exact hand-over between levels ---------------------------------------
-    // A task whose band outgrows this window is written out after antidiagonal
-    // d (values of d and d-1 plus every scalar) and the next, wider level
-    // continues it from d + 1: cells outside the old window are dead (the band
-    // invariant), so the continuation is exact.
-    __device__ __forceinline__ void save(int32_t *rec) const {
+    // Called at the check point of an odd step e (after the kill of e-1, with
+    // e-1's pending raw maximum folded by the step): the canonical state after
+    // antidiagonal d = e - 1 is written (values of d and d-1, both killed;
+    // best = best_d), and the next, wider level continues it from d + 1: cells
+    // outside the old window are dead (the band invariant), so the continuation
+    // is exact. The value arrays are stored by parity (E, then O).
+    __device__ __forceinline__ void save(const Params &P, int32_t *rec) const {
+        const int32_t d = st.d;
+        const int p = d & 1;
 #pragma unroll
         for (int r = 0; r < R; ++r) {
             rec[REC_HDR + gl * R + r] = E[r];
             rec[REC_HDR + W + gl * R + r] = O[r];
         }
         if (gl == 0) {
-            rec[0] = (int32_t)st.task; rec[1] = st.d; rec[2] = st.S0; rec[3] = st.best;
-            const bool odd = st.d & 1;  // record order: d, then d-1
-            rec[4] = st.arg_i; rec[5] = st.arg_j; rec[6] = st.Tn;
-            rec[7] = odd ? st.Tq[1] : st.Tq[0];
-            rec[8] = odd ? st.Tq[0] : st.Tq[1];
-            rec[9] = odd ? st.sF[1] : st.sF[0];
-            rec[10] = odd ? st.sL[1] : st.sL[0];
-            rec[11] = odd ? st.sF[0] : st.sF[1];
-            rec[12] = odd ? st.sL[0] : st.sL[1];
+            rec[0] = (int32_t)st.task; rec[1] = d; rec[2] = st.S0; rec[3] = st.best;
+            rec[4] = st.arg_i; rec[5] = st.arg_j;
+            // (parity-indexed state through selects: a run-time index would put
+            // the arrays in local memory)
+            rec[6] = st.best - P.xdrop;                       // T_{d+1}
+            rec[7] = p ? st.Tq[1] : st.Tq[0];                 // T_d
+            rec[8] = p ? st.Tq[0] : st.Tq[1];                 // T_{d-1}
+            rec[9] = p ? st.sF[1] : st.sF[0];                 // extremes of d
+            rec[10] = p ? st.sL[1] : st.sL[0];
+            rec[11] = p ? st.sF[0] : st.sF[1];                // extremes of d-1
+            rec[12] = p ? st.sL[0] : st.sL[1];
             rec[13] = 0;
             rec[14] = (int32_t)st.shifts; rec[15] = W;
             rec[16] = (int32_t)(uint32_t)st.cells; rec[17] = (int32_t)(uint32_t)(st.cells >> 32);
         }
     }
 
+    // Resume from the canonical record after antidiagonal d into the pipelined
+    // state before step e = d + 1: killed d is re-expressed as raw relative to
+    // T_{d-1} (u + T_d - T_{d-1}; the late kill at step e restores it exactly),
+    // best := best_{d-1} = T_d + X, and a raise on d (best_d > best_{d-1}, at the
+    // recorded argmax, which then lies on d) is re-issued as d's pending key.
     __device__ __forceinline__ void resume(const Params &P, const int32_t *rec) {
         st.task = (uint32_t)rec[0];
         const TaskDesc td = task_desc(P, st.task);
@@ -307,97 +368,197 @@ struct Window {
         st.n = td.b.len;
         st.sa.s = td.a;
         st.sb.s = td.b;
-        st.d = rec[1];
+        const int32_t d = rec[1];
+        st.d = d;
         const int32_t S0src = rec[2];
-        st.best = rec[3]; st.arg_i = rec[4]; st.arg_j = rec[5];
-        const bool odd = st.d & 1;
-        st.Tn = rec[6];
-        st.Tq[0] = odd ? rec[8] : rec[7];
-        st.Tq[1] = odd ? rec[7] : rec[8];
-        st.sF[0] = odd ? rec[11] : rec[9];
-        st.sF[1] = odd ? rec[9] : rec[11];
-        st.sL[0] = odd ? rec[12] : rec[10];
-        st.sL[1] = odd ? rec[10] : rec[12];
+        const int32_t best_d = rec[3];
+        st.arg_i = rec[4]; st.arg_j = rec[5];
+        const int32_t Td = rec[7], Td1 = rec[8];
+        const int p = d & 1;
+        st.Tq[0] = st.Tq[1] = Td1;  // T_{e-2} = T_{d-1}; T_{e-3} only decodes K[1-p] = KNONE
+        st.best = Td + P.xdrop;     // best_{d-1}
+        st.sF[0] = p ? rec[11] : rec[9];
+        st.sL[0] = p ? rec[12] : rec[10];
+        st.sF[1] = p ? rec[9] : rec[11];
+        st.sL[1] = p ? rec[10] : rec[12];
         st.shifts = (uint32_t)rec[14];
         const int32_t Wsrc = rec[15];
         st.cells = (uint64_t)(uint32_t)rec[16] | ((uint64_t)(uint32_t)rec[17] << 32);
         st.cells_entry = st.cells;
+        st.KZ[0] = st.KZ[1] = KNONE;
+        st.dc[0] = st.dc[1] = 0;
         // centre the wider window on the live band of d and d-1
         int32_t Fm = min(st.sF[0], st.sF[1]), Lm = max(st.sL[0], st.sL[1]);
         if (Fm > Lm) { Fm = S0src; Lm = S0src + Wsrc - 1; }
         st.S0 = ((Fm + Lm) >> 1) - W / 2;
+        const int32_t kd = best_d > st.best
+                               ? (best_d - Td1) * KEYMUL + (1023 - (st.arg_i - ceil_half(d) - st.S0)) : KNONE;
+        st.K[0] = p ? KNONE : kd;
+        st.K[1] = p ? kd : KNONE;
+        const int32_t rb = Td - Td1;  // killed d (relative to T_d) as raw relative to T_{d-1}
         const int32_t s0 = st.S0 + gl * R;
 #pragma unroll
         for (int r = 0; r < R; ++r) {
             const int32_t q = s0 + r - S0src;
             const bool in = q >= 0 && q < Wsrc;
-            E[r] = in ? rec[REC_HDR + q] : DEAD;
-            O[r] = in ? rec[REC_HDR + Wsrc + q] : DEAD;
+            const int32_t ve = in ? rec[REC_HDR + q] : DEAD;         // even array
+            const int32_t vo = in ? rec[REC_HDR + Wsrc + q] : DEAD;  // odd array
+            E[r] = p == 0 ? ve + rb : ve;
+            O[r] = p == 1 ? vo + rb : vo;
         }
         load_bases(P);
     }
 
-    // ---- one antidiagonal d = st.d + 1 of parity PAR ---------------------------
-    // returns 0 = continue, 1 = finished, 2 = overflow
+    // ---- one pipelined step: antidiagonal e = st.d + 1 of parity PAR ----------
+    // (a) fold the pending raw maximum of e-2 -> best_{e-2}, T_{e-1};
+    // (b) kill e-1 with T_{e-1} (its live extremes);
+    // (c) odd e only: termination (e-1 and e-2 empty) and the window check;
+    // (d) the band cells of e; (e) bases of e; (f) raw e; (g) its maximum,
+    // left pending (reduced across the group while the next step runs).
+    // Returns 0 = continue, 1 = finished, 2 = overflow (hand over).
     template <int PAR>
-    __device__ __forceinline__ int step(const Params &P) {
-        const int32_t d = st.d + 1;
-        const int32_t ch = PAR ? (d + 1) >> 1 : d >> 1, fh = PAR ? (d - 1) >> 1 : d >> 1;
+    __device__ __forceinline__ int step(const Params &P, bool force) {
+        const int32_t e = st.d + 1;
+        constexpr int Q = 1 - PAR;  // parity of e-1 (array E for odd e, O for even e)
 
-        // (1) band cells of antidiagonal d from the live extremes of d-1, d-2
-        //     (c-amb-14: lo = max(1, d-n, min(F1, F2+1)), hi = min(m, d-1, max(L1, L2)+1))
-        //     Empty antidiagonals carry EMPTY_F / EMPTY_L and drop out of the
-        //     min / max; d = 1 clips to an empty band by itself.
+        // (a) best_{e-2} from the raw maximum of e-2 (relative to T_{e-3} = Tq[Q])
+        fold(st.K[PAR], st.Tq[Q], e - 2);
+        st.K[PAR] = KNONE;
+        const int32_t T1 = st.best - P.xdrop;  // T_{e-1}
+        const int32_t T2 = st.Tq[PAR];         // T_{e-2}
+        if (ZON && P.zdrop >= 0) {
+            if (zstop(P, st.KZ[PAR], st.Tq[Q], T2, e - 2)) {
+                st.cells -= st.dc[Q];  // the sweep ends after e-2: e-1's band was counted already
+                return 1;
+            }
+            st.KZ[PAR] = KNONE;
+        }
+        const int32_t dl = T1 - T2;  // >= 0
+
+        // (b) late kill of e-1 (dead iff S < best_{e-2} - X), sign masks
+        constexpr int NCH = LOGAN_NCHAIN;  // independent dead-mask chains per lane
+        constexpr int RQ = (R + NCH - 1) / NCH;
+        uint32_t dq[NCH];
+#pragma unroll
+        for (int r = R - 1; r >= 0; --r) {
+            int32_t u;
+            if (PAR) { u = kill_u(E[r], -dl); E[r] = u; }
+            else { u = kill_u(O[r], -dl); O[r] = u; }
+            const int c = r / RQ;
+            const bool top = (r == R - 1) || (r == (c + 1) * RQ - 1);
+            dq[c] = top ? ((uint32_t)u >> 31) : __funnelshift_l((uint32_t)u, dq[c], 1);
+        }
+        uint32_t dead = 0;
+#pragma unroll
+        for (int c = 0; c < NCH; ++c)
+            if (c * RQ < R) dead |= dq[c] << (c * RQ);
         {
-            // column of slot 0 on d-1 (c1) and d-2 (c2 = c1 - 1 + PAR), so with
-            // c = c1: odd d: lo = max(min(F1, F2 + 1) + c, 1, d-n), hi = min(max(L1, L2) + c + 1, m, d-1);
-            // even d: lo = max(min(F1, F2) + c, 1, d-n), hi = min(max(L1, L2 - 1) + c + 1, m, d-1)
-            // (3-input DPX min / max; d-1 has the other parity, d-2 this parity)
-            const int32_t c = PAR ? (d - 1) >> 1 : d >> 1;
-            const int32_t F1 = st.sF[1 - PAR], F2 = st.sF[PAR], L1 = st.sL[1 - PAR], L2 = st.sL[PAR];
-            const int32_t fmin = PAR ? min(F1, F2 + 1) : min(F1, F2);
-            const int32_t lmax = PAR ? max(L1, L2) : max(L1, L2 - 1);
-            const int32_t lo = __vimax3_s32(fmin + c, 1, d - st.n);
-            const int32_t hi = __vimin3_s32(lmax + c + 1, st.m, d - 1);
-            st.cells += (uint32_t)__vimax_s32_relu(hi - lo + 1, 0);
+            // validity of slots on e-1: i <= m <=> s <= m - ceil((e-1)/2),
+            // j <= n <=> s >= floor((e-1)/2) - n (cells with i < 0 or j < 0 are
+            // dead by construction)
+            const int32_t chq = e >> 1, fhq = (e - 1) >> 1;  // ceil((e-1)/2), floor((e-1)/2)
+            const int32_t vlo = fhq - st.n, vhi = st.m - chq;
+            const int32_t base = st.S0 + gl * R;
+            uint32_t vmask = (R == 32) ? 0xffffffffu : ((1u << R) - 1u);
+            if (vlo > base || vhi < base + R - 1) {
+                const int32_t rlo = max(vlo - base, 0), rhi = min(vhi - base, R - 1);
+                vmask = (rlo <= rhi) ? ((0xffffffffu >> (31 - rhi)) & ~((1u << rlo) - 1u)) : 0u;
+            }
+            const uint32_t live = ~dead & vmask;
+            if (G == 1) {  // one lane per task: extremes only read when live != 0
+                const bool h = live != 0;
+                st.sF[Q] = h ? base + __ffs(live) - 1 : EMPTY_F;
+                st.sL[Q] = h ? base + 31 - __clz(live) : EMPTY_L;
+            } else {
+                int32_t lf = live ? gl * R + __ffs(live) - 1 : INT32_MAX;
+                int32_t ll = live ? gl * R + 31 - __clz(live) : INT32_MIN;
+                lf = grp_min<G>(lf, gmask);
+                ll = grp_max<G>(ll, gmask);
+                const bool h = lf != INT32_MAX;
+                st.sF[Q] = h ? st.S0 + lf : EMPTY_F;
+                st.sL[Q] = h ? st.S0 + ll : EMPTY_L;
+            }
+        }
+        st.Tq[Q] = T1;
+
+        // (c) after an even antidiagonal e-1 (odd e): termination -- antidiagonals
+        // e-1 and e-2 both empty (c-amb-7); best_{e-2} is final (a raw
+        // value of e-1 above best_{e-2} would have been live) -- and the window:
+        // the band's right edge can grow (by one slot) only on even antidiagonals
+        // and its left edge only on odd ones, so the margin-1 invariant checked
+        // here keeps every cell outside the window dead through the next two.
+        if (PAR == 1) {
+            if (st.sF[0] == EMPTY_F && st.sF[1] == EMPTY_F) return 1;
+            bool ho = force;  // force: test knob (options.handover)
+            if (!ho) {
+                // keep the live band of e-1 and e-2 inside [S0+1, S0+W-2]
+                const int32_t Fm = min(st.sF[0], st.sF[1]), Lm = max(st.sL[0], st.sL[1]);
+                const bool lowv = Fm < st.S0 + 1, highv = Lm > st.S0 + W - 2;
+                if (lowv || highv) {
+                    if (lowv && highv) ho = true;
+                    else if (lowv) {
+                        if (Lm > st.S0 + W - 3) ho = true;
+                        else shift_left(P, e - 1);
+                    } else {
+                        if (Fm < st.S0 + 2) ho = true;
+                        else shift_right(P, e - 1);
+                    }
+                }
+            }
+            if (ho) {  // hand over the canonical state after e-1 (save): fold e-1's maximum
+                fold(st.K[Q], T2, e - 1);
+                st.K[Q] = KNONE;
+                if (ZON && P.zdrop >= 0 && zstop(P, st.KZ[Q], T2, T1, e - 1)) return 1;
+                return 2;
+            }
         }
 
-        // (2) bases for antidiagonal d
+        // (d) band cells of e from the live extremes of e-1, e-2 (c-amb-14:
+        //     lo = max(1, e-n, min(F1, F2+1)), hi = min(m, e-1, max(L1, L2)+1)).
+        //     Empty antidiagonals carry EMPTY_F / EMPTY_L and drop out of the
+        //     min / max; e = 1 clips to an empty band by itself.
+        {
+            // column of slot 0 on e-1 (c1) and e-2 (c2 = c1 - 1 + PAR), so with
+            // c = c1: odd e: lo = max(min(F1, F2 + 1) + c, 1, e-n), hi = min(max(L1, L2) + c + 1, m, e-1);
+            // even e: lo = max(min(F1, F2) + c, 1, e-n), hi = min(max(L1, L2 - 1) + c + 1, m, e-1)
+            const int32_t c = PAR ? (e - 1) >> 1 : e >> 1;
+            const int32_t F1 = st.sF[Q], F2 = st.sF[PAR], L1 = st.sL[Q], L2 = st.sL[PAR];
+            const int32_t fmin = PAR ? min(F1, F2 + 1) : min(F1, F2);
+            const int32_t lmax = PAR ? max(L1, L2) : max(L1, L2 - 1);
+            const int32_t lo = __vimax3_s32(fmin + c, 1, e - st.n);
+            const int32_t hi = __vimin3_s32(lmax + c + 1, st.m, e - 1);
+            const uint32_t nc = (uint32_t)__vimax_s32_relu(hi - lo + 1, 0);
+            st.cells += nc;
+            if (ZON) st.dc[PAR] = nc;
+        }
+
+        // (e) bases for antidiagonal e
         if (PAR == 1) {  // i advances: A fields move down one slot
             uint32_t in = 0;
             if (G > 1) in = __shfl_down_sync(gmask, Aw[0], 1, G) & FM;
-            // one or two lanes per task: many lanes of the warp read a stream, so its
-            // refill is predicated; wider groups have few readers per warp: branch
-            if (gl == G - 1) in = RF::fa(G <= 2 ? st.sa.next_fast(RF::SA) : st.sa.next(P, RF::SA));
+            const uint32_t x = RF::fa(st.sa.next_fast(RF::SA));
+            if (gl == G - 1) in = x;
             shift_down(Aw, in);
         } else {         // j advances: B fields move up one slot
             uint32_t in = 0;
             if (G > 1) in = __shfl_up_sync(gmask, top_field(Bw), 1, G);
-            if (gl == 0) in = RF::fb(G <= 2 ? st.sb.next_fast(RF::SB) : st.sb.next(P, RF::SB));
+            const uint32_t x = RF::fb(st.sb.next_fast(RF::SB));
+            if (gl == 0) in = x;
             shift_up(Bw, in);
         }
 
-        // (3) rebased constants (T_d = st.Tn is this step's threshold; T_{d-1} is
-        //     the other parity's, T_{d-2} this parity's)
-        const int32_t Tc = st.Tn;
-        const int32_t gp = P.gap - (Tc - st.Tq[1 - PAR]);
-        const int32_t sma = P.match - (Tc - st.Tq[PAR]);
-        const int32_t smi = P.mismatch - (Tc - st.Tq[PAR]);
+        // (f) raw cells of e, relative to T_{e-1}: up / left from killed e-1,
+        //     diag from killed e-2 rebased by -(T_{e-1} - T_{e-2}) = -dl
+        const int32_t gp = P.gap;
+        const int32_t sma = P.match - dl;
+        const int32_t smi = P.mismatch - dl;
         const int32_t fg = DEAD - gp;  // max(up, left, fg) + gp >= DEAD: the floor
-
-        const uint32_t two = 2u * (uint32_t)P.one;  // = 2, opaque to the compiler
         constexpr bool SUB = fmt_base(FMT) == FMT_U8S;
-        const int32_t sr = -(Tc - st.Tq[PAR]);  // diagonal rebase (SUB: s' = table entry + sr)
+        const int32_t sr = -dl;        // diagonal rebase (SUB: s' = table entry + sr)
         uint32_t X[NW];
 #pragma unroll
         for (int q = 0; q < NW; ++q) X[q] = SUB ? Aw[q] + Bw[q] : Aw[q] ^ Bw[q];  // SUB: two table indices
-
-        // (4) cells
-        constexpr int NCH = LOGAN_NCHAIN;  // independent key / dead-mask chains per lane
-        int32_t kq[NCH];
-        uint32_t dq[NCH];
-        constexpr int RQ = (R + NCH - 1) / NCH;
-        if (PAR == 1) {
+        if (PAR == 1) {  // odd e: up = E[s+1], left = E[s], diag = O[s]
             int32_t nb = DEAD;  // E[R] of this lane = E[0] of the next lane
             if (G > 1) {
                 nb = __shfl_down_sync(gmask, E[0], 1, G);
@@ -413,7 +574,7 @@ struct Window {
                     O[r] = cell(up, E[r], O[r], mis, gp, fg, sma, smi, P.one);
                 }
             }
-        } else {
+        } else {         // even e: up = O[s], left = O[s-1], diag = E[s]
             int32_t nb = DEAD;  // O[-1] of this lane = O[R-1] of the previous lane
             if (G > 1) {
                 nb = __shfl_up_sync(gmask, O[R - 1], 1, G);
@@ -430,125 +591,52 @@ struct Window {
                 }
             }
         }
-        // keys u * KEYMUL + 1023 - r and dead masks over the new antidiagonal
+
+        // (g) the maximum of raw e (key u' * KEYMUL + 1023 - slot), pending until
+        //     step e + 2; any raw value above best_{e-1} is live (it is >= T_e)
+        int32_t kq[NCH];
 #pragma unroll
         for (int r = R - 1; r >= 0; --r) {
-            const int32_t u = PAR ? O[r] : E[r];
+            const int32_t key = (PAR ? O[r] : E[r]) * KEYMUL + (1023 - r);
             const int c = r / RQ;
-            const bool top = (r == R - 1) || (r == (c + 1) * RQ - 1);  // first slot of chain c
-            const int32_t key = u * KEYMUL + (1023 - r);
+            const bool top = (r == R - 1) || (r == (c + 1) * RQ - 1);
             kq[c] = top ? key : max(kq[c], key);
-            if (LOGAN_MASK_FMA_CHAINS > c) {  // two IMADs on the FMA pipe
-                // append sign(u) (1 = dead) as bit (r - c*RQ): dq = 2*dq + (u >>> 31)
-                uint32_t sg;
-                asm("mul.hi.u32 %0, %1, %2;" : "=r"(sg) : "r"((uint32_t)u), "r"(two));
-                if (top) dq[c] = sg;
-                else asm("mad.lo.u32 %0, %1, %2, %3;" : "=r"(dq[c]) : "r"(dq[c]), "r"(two), "r"(sg));
-            } else {  // one funnel shift on the ALU pipe (same bit order)
-                dq[c] = top ? ((uint32_t)u >> 31) : __funnelshift_l((uint32_t)u, dq[c], 1);
-            }
         }
         int32_t kmax = kq[0];
 #pragma unroll
         for (int c = 1; c < NCH; ++c)
             if (c * RQ < R) kmax = max(kmax, kq[c]);
-        uint32_t dead = 0;
-#pragma unroll
-        for (int c = 0; c < NCH; ++c)
-            if (c * RQ < R) dead |= dq[c] << (c * RQ);
-
-        // (5) validity of slots for this lane: cells with i < 0 or j < 0 are dead
-        //     by construction; cells past the matrix (i > m or j > n) are masked
-        //     out of the band bookkeeping (slot s: i <= m <=> s <= m - ch,
-        //     j <= n <=> s >= fh - n). Most steps take the all-valid path.
-        const int32_t vlo = fh - st.n, vhi = st.m - ch;
-        const int32_t base = st.S0 + gl * R;
-        uint32_t vmask = (R == 32) ? 0xffffffffu : ((1u << R) - 1u);
-        if (vlo > base || vhi < base + R - 1) {
-            const int32_t rlo = max(vlo - base, 0), rhi = min(vhi - base, R - 1);
-            vmask = (rlo <= rhi) ? ((0xffffffffu >> (31 - rhi)) & ~((1u << rlo) - 1u)) : 0u;
-        }
-        const uint32_t live = ~dead & vmask;
-        // one lane per task: the extremes are only read when live != 0, so no
-        // sentinel selects (a sub-warp or warp group reduces with sentinels)
-        int32_t lf = G == 1 ? __ffs(live) - 1 : (live ? gl * R + __ffs(live) - 1 : INT32_MAX);
-        int32_t ll = G == 1 ? 31 - __clz(live) : (live ? gl * R + 31 - __clz(live) : INT32_MIN);
-        kmax = kmax - gl * R;  // key = u*KEYMUL + 1023 - (gl*R + r)
+        kmax -= gl * R;  // key = u' * KEYMUL + 1023 - (gl * R + r)
         // Z-drop (c-amb-19) needs the max over in-matrix cells only: cells past
         // the matrix stay below an earlier best (harmless for best) but can top
         // an antidiagonal; near the matrix edges the key is recomputed masked
         int32_t kz = kmax;
-        const bool zon = fmt_z(FMT) && P.zdrop >= 0;
-        if (zon && vmask != ((R == 32) ? 0xffffffffu : ((1u << R) - 1u))) {
-            kz = INT32_MIN / 2;  // no valid slot (the offset below must not wrap)
+        if (ZON && P.zdrop >= 0) {
+            const int32_t ch = (e + 1) >> 1, fh = e >> 1;
+            const int32_t vlo = fh - st.n, vhi = st.m - ch;
+            const int32_t base = st.S0 + gl * R;
+            if (vlo > base || vhi < base + R - 1) {
+                kz = INT32_MIN / 2;  // no valid slot (the offset below must not wrap)
 #pragma unroll
-            for (int r = 0; r < R; ++r)
-                if ((vmask >> r) & 1u) kz = max(kz, (PAR ? O[r] : E[r]) * KEYMUL + (1023 - r));
-            kz -= gl * R;
+                for (int r = 0; r < R; ++r) {
+                    const int32_t s = base + r;
+                    if (s >= vlo && s <= vhi) kz = max(kz, (PAR ? O[r] : E[r]) * KEYMUL + (1023 - r));
+                }
+                kz -= gl * R;
+            }
         }
         if (G > 1) {
             kmax = grp_max<G>(kmax, gmask);
-            lf = grp_min<G>(lf, gmask);
-            ll = grp_max<G>(ll, gmask);
-            if (zon) kz = grp_max<G>(kz, gmask);
+            if (ZON && P.zdrop >= 0) kz = grp_max<G>(kz, gmask);
         }
-        const bool h = G == 1 ? live != 0 : (lf != INT32_MAX);
-
-        // (6) best after the complete antidiagonal; argmax on strict increase
-        // V = u + T_d > best_{d-1} = T_d + X  <=>  u > X  <=>  kmax >= (X + 1) * KEYMUL:
-        // the key decode runs only on antidiagonals that raise best
-        if (kmax >= (P.xdrop + 1) * KEYMUL) {
-            const int32_t ku = kmax / KEYMUL;
-            st.best = ku + Tc;
-            const int32_t slot = st.S0 + (1023 - (kmax - ku * KEYMUL));
-            st.arg_i = slot + ch;
-            st.arg_j = d - st.arg_i;
-        }
-        // Z-drop stop (c-amb-19): best - M_d > Z + |gap| * |(i_d - i*) - (j_d - j*)|
-        // Every live u is >= 0 and best >= T_d + X, so a stop needs u_max < X - Z on
-        // this antidiagonal: key below (X - Z) * KEYMUL (cheap test first; an
-        // antidiagonal that raised best has u_max > X and never stops)
-        bool zstop = false;
-        if (zon && kz >= 0 && kz < (P.xdrop - P.zdrop) * KEYMUL) {
-            const int32_t kzu = kz / KEYMUL;
-            const int32_t zi = st.S0 + (1023 - (kz - kzu * KEYMUL)) + ch;
-            const int32_t off = abs((zi - st.arg_i) - ((d - zi) - st.arg_j));
-            zstop = st.best - (kzu + Tc) > P.zdrop - P.gap * off;
-        }
-        st.Tq[PAR] = Tc;
-        st.Tn = st.best - P.xdrop;
-        st.d = d;
-
-        st.sF[PAR] = h ? st.S0 + lf : EMPTY_F;
-        st.sL[PAR] = h ? st.S0 + ll : EMPTY_L;
-        // The checks below run after the even antidiagonal only. The band's
-        // right edge can grow (by one slot) only on even steps and its left
-        // edge only on odd steps, so the margin-1 invariant checked here keeps
-        // every cell outside the window dead through both steps of the next
-        // iteration. An odd antidiagonal that ends the task is followed by one
-        // extra even one whose band is empty: no cells, no best change.
-        if (PAR == 1) return zstop ? 1 : 0;
-
-        // (7) termination: antidiagonals d and d-1 both empty (c-amb-7), or Z-drop
-        if (zstop || (st.sF[0] == EMPTY_F && st.sF[1] == EMPTY_F)) return 1;
-
-        // (8) keep the live band of d and d-1 inside [S0+1, S0+W-2]
-        const int32_t Fm = min(st.sF[0], st.sF[1]), Lm = max(st.sL[0], st.sL[1]);
-        const bool lowv = Fm < st.S0 + 1, highv = Lm > st.S0 + W - 2;
-        if (lowv || highv) {
-            if (lowv && highv) return 2;
-            if (lowv) {
-                if (Lm > st.S0 + W - 3) return 2;
-                shift_left(P, d);
-            } else {
-                if (Fm < st.S0 + 2) return 2;
-                shift_right(P, d);
-            }
-        }
+        st.K[PAR] = kmax;
+        if (ZON) st.KZ[PAR] = kz;
+        st.d = e;
         return 0;
     }
 
-    // window slot base S0 += 1 (band drifted towards higher slots)
+    // window slot base S0 += 1 (band drifted towards higher slots); the pending
+    // raw maximum of antidiagonal d (keys count slots from S0) moves with it
     __device__ __forceinline__ void shift_right(const Params &P, int32_t d) {
         int32_t eIn = DEAD, oIn = DEAD;
         uint32_t aIn = 0, bIn = 0;
@@ -577,6 +665,7 @@ struct Window {
         shift_down(Aw, aIn);
         shift_down(Bw, bIn);
         st.S0 = S1;
+        adjust_pending(d, +1);
         ++st.shifts;
     }
 
@@ -606,22 +695,47 @@ struct Window {
         shift_up(Aw, aIn);
         shift_up(Bw, bIn);
         st.S0 = S1;
+        adjust_pending(d, -1);
         ++st.shifts;
+    }
+
+    // The raw maximum of antidiagonal d (parity d&1) is still pending at a shift:
+    // a slot index s becomes s - by, so the key's 1023 - s part grows by `by`.
+    // (A raising maximum is a live cell inside the band, so it stays in 0..W-1;
+    // a non-raising one is never decoded.)
+    __device__ __forceinline__ void adjust_pending(int32_t d, int32_t by) {
+        const bool p = d & 1;
+        const int32_t k = p ? st.K[1] : st.K[0];
+        const int32_t kn = k != KNONE ? k + by : k;
+        st.K[0] = p ? st.K[0] : kn;
+        st.K[1] = p ? kn : st.K[1];
+        if (ZON) {
+            const int32_t z = p ? st.KZ[1] : st.KZ[0];
+            const int32_t zn = z != KNONE ? z + by : z;
+            st.KZ[0] = p ? st.KZ[0] : zn;
+            st.KZ[1] = p ? zn : st.KZ[1];
+        }
     }
 };
 
 // Runs one group's task loop. `fetch(pos&)` yields the next list position (or
 // false when there is none); the loop starts or resumes that task, sweeps it to
 // completion or hand-over, and writes the result / publishes the hand-over.
+// gpu-scope relaxed load (a volatile load compiles to a system-scope strong one)
+__device__ __forceinline__ uint32_t ld_relaxed(const uint32_t *p) {
+    uint32_t v;
+    asm volatile("ld.relaxed.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+    return v;
+}
+
 template <class Win, class Fetch>
 __device__ __forceinline__ void run_group(Win &w, const Params &P, const LevelIO &io, Fetch fetch) {
     constexpr int G = Win::GG;
     const int lane = threadIdx.x & 31;
     const int leader = lane - w.gl;
-    // start or resume the next task; a task resumed after an odd antidiagonal
-    // takes the even one here, so the hot loop below always starts at an even d
-    // (a single code path: no per-iteration register shuffling). `rc` returns
-    // the outcome of that alignment step (0 = keep sweeping).
+    // start or resume the next task; the hot loop below always starts with an odd
+    // antidiagonal (a task resumed after an odd one takes the even one here), so
+    // it has a single code path. `rc` returns the outcome of that step (0 = go on).
     auto next_task = [&](int &rc) -> bool {
         rc = 0;
         uint32_t pos;
@@ -634,7 +748,7 @@ __device__ __forceinline__ void run_group(Win &w, const Params &P, const LevelIO
             atomicAdd((unsigned long long *)&io.stats->tasks_started[io.level], 1ull);
             if (io.is_helper) atomicAdd((unsigned long long *)&io.stats->helper_tasks, 1ull);
         }
-        if (w.st.d & 1) rc = w.template step<0>(P);
+        if (w.st.d & 1) rc = w.template step<0>(P, false);
         return true;
     };
 
@@ -644,12 +758,11 @@ __device__ __forceinline__ void run_group(Win &w, const Params &P, const LevelIO
     while (active) {
         // one iteration = the odd then the even antidiagonal
         if (rc == 0) {
-            rc = w.template step<1>(P);
-            if (rc == 0) rc = w.template step<0>(P);
-        }
-        if (io.handover > 0) {  // test knob (uniform branch, off in production)
+            // test knob (uniform, off in production): hand over at the next check point
+            const bool force = io.handover > 0 && io.rec_out && since >= io.handover;
+            rc = w.template step<1>(P, force);
+            if (rc == 0) rc = w.template step<0>(P, false);
             since += 2;
-            if (rc == 0 && io.rec_out && since >= io.handover) rc = 2;
         }
         if (rc != 0) {
             uint32_t rec = NO_REC;
@@ -659,7 +772,7 @@ __device__ __forceinline__ void run_group(Win &w, const Params &P, const LevelIO
                     if (rec >= io.rec_out_cap) rec = NO_REC;  // pool full: the next level restarts it
                 }
                 if (G > 1) rec = __shfl_sync(w.gmask, rec, leader);
-                if (rec != NO_REC) w.save(io.rec_out + (size_t)rec * io.rec_out_stride);
+                if (rec != NO_REC) w.save(P, io.rec_out + (size_t)rec * io.rec_out_stride);
                 if (G > 1) __syncwarp(w.gmask);
             }
             if (w.gl == 0) {
@@ -696,6 +809,7 @@ __device__ __forceinline__ void run_group(Win &w, const Params &P, const LevelIO
         }
     }
 }
+
 
 // Persistent kernel: each group of G lanes pulls tasks from the level's list.
 // A level may exist in two shapes (throughput: G small, R = 32; latency: one
@@ -740,8 +854,8 @@ __global__ void __launch_bounds__(128, (G == 1 ? ((fmt_z(FMT) || fmt_base(FMT) =
         // goes to the next level's own launch (throughput shape if many).
         auto fetch = [&](uint32_t &pos) -> bool {
             for (;;) {  // take a new entry only while producers are running
-                if (*(volatile const uint32_t *)io.done == total) return false;
-                if (*(volatile const uint32_t *)hio.cursor < *(volatile const uint32_t *)io.out_count) break;
+                if (ld_relaxed(io.done) == total) return false;
+                if (ld_relaxed(hio.cursor) < ld_relaxed(io.out_count)) break;
                 __nanosleep(1000);
             }
             uint32_t p = 0;
@@ -749,15 +863,15 @@ __global__ void __launch_bounds__(128, (G == 1 ? ((fmt_z(FMT) || fmt_base(FMT) =
             if (HG_ > 1) p = __shfl_sync(w.gmask, p, leader);
             // a claimed position is either processed here or proven not to exist
             for (;;) {
-                if (p < *(volatile const uint32_t *)io.out_count) break;
-                if (*(volatile const uint32_t *)io.done == total) {
+                if (p < ld_relaxed(io.out_count)) break;
+                if (ld_relaxed(io.done) == total) {
                     __threadfence();
-                    if (p >= *(volatile const uint32_t *)io.out_count) return false;
+                    if (p >= ld_relaxed(io.out_count)) return false;
                     break;
                 }
                 __nanosleep(500);
             }
-            while (*(volatile const uint32_t *)&io.out_list[p] == NO_TASK) __nanosleep(64);
+            while (ld_relaxed(&io.out_list[p]) == NO_TASK) __nanosleep(64);
             __threadfence();
             pos = p;
             return true;
