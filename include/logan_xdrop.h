@@ -106,6 +106,8 @@ enum {
  *                  bit 2 = Z-drop on, threshold `zdrop` (0 <= zdrop <= 2^28).
  *                  bit 3 = run the first level in its throughput shape even
  *                  when the batch has few tasks (test / tuning knob; bit 0 wins).
+ *                  bit 4 = test / A-B knob: the first window of a 2-bit pool
+ *                  runs on int32 values instead of packed int16 pairs.
  *                  bit 1 = test knob: the band level fills its shared-memory
  *                  code buffers with garbage before each task, so the tests
  *                  see the worst case of stale shared memory. Results never

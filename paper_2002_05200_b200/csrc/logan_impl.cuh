@@ -10,6 +10,7 @@
 #include "xdrop_band.cuh"
 #include "xdrop_wide.cuh"
 #include "xdrop_window.cuh"
+#include "xdrop_window16.cuh"
 
 namespace logan {
 
@@ -214,12 +215,12 @@ static __global__ void k_combine(const Params P, const TaskRes *tres, logan_resu
 #define LOGAN_HSHAPE(W) 32, ((W) / 32)
 #endif
 
-template <int G, int R, int FMT, int HG, int HR>
+template <int G, int R, int FMT, int HG, int HR, bool PK = false>
 static cudaError_t launch_win(const Params &P, const LevelIO &io_in, const LevelIO &hio, int sms, cudaStream_t s) {
     constexpr int S1 = Window<G, R, FMT>::SB_STRIDE;
     constexpr int S2 = HR > 0 ? Window<(HG > 0 ? HG : 32), (HR > 0 ? HR : 1), FMT>::SB_STRIDE : 0;
     const size_t smem = 128 * sizeof(int32_t) * (S1 > S2 ? S1 : S2) + (fmt_base(FMT) == FMT_U8S ? SUBST_TAB_BYTES : 0);
-    auto kern = k_window<G, R, FMT, HG, HR>;
+    auto kern = k_window<G, R, FMT, HG, HR, PK>;
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return e;
     int occ = 0;
@@ -243,6 +244,23 @@ static cudaError_t launch_win(const Params &P, const LevelIO &io_in, const Level
 template <int FMT>
 static cudaError_t launch_first(int w0, bool helpers, const Params &P, const LevelIO &io, const LevelIO &hio,
                                 int sms, cudaStream_t s) {
+    // 2-bit pools (no Z-drop) at X <= 16000: the packed int16 window (xdrop_window16.cuh)
+    if constexpr (FMT == LOGAN_SEQ_2BIT) {
+        if (P.xdrop <= PACK_XMAX && !P.nopack) {
+            switch (w0) {
+                case 16: return helpers ? launch_win<1, 16, FMT, LOGAN_HSHAPE(64), true>(P, io, hio, sms, s)
+                                        : launch_win<1, 16, FMT, 0, 0, true>(P, io, hio, sms, s);
+                case 20: return helpers ? launch_win<1, 20, FMT, LOGAN_HSHAPE(64), true>(P, io, hio, sms, s)
+                                        : launch_win<1, 20, FMT, 0, 0, true>(P, io, hio, sms, s);
+                case 24: return helpers ? launch_win<1, 24, FMT, LOGAN_HSHAPE(64), true>(P, io, hio, sms, s)
+                                        : launch_win<1, 24, FMT, 0, 0, true>(P, io, hio, sms, s);
+                case 28: return helpers ? launch_win<1, 28, FMT, LOGAN_HSHAPE(64), true>(P, io, hio, sms, s)
+                                        : launch_win<1, 28, FMT, 0, 0, true>(P, io, hio, sms, s);
+                default: return helpers ? launch_win<1, 32, FMT, LOGAN_HSHAPE(64), true>(P, io, hio, sms, s)
+                                        : launch_win<1, 32, FMT, 0, 0, true>(P, io, hio, sms, s);
+            }
+        }
+    }
     switch (w0) {
         case 16: return helpers ? launch_win<1, 16, FMT, LOGAN_HSHAPE(64)>(P, io, hio, sms, s)
                                 : launch_win<1, 16, FMT, 0, 0>(P, io, hio, sms, s);

@@ -110,6 +110,7 @@ int logan_xdrop_batch(const uint8_t *seq_pool, int32_t seq_fmt, int64_t pool_len
     P.match = sc.match; P.mismatch = sc.mismatch; P.gap = sc.gap;
     P.one = 1;
     P.poison = (opt && (opt->flags & 2)) ? 1 : 0;
+    P.nopack = (opt && (opt->flags & 16)) ? 1 : 0;
     P.subst = opt ? opt->subst : nullptr;
     P.alphabet = (opt && opt->subst) ? opt->alphabet : 0;
     P.stats = stats;

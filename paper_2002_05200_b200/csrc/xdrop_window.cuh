@@ -48,6 +48,8 @@
 //    canonical (un-pipelined) state after an even antidiagonal.
 #pragma once
 
+#include <type_traits>
+
 #include "xdrop_common.cuh"
 
 namespace logan {
@@ -297,6 +299,9 @@ struct Window {
         if (gl == G - 1) st.sa.seek(P, st.S0 + W + ch);  // sa.idx = S0 + W + ceil(d/2)
         if (gl == 0) st.sb.seek(P, fh - st.S0 + 1);      // sb.idx = floor(d/2) - S0 + 1
     }
+
+    // the argmax is decoded at each raise (nothing pending at the task's end)
+    __device__ __forceinline__ void finalize() {}
 
     // ---- pending maxima -------------------------------------------------------
     // Fold the pending key k of raw antidiagonal a (relative to threshold T, with
@@ -775,6 +780,7 @@ __device__ __forceinline__ void run_group(Win &w, const Params &P, const LevelIO
                 if (rec != NO_REC) w.save(P, io.rec_out + (size_t)rec * io.rec_out_stride);
                 if (G > 1) __syncwarp(w.gmask);
             }
+            if (rc == 1) w.finalize();
             if (w.gl == 0) {
                 if (rc == 1) {
                     TaskRes tr;
@@ -822,9 +828,13 @@ __device__ __forceinline__ void run_group(Win &w, const Params &P, const LevelIO
 // overflowing tasks then finish while this level is still running instead of
 // forming a serial tail after it. What the helpers do not take, the next
 // level's own launch does (it shares their cursor).
-template <int G, int R, int FMT, int HG, int HR>
+template <int R, int FMT> struct Window16;  // xdrop_window16.cuh
+
+// PK: the producers run the packed int16 window (Window16, one lane per task)
+template <int G, int R, int FMT, int HG, int HR, bool PK = false>
 __global__ void __launch_bounds__(128, (G == 1 ? ((fmt_z(FMT) || fmt_base(FMT) == FMT_U8S) ? 3 : LOGAN_L0_MINB) : 1))
     k_window(const Params P, const LevelIO io, const LevelIO hio) {
+    using PW = typename std::conditional<PK, Window16<R, FMT>, Window<G, R, FMT>>::type;
     const uint32_t count = *io.count;
     const uint32_t taken = *io.cursor;  // entries already taken (by in-kernel helpers)
     const uint32_t remaining = count - (taken < count ? taken : count);
@@ -853,10 +863,12 @@ __global__ void __launch_bounds__(128, (G == 1 ? ((fmt_z(FMT) || fmt_base(FMT) =
         // producer group is done they stop taking entries, and whatever is left
         // goes to the next level's own launch (throughput shape if many).
         auto fetch = [&](uint32_t &pos) -> bool {
-            for (;;) {  // take a new entry only while producers are running
+            // take a new entry only while producers are running; idle helpers back
+            // off (their polls would take issue slots from the producers on their SM)
+            for (uint32_t ns = 256;; ns = ns < 32768 ? 2 * ns : ns) {
                 if (ld_relaxed(io.done) == total) return false;
                 if (ld_relaxed(hio.cursor) < ld_relaxed(io.out_count)) break;
-                __nanosleep(1000);
+                __nanosleep(ns);
             }
             uint32_t p = 0;
             if (w.gl == 0) p = atomicAdd(hio.cursor, 1u);
@@ -879,9 +891,9 @@ __global__ void __launch_bounds__(128, (G == 1 ? ((fmt_z(FMT) || fmt_base(FMT) =
         run_group(w, P, hio, fetch);
         return;
     }
-    Window<G, R, FMT> w;
+    PW w;
     w.tab = tab;
-    w.sbase = win_smem + threadIdx.x * Window<G, R, FMT>::SB_STRIDE;
+    w.sbase = win_smem + threadIdx.x * PW::SB_STRIDE;
     w.gl = lane % G;
     w.gmask = (G == 32) ? 0xffffffffu : (((1u << G) - 1u) << (lane - w.gl));
     const int leader = lane - w.gl;

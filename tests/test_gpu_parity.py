@@ -690,3 +690,25 @@ def test_partition_independence_multi_device_wrapper():
         for g in (1, 2, 4, 8):
             o, c = multi.xdrop_multi(b, w, ["cuda:0"] * g)
             assert_same(o, c, *ref, what=f"xdrop_multi config {cfg} G={g}")
+
+
+@pytest.mark.parametrize("cfg,X,lvl", [(2, 5, None), (2, 12, None), (2, 20, None), (3, 20, None), (2, 60, 1),
+                                       (6, 300, 1), (2, 20, 1)])
+def test_packed_first_window_equals_int32_window(cfg, X, lvl):
+    """The packed int16 first window (2-bit pools, X <= 16000) against the
+    int32 window (options.flags bit 4) on every pair, and both against the
+    oracle on a sample; forced level 1 at large X makes most tasks overflow
+    (hand-over records written from the packed layout)."""
+    w = datagen.CONFIGS[cfg].with_(xdrop=X)
+    b = datagen.generate(w, n_pairs=20000 if cfg != 3 else 4000, u8=False)
+    db = logan.to_device(b, logan.LOGAN_SEQ_2BIT)
+    res = []
+    for nopack in (False, True):
+        out, cells = logan.xdrop_batch(db, 1, -1, -1, X, first_level=lvl, nopack=nopack, throughput_first=True)
+        torch.cuda.synchronize()
+        res.append((out.cpu().numpy(), cells.cpu().numpy().view(np.uint64)))
+    assert_same(*res[0], *res[1], what=f"packed vs int32 config {cfg} X={X} level={lvl}")
+    idx = np.arange(0, b.n_pairs, 97)
+    ref = oracle.pairs(b.pool_2bit, 1, b.q_off[idx], b.q_len[idx], b.t_off[idx], b.t_len[idx], b.q_seed[idx],
+                       b.t_seed[idx], w.k, 1, -1, -1, X, pool_len=b.pool_len)
+    assert_same(res[0][0][idx], res[0][1][idx], *ref, what=f"packed vs oracle config {cfg} X={X}")

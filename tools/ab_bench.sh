@@ -2,6 +2,7 @@
 # A/B of library variants on one box: tools/ab_bench.sh "<bench args>" name=path ...
 args="$1"; shift
 mkdir -p gpurun_out
+echo "== $args"
 for rep in 1 2; do
   for nv in "$@"; do
     name=${nv%%=*}; lib=${nv#*=}
