@@ -474,6 +474,7 @@ int run_batch(const Params &P, const logan_options_t *opt, bool wide_only, logan
         if (!mark(1 + lv, 0)) return LOGAN_ECUDA;
         if (lv < NWIDTH) {
             if (lv == first) {
+                io.sms = sms;  // the first level's static first round (xdrop_window.cuh)
                 const bool helpers = !latency_first && lv + 1 < NWIDTH;
                 LevelIO hio{};
                 if (helpers) {

@@ -74,6 +74,7 @@ struct LevelIO {
     uint32_t workers;            // producer groups (non-helper groups) in the launch
     uint32_t *done;              // producer groups that finished
     int32_t is_helper;           // this IO drives in-kernel helpers (stats.helper_tasks)
+    int32_t sms;                 // > 0: first level, static first round over this many SMs
 };
 
 constexpr uint32_t NO_TASK = 0xffffffffu;

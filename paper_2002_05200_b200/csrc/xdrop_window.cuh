@@ -849,7 +849,9 @@ __global__ void __launch_bounds__(128, (G == 1 ? ((fmt_z(FMT) || fmt_base(FMT) =
         load_subst_tab(P, tab, threadIdx.x, blockDim.x);
         __syncthreads();
     }
-    const bool helper = HR > 0 && (int)blockIdx.x < io.helpers && (threadIdx.x >> 5) == (blockDim.x >> 5) - 1;
+    // helpers: the last warp of the LAST io.helpers blocks (see the static first round below)
+    const bool helper = HR > 0 && (int)blockIdx.x >= (int)gridDim.x - io.helpers &&
+                        (threadIdx.x >> 5) == (blockDim.x >> 5) - 1;
     if (HR > 0 && helper) {
         constexpr int HG_ = HG > 0 ? HG : 32, HR_ = HR > 0 ? HR : 1;
         Window<HG_, HR_, FMT> w;
@@ -865,7 +867,7 @@ __global__ void __launch_bounds__(128, (G == 1 ? ((fmt_z(FMT) || fmt_base(FMT) =
         auto fetch = [&](uint32_t &pos) -> bool {
             // take a new entry only while producers are running; idle helpers back
             // off (their polls would take issue slots from the producers on their SM)
-            for (uint32_t ns = 256;; ns = ns < 32768 ? 2 * ns : ns) {
+            for (uint32_t ns = 256;; ns = ns < 4096 ? 2 * ns : ns) {
                 if (ld_relaxed(io.done) == total) return false;
                 if (ld_relaxed(hio.cursor) < ld_relaxed(io.out_count)) break;
                 __nanosleep(ns);
@@ -897,10 +899,30 @@ __global__ void __launch_bounds__(128, (G == 1 ? ((fmt_z(FMT) || fmt_base(FMT) =
     w.gl = lane % G;
     w.gmask = (G == 32) ? 0xffffffffu : (((1u << G) - 1u) << (lane - w.gl));
     const int leader = lane - w.gl;
+    // First level (io.sms > 0): a static first round spreads the LPT queue's head
+    // over the SM sub-partitions. With blocks dispatched round-robin (block b on SM
+    // b mod #SM, warp w on sub-partition w), chunk c = (b mod #SM) + #SM * w +
+    // 4 #SM * (b div #SM) (32 / G tasks per warp) puts the longest 32/G-task chunks
+    // one per sub-partition before any doubles up -- what matters when the tasks
+    // are few (a strong-scaling share). The helpers (last warp of the last blocks)
+    // own the last chunk numbers, so the producers' chunks are dense. Later
+    // fetches take the dynamic cursor past the static region.
+    const int wib = threadIdx.x >> 5;
+    const uint32_t gpw = 32 / G;  // groups per warp
+    const uint32_t nprod = gridDim.x * (blockDim.x >> 5) - (uint32_t)io.helpers;  // producer warps
+    const bool stat = io.sms > 0 && (gridDim.x % (uint32_t)io.sms) == 0 && (blockDim.x >> 5) == 4;
+    const uint32_t sbase = stat ? nprod * gpw : 0u;
+    bool first = stat;
     auto fetch = [&](uint32_t &pos) -> bool {
         uint32_t p = 0xffffffffu;
-        if (w.gl == 0) p = atomicAdd(io.cursor, 1u);
-        if (G > 1) p = __shfl_sync(w.gmask, p, leader);
+        if (first) {
+            first = false;
+            const uint32_t c = blockIdx.x % io.sms + io.sms * wib + 4u * io.sms * (blockIdx.x / io.sms);
+            p = c * gpw + (uint32_t)(lane / G);
+        } else {
+            if (w.gl == 0) p = atomicAdd(io.cursor, 1u) + sbase;
+            if (G > 1) p = __shfl_sync(w.gmask, p, leader);
+        }
         pos = p;
         return p < count;
     };

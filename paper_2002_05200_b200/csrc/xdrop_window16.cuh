@@ -267,6 +267,31 @@ struct Window16 {
         return s < H ? 4 * (s >> 1) + (s & 1) : 4 * ((s - H) >> 1) + 2 + ((s - H) & 1);
     }
 
+    // live extremes of the killed antidiagonal e-1 (parity Qp) in array a:
+    // sF / sL[Qp] (validity-masked: cells past the matrix do not count)
+    template <int Qp>
+    __device__ __forceinline__ void extremes(int32_t e, const uint32_t (&a)[H]) {
+        const uint32_t z = dead_z(a);
+        const int32_t chq = e >> 1, fhq = (e - 1) >> 1;  // ceil((e-1)/2), floor((e-1)/2)
+        const int32_t vlo = fhq - st.n, vhi = st.m - chq;
+        uint32_t vmask = 0xffffffffu;
+        if (vlo > st.S0 || vhi < st.S0 + R - 1) {  // near the matrix edges
+            // valid slots [rlo, rhi] as a slot-order mask, then spread to the z
+            // layout (bit s -> 4(s>>1) + (s&1) for s < H, 4((s-H)>>1) + 2 + ((s-H)&1))
+            const int32_t rlo = max(vlo - st.S0, 0), rhi = min(vhi - st.S0, R - 1);
+            const uint32_t m = (rlo <= rhi) ? ((0xffffffffu >> (31 - rhi)) & ~((1u << rlo) - 1u)) : 0u;
+            vmask = spread2(m & ((1u << H) - 1u)) | (spread2(m >> H) << 2);
+        }
+        const uint32_t live = ~z & vmask & (H == 16 ? 0xffffffffu : ((1u << (2 * H)) - 1u));
+        const uint32_t llo = live & 0x33333333u, lhi = live & 0xCCCCCCCCu;
+        const bool h = live != 0;
+        const int pf = __ffs(llo ? llo : lhi) - 1, pl = 31 - __clz(lhi ? lhi : llo);
+        const int32_t f = (llo ? 0 : H) + ((pf & ~2) >> 1) + (pf & 1);
+        const int32_t l = (lhi ? H : 0) + ((pl & ~2) >> 1) + (pl & 1);
+        st.sF[Qp] = h ? st.S0 + f : EMPTY_F;
+        st.sL[Qp] = h ? st.S0 + l : EMPTY_L;
+    }
+
     template <int PAR>
     __device__ __forceinline__ int step(const Params &P, bool force) {
         const int32_t e = st.d + 1;
@@ -282,75 +307,52 @@ struct Window16 {
         const int32_t dl = T1 - T2;
         const uint32_t ndl2 = pk2(-dl);
 
-        // (b) late kill of e-1, dead mask and live extremes
-        uint32_t z;
+        // (b) late kill of e-1
         if (PAR) {
 #pragma unroll
             for (int k = 0; k < H; ++k) E[k] = __viaddmin_u16x2(E[k], ndl2, DEAD2);
-            z = dead_z(E);
         } else {
 #pragma unroll
             for (int k = 0; k < H; ++k) O[k] = __viaddmin_u16x2(O[k], ndl2, DEAD2);
-            z = dead_z(O);
-        }
-        {
-            const int32_t chq = e >> 1, fhq = (e - 1) >> 1;
-            const int32_t vlo = fhq - st.n, vhi = st.m - chq;
-            uint32_t vmask = 0xffffffffu;
-            if (vlo > st.S0 || vhi < st.S0 + R - 1) {  // near the matrix edges
-                // valid slots [rlo, rhi] as a slot-order mask, then spread to the z
-                // layout (bit s -> 4(s>>1) + (s&1) for s < H, 4((s-H)>>1) + 2 + ((s-H)&1))
-                const int32_t rlo = max(vlo - st.S0, 0), rhi = min(vhi - st.S0, R - 1);
-                const uint32_t m = (rlo <= rhi) ? ((0xffffffffu >> (31 - rhi)) & ~((1u << rlo) - 1u)) : 0u;
-                vmask = spread2(m & ((1u << H) - 1u)) | (spread2(m >> H) << 2);
-            }
-            const uint32_t live = ~z & vmask & (H == 16 ? 0xffffffffu : ((1u << (2 * H)) - 1u));
-            const uint32_t llo = live & 0x33333333u, lhi = live & 0xCCCCCCCCu;
-            const bool h = live != 0;
-            int32_t f, l;
-            if (llo) { const int p = __ffs(llo) - 1; f = (p >> 1) + (p & 1); }
-            else { const int p = __ffs(lhi) - 1; f = H + ((p - 2) >> 1) + (p & 1); }
-            if (lhi) { const int p = 31 - __clz(lhi); l = H + ((p - 2) >> 1) + (p & 1); }
-            else { const int p = 31 - __clz(llo); l = (p >> 1) + (p & 1); }
-            st.sF[Q] = h ? st.S0 + f : EMPTY_F;
-            st.sL[Q] = h ? st.S0 + l : EMPTY_L;
         }
         st.Tq[Q] = T1;
 
-        // (c) odd e: termination, window check (as Window::step)
+        // (c) odd e: the window check of Window::step needs the live extremes of e-1
+        //     and e-2 only at the window's edges: slots 0 and R-1 both dead in both
+        //     arrays (a sign test) means nothing to do, and the raw cells of e need not
+        //     wait for the extremes. Otherwise (numerically live edge slots, which can
+        //     also be cells past the matrix) the rare path takes the exact decision.
         if (PAR == 1) {
-            if (st.sF[0] == EMPTY_F && st.sF[1] == EMPTY_F) return 1;
-            bool ho = force;
-            if (!ho) {
-                const int32_t Fm = min(st.sF[0], st.sF[1]), Lm = max(st.sL[0], st.sL[1]);
-                const bool lowv = Fm < st.S0 + 1, highv = Lm > st.S0 + W - 2;
-                if (lowv || highv) {
-                    if (lowv && highv) ho = true;
-                    else if (lowv) {
-                        if (Lm > st.S0 + W - 3) ho = true;
-                        else shift_left(P, e - 1);
-                    } else {
-                        if (Fm < st.S0 + 2) ho = true;
-                        else shift_right(P, e - 1);
+            // an edge slot counts only inside the matrix on e-1 (slot 0 has the
+            // largest j, slot R-1 the largest i); e-2's validity range differs from
+            // e-1's by at most one slot on each side, which only makes this test
+            // more eager (the exact decision below is unaffected)
+            const uint32_t lo0 = E[0] & O[0], hiR = E[H - 1] & O[H - 1];
+            const bool in0 = st.S0 >= ((e - 1) >> 1) - st.n, inR = st.S0 + R - 1 <= st.m - (e >> 1);
+            if (force || (!(lo0 & 0x8000u) && in0) || (!(hiR & 0x80000000u) && inR)) {
+                extremes<Q>(e, E);
+                if (st.sF[0] == EMPTY_F && st.sF[1] == EMPTY_F) return 1;  // P:186, c-amb-7
+                bool ho = force;
+                if (!ho) {
+                    const int32_t Fm = min(st.sF[0], st.sF[1]), Lm = max(st.sL[0], st.sL[1]);
+                    const bool lowv = Fm < st.S0 + 1, highv = Lm > st.S0 + W - 2;
+                    if (lowv || highv) {
+                        if (lowv && highv) ho = true;
+                        else if (lowv) {
+                            if (Lm > st.S0 + W - 3) ho = true;
+                            else shift_left(P, e - 1);
+                        } else {
+                            if (Fm < st.S0 + 2) ho = true;
+                            else shift_right(P, e - 1);
+                        }
                     }
                 }
+                if (ho) {
+                    fold(st.K[Q], T2, e - 1, dl, E);  // e-1 is even here: array E (killed above)
+                    st.K[Q] = KNONE;
+                    return 2;
+                }
             }
-            if (ho) {
-                fold(st.K[Q], T2, e - 1, dl, E);  // e-1 is even here: array E (killed above)
-                st.K[Q] = KNONE;
-                return 2;
-            }
-        }
-
-        // (d) band cells of e (c-amb-14)
-        {
-            const int32_t c = PAR ? (e - 1) >> 1 : e >> 1;
-            const int32_t F1 = st.sF[Q], F2 = st.sF[PAR], L1 = st.sL[Q], L2 = st.sL[PAR];
-            const int32_t fmin = PAR ? min(F1, F2 + 1) : min(F1, F2);
-            const int32_t lmax = PAR ? max(L1, L2) : max(L1, L2 - 1);
-            const int32_t lo = __vimax3_s32(fmin + c, 1, e - st.n);
-            const int32_t hi = __vimin3_s32(lmax + c + 1, st.m, e - 1);
-            st.cells += (uint32_t)__vimax_s32_relu(hi - lo + 1, 0);
         }
 
         // (e) bases for antidiagonal e
@@ -416,6 +418,25 @@ struct Window16 {
         for (int q = 1; q < NM; q += 2)
             m2 = __vimax3_s16x2(m2, mx[q], (q + 1 < NM) ? mx[q + 1] : mx[q]);
         st.K[PAR] = max(lo16(m2), hi16(m2));
+
+        // (b') live extremes of e-1 (band bookkeeping, off the cells' critical path)
+        if (PAR) extremes<Q>(e, E);
+        else extremes<Q>(e, O);
+        // termination after an even e-1 (c-amb-7): e-1 and e-2 both empty;
+        // best_{e-2} is final and the raw cells of e just computed are discarded
+        if (PAR == 1 && st.sF[0] == EMPTY_F && st.sF[1] == EMPTY_F) return 1;
+
+        // (d) band cells of e (c-amb-14)
+        {
+            const int32_t c = PAR ? (e - 1) >> 1 : e >> 1;
+            const int32_t F1 = st.sF[Q], F2 = st.sF[PAR], L1 = st.sL[Q], L2 = st.sL[PAR];
+            const int32_t fmin = PAR ? min(F1, F2 + 1) : min(F1, F2);
+            const int32_t lmax = PAR ? max(L1, L2) : max(L1, L2 - 1);
+            const int32_t lo = __vimax3_s32(fmin + c, 1, e - st.n);
+            const int32_t hi = __vimin3_s32(lmax + c + 1, st.m, e - 1);
+            st.cells += (uint32_t)__vimax_s32_relu(hi - lo + 1, 0);
+        }
+
         st.d = e;
         return 0;
     }
