@@ -331,3 +331,74 @@ def protein_pairs(n_pairs: int, len_lo: int = 200, len_hi: int = 1000, sub: floa
     return Batch(w, pair_base, np.array(qo_, np.int64), np.array(ql_, np.int32), np.array(to_, np.int64),
                  np.array(tl_, np.int32), np.array(qs_, np.int32), np.array(ts_, np.int32), pool_len, pu8, None,
                  meta={"alphabet": PROTEIN_ALPHABET})
+
+
+# ---------------------------------------------------------------------------
+# A read SET for the BELLA-like many-to-many shell (
+# PAPER.md §V). Pure numpy, seeded: a random genome, reads cut at
+# uniform positions with log-uniform lengths, each mutated at e/2 (1/3
+# substitution, 1/3 insertion after the base, 1/3 deletion; as gen.c), forward
+# strand only. Holds none of the method's arithmetic.
+READSET_SEED = SEED_BASE + 8
+
+
+@dataclass
+class ReadSet:
+    n_reads: int
+    off: np.ndarray       # int64 pool offset of every read (multiple of 4)
+    len: np.ndarray       # int32 read lengths
+    g_start: np.ndarray   # genome interval each read was cut from (ground truth)
+    g_end: np.ndarray
+    pool_len: int
+    pool_u8: np.ndarray
+    pool_2bit: np.ndarray
+    codes: np.ndarray     # 2-bit code of every pool position (A=0 C=1 G=2 T=3)
+    err: float
+    coverage: float
+
+
+def _mutate_dna(rng, t: np.ndarray, rate: float) -> np.ndarray:
+    L = len(t)
+    r = rng.random(L)
+    subm = r < rate / 3
+    delm = (r >= rate / 3) & (r < 2 * rate / 3)
+    insm = (r >= 2 * rate / 3) & (r < rate)
+    codes = t.copy()
+    codes[subm] = (t[subm] + rng.integers(1, 4, int(subm.sum()))) % 4
+    vals = np.stack([codes, rng.integers(0, 4, L)], 1)
+    mask = np.stack([~delm, insm], 1)
+    return vals[mask].astype(np.uint8)
+
+
+def read_set(n_reads: int = 400, genome_len: int = 200_000, len_lo: int = 2000, len_hi: int = 8000,
+             err: float = 0.15, repeats: int = 0, repeat_len: int = 400, seed: int = READSET_SEED) -> ReadSet:
+    """Reads sampled from one random genome (BELLA-like input, synthetic).
+    ``repeats`` families of two identical copies of a ``repeat_len`` block are
+    planted at random genome positions: reads covering different copies share
+    k-mers without overlapping (the false candidates BELLA's threshold rejects)."""
+    rng = np.random.default_rng(seed)
+    genome = rng.integers(0, 4, genome_len).astype(np.uint8)
+    for _ in range(repeats):
+        unit = rng.integers(0, 4, repeat_len).astype(np.uint8)
+        for p in rng.integers(0, genome_len - repeat_len, 2):
+            genome[p:p + repeat_len] = unit
+    lens = np.exp(rng.uniform(math.log(len_lo), math.log(len_hi), n_reads)).astype(np.int64)
+    starts = rng.integers(0, np.maximum(genome_len - lens, 1))
+    reads = [_mutate_dna(np.random.default_rng([seed, r]), genome[starts[r]:starts[r] + lens[r]], err / 2)
+             for r in range(n_reads)]
+    rl = np.array([len(x) for x in reads], np.int64)
+    region = (rl + 3) // 4 * 4
+    off = np.zeros(n_reads, np.int64)
+    if n_reads > 1:
+        np.cumsum(region[:-1], out=off[1:])
+    pool_len = int(off[-1] + region[-1]) if n_reads else 0
+    codes = np.zeros(_pad16(pool_len) + 16, np.uint8)
+    for r in range(n_reads):
+        codes[off[r]:off[r] + rl[r]] = reads[r]
+    pu8 = np.frombuffer(b"ACGT", np.uint8)[codes]
+    pu8[pool_len:] = 0
+    p2 = np.zeros(_pad16((pool_len + 3) // 4) + 16, np.uint8)
+    c = codes[:(pool_len + 3) // 4 * 4].reshape(-1, 4)
+    p2[:len(c)] = c[:, 0] | (c[:, 1] << 2) | (c[:, 2] << 4) | (c[:, 3] << 6)
+    return ReadSet(n_reads, off, rl.astype(np.int32), starts.astype(np.int64), (starts + lens).astype(np.int64),
+                   pool_len, pu8, p2, codes, err, float(lens.sum()) / genome_len)

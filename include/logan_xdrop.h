@@ -106,6 +106,15 @@ enum {
  *                  bit 2 = Z-drop on, threshold `zdrop` (0 <= zdrop <= 2^28).
  *                  bit 3 = run the first level in its throughput shape even
  *                  when the batch has few tasks (test / tuning knob; bit 0 wins).
+ *                  bit 5 = SeqAn-compat mode ([outside-PAPER]
+ *                  readings c-amb-24/25 of DESIGN.md §3, not verified against
+ *                  SeqAn): boundary cells (i = 0 or j = 0) on antidiagonals
+ *                  d >= 2 are live only if S > best - X (strict), and each
+ *                  extension's end cell is the "longest extension" -- the
+ *                  best live cell (smallest i) of the last antidiagonal with a
+ *                  live cell -- instead of the argmax; score = seed + best_L +
+ *                  best_R as usual. Runs on the CTA level (8) only; match /
+ *                  mismatch scoring only (a substitution matrix -> EINVAL).
  *                  bit 4 = test / A-B knob: the first window of a 2-bit pool
  *                  runs on int32 values instead of packed int16 pairs.
  *                  bit 1 = test knob: the band level fills its shared-memory

@@ -80,6 +80,13 @@ def _load():
                                        i64, i64, i64, i64, i8p, i64, i64, i64, i64, i32p,
                                        ctypes.POINTER(ctypes.c_uint64), ctypes.c_int]
         lib.oracle_pairs_z.restype = ctypes.c_int
+        lib.oracle_extend_compat.argtypes = [u8p, i64, u8p, i64, i64, i64, i64, i64, i64, ctypes.c_int,
+                                             ctypes.POINTER(_Ext)]
+        lib.oracle_extend_compat.restype = ctypes.c_int
+        lib.oracle_pairs_compat.argtypes = [u8p, ctypes.c_int, i64, i64p, i32p, i64p, i32p, i32p, i32p,
+                                            i64, i64, i64, i64, i64, i64, i64, i32p,
+                                            ctypes.POINTER(ctypes.c_uint64), ctypes.c_int]
+        lib.oracle_pairs_compat.restype = ctypes.c_int
         _lib = lib
     return _lib
 
@@ -253,4 +260,47 @@ def pairs_z(pool: np.ndarray, fmt: int, q_off, q_len, t_off, t_len, q_seed, t_se
         zdrop, out.ctypes.data_as(P(ctypes.c_int32)), cells.ctypes.data_as(P(ctypes.c_uint64)), int(n_threads))
     if st != 0:
         raise RuntimeError(f"oracle_pairs_z failed with status {st}")
+    return out, cells
+
+
+def extend_compat(A, B, X: int, match: int = 1, mismatch: int = -1, gap: int = -1, zdrop: int = -1,
+                  full_scan: bool = False) -> ExtResult:
+    """SeqAn-compat extension (oracle header step 6; [outside-PAPER] readings
+    c-amb-24/25): strict boundary drop for d >= 2, (i, j) = the longest-extension
+    cell (the best live cell of the last live antidiagonal)."""
+    a, b = _as_u8(A), _as_u8(B)
+    out = _Ext()
+    u8p = ctypes.POINTER(ctypes.c_uint8)
+    st = _load().oracle_extend_compat(a.ctypes.data_as(u8p), len(a), b.ctypes.data_as(u8p), len(b),
+                                      match, mismatch, gap, X, zdrop, int(full_scan), ctypes.byref(out))
+    if st != 0:
+        raise RuntimeError(f"oracle_extend_compat failed with status {st}")
+    return ExtResult(out.best, out.i, out.j, out.cells, out.last_d)
+
+
+def pairs_compat(pool: np.ndarray, fmt: int, q_off, q_len, t_off, t_len, q_seed, t_seed, k: int,
+                 match: int, mismatch: int, gap: int, X: int, zdrop: int = -1, pool_len: int | None = None,
+                 n_threads: int | None = None):
+    """Batch of pairs in SeqAn-compat mode -> (int32[n,5], uint64[n])."""
+    pool = np.ascontiguousarray(pool, dtype=np.uint8)
+    if pool_len is None:
+        pool_len = len(pool) if fmt == 0 else 4 * len(pool)
+    cols = [np.ascontiguousarray(x, dtype=dt) for x, dt in
+            ((q_off, np.int64), (q_len, np.int32), (t_off, np.int64), (t_len, np.int32),
+             (q_seed, np.int32), (t_seed, np.int32))]
+    n = len(cols[0])
+    out = np.zeros((n, 5), dtype=np.int32)
+    cells = np.zeros(n, dtype=np.uint64)
+    if n_threads is None:
+        n_threads = len(os.sched_getaffinity(0))
+    P = ctypes.POINTER
+    st = _load().oracle_pairs_compat(
+        pool.ctypes.data_as(P(ctypes.c_uint8)), fmt, pool_len,
+        cols[0].ctypes.data_as(P(ctypes.c_int64)), cols[1].ctypes.data_as(P(ctypes.c_int32)),
+        cols[2].ctypes.data_as(P(ctypes.c_int64)), cols[3].ctypes.data_as(P(ctypes.c_int32)),
+        cols[4].ctypes.data_as(P(ctypes.c_int32)), cols[5].ctypes.data_as(P(ctypes.c_int32)),
+        n, k, match, mismatch, gap, X, zdrop, out.ctypes.data_as(P(ctypes.c_int32)),
+        cells.ctypes.data_as(P(ctypes.c_uint64)), int(n_threads))
+    if st != 0:
+        raise RuntimeError(f"oracle_pairs_compat failed with status {st}")
     return out, cells

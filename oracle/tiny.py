@@ -53,11 +53,18 @@ def full_dp_best(A, B, match: int = 1, mismatch: int = -1, gap: int = -1, subst=
     return best, bi, bj
 
 
-def xdrop_dict(A: str, B: str, X: int, match: int = 1, mismatch: int = -1, gap: int = -1):
-    """Literal X-drop over a dict of live cells -> (best, i*, j*, cells)."""
+def xdrop_dict(A: str, B: str, X: int, match: int = 1, mismatch: int = -1, gap: int = -1,
+               compat: bool = False):
+    """Literal X-drop over a dict of live cells -> (best, i*, j*, cells).
+    ``compat``: the SeqAn-compat reading (oracle header step 6): strict ``>`` on
+    boundary cells for d >= 2, and (i*, j*) = the best live cell (smallest i) of
+    the last antidiagonal with a live cell."""
     m, n = len(A), len(B)
+    if compat and (m == 0 or n == 0):
+        return 0, 0, 0, 0  # empty extension (c-amb-13)
     live = {0: {0: 0}}  # d -> {i: S}
     best, bi, bj = 0, 0, 0
+    last = (0, 0)  # compat: the origin unless a later antidiagonal has a live cell
     cells = 0
     d = 0
     while True:
@@ -86,7 +93,8 @@ def xdrop_dict(A: str, B: str, X: int, match: int = 1, mismatch: int = -1, gap: 
                 cand.append(p1[i] + gap)
             if i >= 1 and (i - 1) in p1:
                 cand.append(p1[i - 1] + gap)
-            if cand and max(cand) >= thr:
+            boundary = compat and d >= 2 and (i == 0 or j == 0)
+            if cand and (max(cand) > thr if boundary else max(cand) >= thr):
                 cur[i] = max(cand)
         live[d] = cur
         if cur:
@@ -95,6 +103,10 @@ def xdrop_dict(A: str, B: str, X: int, match: int = 1, mismatch: int = -1, gap: 
                 best = v
                 bi = min(i for i, s in cur.items() if s == v)
                 bj = d - bi
+            li = min(i for i, s in cur.items() if s == v)
+            last = (li, d - li)
         if not cur and not p1:
             break
+    if compat:
+        bi, bj = last if d > 0 and any(live.values()) else (0, 0)
     return best, bi, bj, cells

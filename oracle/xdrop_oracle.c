@@ -37,6 +37,16 @@
  *      (boundary cells included; F_0 = L_0 = 0), only the terms of non-empty
  *      antidiagonals taken, empty band if both are empty     (c-amb-14)
  *
+ *  (6) optional SeqAn-compat mode ([outside-PAPER] readings
+ *      c-amb-24/25 of DESIGN.md §3, not verified against SeqAn, which is not
+ *      available here): boundary cells (i = 0 or j = 0) on antidiagonals d >= 2
+ *      are live only if S > best_{d-1} - X (strict; antidiagonal 1 keeps >=),
+ *      and the returned cell is the "longest extension": the highest-scoring
+ *      live cell (smallest i on ties) of the LAST antidiagonal that has a live
+ *      cell, instead of the argmax of step (4); best is unchanged. An empty
+ *      extension (m = 0 or n = 0) returns best 0 at (0,0) with 0 cells, as in
+ *      the standard mode (c-amb-13; SeqAn returns at once for an empty segment).
+ *
  * Step (2) visits, on antidiagonal d, only the columns that are adjacent to a
  * live cell of d-1 or d-2: a cell elsewhere has C = {} and is dead by
  * definition, so skipping it changes nothing. `full_scan = 1` visits every
@@ -131,12 +141,12 @@ static int64_t sub_score(uint8_t a, uint8_t b, int64_t match, int64_t mismatch,
 
 static int extend_impl(const uint8_t *A, int64_t m, const uint8_t *B, int64_t n,
                        int64_t match, int64_t mismatch, const int8_t *subst, int64_t alph,
-                       int64_t gap, int64_t X, int64_t zdrop, int full_scan, oracle_ext_t *out);
+                       int64_t gap, int64_t X, int64_t zdrop, int compat, int full_scan, oracle_ext_t *out);
 
 int oracle_extend(const uint8_t *A, int64_t m, const uint8_t *B, int64_t n,
                   int64_t match, int64_t mismatch, int64_t gap, int64_t X,
                   int full_scan, oracle_ext_t *out) {
-    return extend_impl(A, m, B, n, match, mismatch, NULL, 0, gap, X, -1, full_scan, out);
+    return extend_impl(A, m, B, n, match, mismatch, NULL, 0, gap, X, -1, 0, full_scan, out);
 }
 
 /* The same extension with s(a, b) = subst[a * alph + b]; every code of A and B
@@ -147,7 +157,7 @@ int oracle_extend_subst(const uint8_t *A, int64_t m, const uint8_t *B, int64_t n
     if (!subst || alph < 1 || alph > 256) return ORACLE_EINVAL;
     for (int64_t i = 0; i < m; ++i) if (A[i] >= alph) return ORACLE_EINVAL;
     for (int64_t j = 0; j < n; ++j) if (B[j] >= alph) return ORACLE_EINVAL;
-    return extend_impl(A, m, B, n, 0, 0, subst, alph, gap, X, -1, full_scan, out);
+    return extend_impl(A, m, B, n, 0, 0, subst, alph, gap, X, -1, 0, full_scan, out);
 }
 
 /* The general extension: subst = NULL for match / mismatch, zdrop < 0 for no
@@ -160,18 +170,26 @@ int oracle_extend_z(const uint8_t *A, int64_t m, const uint8_t *B, int64_t n,
         for (int64_t i = 0; i < m; ++i) if (A[i] >= alph) return ORACLE_EINVAL;
         for (int64_t j = 0; j < n; ++j) if (B[j] >= alph) return ORACLE_EINVAL;
     }
-    return extend_impl(A, m, B, n, match, mismatch, subst, alph, gap, X, zdrop, full_scan, out);
+    return extend_impl(A, m, B, n, match, mismatch, subst, alph, gap, X, zdrop, 0, full_scan, out);
+}
+
+/* SeqAn-compat mode (header step 6; match / mismatch scoring, optional Z-drop). */
+int oracle_extend_compat(const uint8_t *A, int64_t m, const uint8_t *B, int64_t n,
+                         int64_t match, int64_t mismatch, int64_t gap, int64_t X, int64_t zdrop,
+                         int full_scan, oracle_ext_t *out) {
+    return extend_impl(A, m, B, n, match, mismatch, NULL, 0, gap, X, zdrop, 1, full_scan, out);
 }
 
 static int extend_impl(const uint8_t *A, int64_t m, const uint8_t *B, int64_t n,
                        int64_t match, int64_t mismatch, const int8_t *subst, int64_t alph,
-                       int64_t gap, int64_t X, int64_t zdrop, int full_scan, oracle_ext_t *out) {
+                       int64_t gap, int64_t X, int64_t zdrop, int compat, int full_scan, oracle_ext_t *out) {
     if (!out || m < 0 || n < 0 || X < 0 || (m > 0 && !A) || (n > 0 && !B)) return ORACLE_EINVAL;
     out->best = 0;
     out->i = 0;
     out->j = 0;
     out->cells = 0;
     out->last_d = 0;
+    if (compat && (m == 0 || n == 0)) return ORACLE_OK; /* (6): empty extension */
 
     antidiag_t ad[3]; /* ad[d % 3] holds antidiagonal d */
     for (int k = 0; k < 3; ++k) {
@@ -189,6 +207,7 @@ static int extend_impl(const uint8_t *A, int64_t m, const uint8_t *B, int64_t n,
     a0->has_live = 1;
     a0->F = a0->L = 0;
     int64_t best = 0, arg_i = 0, arg_j = 0;
+    int64_t last_i = 0, last_j = 0; /* compat (step 6): the origin if nothing else is live */
     uint64_t cells = 0;
     /* antidiagonal -1 does not exist: treat it as empty */
     int prev2_exists = 0; /* whether antidiagonal d-2 exists (d >= 2) */
@@ -280,6 +299,8 @@ static int extend_impl(const uint8_t *A, int64_t m, const uint8_t *B, int64_t n,
                 have = 1;
             }
             int live = have && (v >= threshold); /* dropped iff S < best - X */
+            /* (6) compat: boundary cells on d >= 2 need S > best - X */
+            if (compat && d >= 2 && (i == 0 || j == 0)) live = have && (v > threshold);
             cur->live[i] = (uint8_t)live;
             cur->val[i] = live ? v : 0;
             if (live) {
@@ -302,6 +323,11 @@ static int extend_impl(const uint8_t *A, int64_t m, const uint8_t *B, int64_t n,
             arg_i = dmax_i;
             arg_j = d - dmax_i;
         }
+        /* (6) compat: the best live cell of the last antidiagonal with a live cell */
+        if (have_max) {
+            last_i = dmax_i;
+            last_j = d - dmax_i;
+        }
         /* (3b) Z-drop (the variant the paper names; c-amb-19): stop after
          * antidiagonal d when best - M_d > Z + |gap| * |(i_d - i*) - (j_d - j*)|,
          * M_d / (i_d, j_d) = d's max live score and its cell (smallest i). */
@@ -317,8 +343,8 @@ static int extend_impl(const uint8_t *A, int64_t m, const uint8_t *B, int64_t n,
 
     for (int k = 0; k < 3; ++k) antidiag_free(&ad[k]);
     out->best = best;
-    out->i = arg_i;
-    out->j = arg_j;
+    out->i = compat ? last_i : arg_i;
+    out->j = compat ? last_j : arg_j;
     out->cells = cells;
     out->last_d = d;
     return ORACLE_OK;
@@ -342,7 +368,8 @@ static int pair_impl(const uint8_t *pool, int fmt, int64_t pool_len,
                      int64_t q_off, int64_t q_len, int64_t t_off, int64_t t_len,
                      int64_t qs, int64_t ts, int64_t k,
                      int64_t match, int64_t mismatch, const int8_t *subst, int64_t alph,
-                     int64_t gap, int64_t X, int64_t zdrop, oracle_pair_t *res, uint64_t *cells_out);
+                     int64_t gap, int64_t X, int64_t zdrop, int compat, oracle_pair_t *res,
+                     uint64_t *cells_out);
 
 int oracle_pair(const uint8_t *pool, int fmt, int64_t pool_len,
                 int64_t q_off, int64_t q_len, int64_t t_off, int64_t t_len,
@@ -350,14 +377,15 @@ int oracle_pair(const uint8_t *pool, int fmt, int64_t pool_len,
                 int64_t match, int64_t mismatch, int64_t gap, int64_t X,
                 oracle_pair_t *res, uint64_t *cells_out) {
     return pair_impl(pool, fmt, pool_len, q_off, q_len, t_off, t_len, qs, ts, k, match, mismatch,
-                     NULL, 0, gap, X, -1, res, cells_out);
+                     NULL, 0, gap, X, -1, 0, res, cells_out);
 }
 
 static int pair_impl(const uint8_t *pool, int fmt, int64_t pool_len,
                      int64_t q_off, int64_t q_len, int64_t t_off, int64_t t_len,
                      int64_t qs, int64_t ts, int64_t k,
                      int64_t match, int64_t mismatch, const int8_t *subst, int64_t alph,
-                     int64_t gap, int64_t X, int64_t zdrop, oracle_pair_t *res, uint64_t *cells_out) {
+                     int64_t gap, int64_t X, int64_t zdrop, int compat, oracle_pair_t *res,
+                     uint64_t *cells_out) {
     res->score = INT32_MIN;
     res->q_begin = res->q_end = res->t_begin = res->t_end = -1;
     if (cells_out) *cells_out = 0;
@@ -389,8 +417,8 @@ static int pair_impl(const uint8_t *pool, int fmt, int64_t pool_len,
 
     oracle_ext_t L, R;
     int st = bad_code ? ORACLE_EINVAL : ORACLE_OK;
-    if (st == ORACLE_OK) st = oracle_extend_z(AL, mL, BL, nL, match, mismatch, subst, alph, gap, X, zdrop, 0, &L);
-    if (st == ORACLE_OK) st = oracle_extend_z(AR, mR, BR, nR, match, mismatch, subst, alph, gap, X, zdrop, 0, &R);
+    if (st == ORACLE_OK) st = extend_impl(AL, mL, BL, nL, match, mismatch, subst, alph, gap, X, zdrop, compat, 0, &L);
+    if (st == ORACLE_OK) st = extend_impl(AR, mR, BR, nR, match, mismatch, subst, alph, gap, X, zdrop, compat, 0, &R);
     free(AL); free(BL); free(AR); free(BR);
     if (st != ORACLE_OK) return st;
 
@@ -421,6 +449,7 @@ typedef struct {
     const int8_t *subst;
     int64_t alph;
     int64_t zdrop;
+    int compat;
     oracle_pair_t *out;
     uint64_t *cells;
     int64_t next; /* shared cursor */
@@ -442,7 +471,7 @@ static void *batch_worker(void *arg) {
             int st = pair_impl(job->pool, job->fmt, job->pool_len, job->q_off[p], job->q_len[p],
                                job->t_off[p], job->t_len[p], job->q_seed[p], job->t_seed[p],
                                job->k, job->match, job->mismatch, job->subst, job->alph, job->gap, job->X,
-                               job->zdrop, &job->out[p], &c);
+                               job->zdrop, job->compat, &job->out[p], &c);
             if (job->cells) job->cells[p] = c;
             if (st != ORACLE_OK) {
                 pthread_mutex_lock(&job->mu);
@@ -459,7 +488,8 @@ static int pairs_impl(const uint8_t *pool, int fmt, int64_t pool_len,
                       const int64_t *t_off, const int32_t *t_len,
                       const int32_t *q_seed, const int32_t *t_seed, int64_t n_pairs,
                       int64_t k, int64_t match, int64_t mismatch, const int8_t *subst, int64_t alph,
-                      int64_t gap, int64_t X, int64_t zdrop, oracle_pair_t *out, uint64_t *cells, int n_threads);
+                      int64_t gap, int64_t X, int64_t zdrop, int compat, oracle_pair_t *out, uint64_t *cells,
+                      int n_threads);
 
 int oracle_pairs(const uint8_t *pool, int fmt, int64_t pool_len,
                  const int64_t *q_off, const int32_t *q_len,
@@ -468,7 +498,18 @@ int oracle_pairs(const uint8_t *pool, int fmt, int64_t pool_len,
                  int64_t k, int64_t match, int64_t mismatch, int64_t gap, int64_t X,
                  oracle_pair_t *out, uint64_t *cells, int n_threads) {
     return pairs_impl(pool, fmt, pool_len, q_off, q_len, t_off, t_len, q_seed, t_seed, n_pairs, k,
-                      match, mismatch, NULL, 0, gap, X, -1, out, cells, n_threads);
+                      match, mismatch, NULL, 0, gap, X, -1, 0, out, cells, n_threads);
+}
+
+/* SeqAn-compat mode (header step 6): match / mismatch scoring, optional Z-drop. */
+int oracle_pairs_compat(const uint8_t *pool, int fmt, int64_t pool_len,
+                        const int64_t *q_off, const int32_t *q_len,
+                        const int64_t *t_off, const int32_t *t_len,
+                        const int32_t *q_seed, const int32_t *t_seed, int64_t n_pairs,
+                        int64_t k, int64_t match, int64_t mismatch, int64_t gap, int64_t X, int64_t zdrop,
+                        oracle_pair_t *out, uint64_t *cells, int n_threads) {
+    return pairs_impl(pool, fmt, pool_len, q_off, q_len, t_off, t_len, q_seed, t_seed, n_pairs, k,
+                      match, mismatch, NULL, 0, gap, X, zdrop, 1, out, cells, n_threads);
 }
 
 /* Pairs scored with a substitution matrix subst[alph * alph] (u8 pool of
@@ -481,7 +522,7 @@ int oracle_pairs_subst(const uint8_t *pool, int64_t pool_len,
                        oracle_pair_t *out, uint64_t *cells, int n_threads) {
     if (!subst || alph < 1 || alph > 256) return ORACLE_EINVAL;
     return pairs_impl(pool, 0, pool_len, q_off, q_len, t_off, t_len, q_seed, t_seed, n_pairs, k,
-                      0, 0, subst, alph, gap, X, -1, out, cells, n_threads);
+                      0, 0, subst, alph, gap, X, -1, 0, out, cells, n_threads);
 }
 
 /* The general batch: subst = NULL for match / mismatch (then fmt selects the
@@ -494,7 +535,7 @@ int oracle_pairs_z(const uint8_t *pool, int fmt, int64_t pool_len,
                    int64_t gap, int64_t X, int64_t zdrop, oracle_pair_t *out, uint64_t *cells, int n_threads) {
     if (subst && (alph < 1 || alph > 256 || fmt != 0)) return ORACLE_EINVAL;
     return pairs_impl(pool, fmt, pool_len, q_off, q_len, t_off, t_len, q_seed, t_seed, n_pairs, k,
-                      match, mismatch, subst, alph, gap, X, zdrop, out, cells, n_threads);
+                      match, mismatch, subst, alph, gap, X, zdrop, 0, out, cells, n_threads);
 }
 
 static int pairs_impl(const uint8_t *pool, int fmt, int64_t pool_len,
@@ -502,12 +543,14 @@ static int pairs_impl(const uint8_t *pool, int fmt, int64_t pool_len,
                       const int64_t *t_off, const int32_t *t_len,
                       const int32_t *q_seed, const int32_t *t_seed, int64_t n_pairs,
                       int64_t k, int64_t match, int64_t mismatch, const int8_t *subst, int64_t alph,
-                      int64_t gap, int64_t X, int64_t zdrop, oracle_pair_t *out, uint64_t *cells, int n_threads) {
+                      int64_t gap, int64_t X, int64_t zdrop, int compat, oracle_pair_t *out, uint64_t *cells,
+                      int n_threads) {
     if (n_pairs < 0 || (n_pairs > 0 && (!pool || !q_off || !q_len || !t_off || !t_len || !q_seed ||
                                         !t_seed || !out)))
         return ORACLE_EINVAL;
     batch_job_t job = {pool, fmt, pool_len, q_off, t_off, q_len, t_len, q_seed, t_seed, n_pairs,
-                       k, match, mismatch, gap, X, subst, alph, zdrop, out, cells, 0, PTHREAD_MUTEX_INITIALIZER, 0};
+                       k, match, mismatch, gap, X, subst, alph, zdrop, compat, out, cells, 0,
+                       PTHREAD_MUTEX_INITIALIZER, 0};
     if (n_threads < 1) n_threads = 1;
     if (n_threads == 1) {
         batch_worker(&job);

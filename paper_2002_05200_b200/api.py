@@ -51,17 +51,17 @@ def make_workspace(n_pairs: int, max_ext_len: int, device=None) -> Workspace:
 
 def _opts(first_level: int | None, timing_events=None, latency_first: bool = False,
           handover: int = 0, first_slots: int = 0, poison: bool = False, subst=None, zdrop: int | None = None,
-          throughput_first: bool = False, nopack: bool = False):
+          throughput_first: bool = False, nopack: bool = False, compat: bool = False):
     """Options struct; ``timing_events`` = list of 2*N_STAGES torch.cuda.Event;
     ``subst`` = square int8 CUDA tensor (alphabet x alphabet) or None."""
     if not first_level and timing_events is None and not latency_first and not handover \
             and not first_slots and not poison and subst is None and zdrop is None and not throughput_first \
-            and not nopack:
+            and not nopack and not compat:
         return None
     o = _lib.Options()
     o.first_level = int(first_level or 0)
     o.flags = (1 if latency_first else 0) | (2 if poison else 0) | (4 if zdrop is not None else 0) \
-        | (8 if throughput_first else 0) | (16 if nopack else 0)
+        | (8 if throughput_first else 0) | (16 if nopack else 0) | (32 if compat else 0)
     o.zdrop = int(zdrop) if zdrop is not None else 0
     o.handover = int(handover)
     o.first_slots = int(first_slots)
@@ -120,7 +120,7 @@ def xdrop_batch(db: DeviceBatch, match: int, mismatch: int, gap: int, xdrop: int
                 first_level: int | None = None, stream=None, timing_events=None,
                 latency_first: bool = False, handover: int = 0, first_slots: int = 0,
                 poison: bool = False, subst=None, zdrop: int | None = None, throughput_first: bool = False,
-                nopack: bool = False):
+                nopack: bool = False, compat: bool = False):
     """Run the whole hot path on ``db``'s device, asynchronously on ``stream``
     (default: torch's current stream).  Returns ``(out int32[n,5], cells int64[n])``
     device tensors (cells holds uint64 bit patterns)."""
@@ -148,7 +148,7 @@ def xdrop_batch(db: DeviceBatch, match: int, mismatch: int, gap: int, xdrop: int
             db.t_off.data_ptr(), db.t_len.data_ptr(), db.q_seed.data_ptr(), db.t_seed.data_ptr(),
             n, db.max_ext_len, db.k, sc,
             _opts(first_level, timing_events, latency_first, handover, first_slots, poison, subst, zdrop,
-                  throughput_first, nopack),
+                  throughput_first, nopack, compat),
             out.data_ptr(),
             cells.data_ptr(),
             stats.data_ptr() if stats is not None else None,

@@ -67,6 +67,7 @@ static int check_args(const uint8_t *seq_pool, int32_t seq_fmt, int64_t pool_len
     const bool subst = opt && opt->subst;
     if (subst && (seq_fmt != LOGAN_SEQ_U8 || opt->alphabet < 1 || opt->alphabet > LOGAN_MAX_ALPHABET))
         return LOGAN_EINVAL;
+    if (subst && (opt->flags & 32)) return LOGAN_EINVAL;  // SeqAn-compat: match / mismatch scoring only
     if (!subst && (sc.match <= 0 || sc.match > 127 || sc.mismatch >= 0 || sc.mismatch < -127))
         return LOGAN_EINVAL;
     if (sc.gap >= 0 || sc.gap < -127 || sc.xdrop < 0 || sc.xdrop > XDROP_MAX) return LOGAN_EINVAL;
@@ -111,6 +112,7 @@ int logan_xdrop_batch(const uint8_t *seq_pool, int32_t seq_fmt, int64_t pool_len
     P.one = 1;
     P.poison = (opt && (opt->flags & 2)) ? 1 : 0;
     P.nopack = (opt && (opt->flags & 16)) ? 1 : 0;
+    P.compat = (opt && (opt->flags & 32)) ? 1 : 0;
     P.subst = opt ? opt->subst : nullptr;
     P.alphabet = (opt && opt->subst) ? opt->alphabet : 0;
     P.stats = stats;
@@ -123,8 +125,9 @@ int logan_xdrop_batch(const uint8_t *seq_pool, int32_t seq_fmt, int64_t pool_len
     // Z-drop fires only if best - M_d > Z, and best - M_d <= X' on any antidiagonal
     // with a live cell: Z >= X' is the same as no Z-drop (header, zdrop)
     P.zdrop = (opt && (opt->flags & 4) && opt->zdrop < P.xdrop) ? opt->zdrop : -1;
-    // register windows keep X' <= 2^19 (argmax key range); beyond, the CTA level
-    const bool wide_only = P.xdrop > WINDOW_XMAX;
+    // register windows keep X' <= 2^19 (argmax key range); beyond, the CTA level;
+    // the SeqAn-compat mode is implemented on the CTA level only
+    const bool wide_only = P.xdrop > WINDOW_XMAX || P.compat;
 
     cudaStream_t s = (cudaStream_t)stream;
     uint8_t *ws = (uint8_t *)workspace;

@@ -32,6 +32,7 @@ struct Params {
     int32_t one;  // = 1 at run time; opaque to the compiler (see Window::cell)
     int32_t poison;  // test knob (options.flags bit 1): fill shared staging buffers with garbage first
     int32_t nopack;  // test knob (options.flags bit 4): int32 first window instead of the packed one
+    int32_t compat;  // options.flags bit 5: SeqAn-compat mode (readings c-amb-24/25; CTA level only)
     const int8_t *subst;  // NULL, or an alphabet x alphabet substitution matrix (device memory)
     int32_t alphabet;
     int32_t zdrop;        // Z-drop threshold (c-amb-19), < 0 = off

@@ -84,6 +84,7 @@ __global__ void __launch_bounds__(NT) k_wide(const Params P, const LevelIO io,
         int32_t *V0 = V[1], *V1 = V[0], *V2 = V[2];
         if (tid == 0) V1[0] = 0;  // origin S(0,0) = 0
         int32_t best = 0, ai = 0, aj = 0;
+        int32_t li = 0, ld = 0;  // compat: the origin unless a later antidiagonal has a live cell
         uint64_t cells = 0;
         __syncthreads();
 
@@ -120,7 +121,9 @@ __global__ void __launch_bounds__(NT) k_wide(const Params P, const LevelIO io,
                     const int32_t p = V1[i - 1];
                     if (p != WDEAD) { v = have ? max(v, p + P.gap) : p + P.gap; have = true; }
                 }
-                const bool live = have && v >= thr;  // drop iff S < best - X
+                // drop iff S < best - X; SeqAn-compat (reading c-amb-24): boundary
+                // cells (i = 0 or j = 0) on d >= 2 need S > best - X
+                const bool live = have && ((P.compat && d >= 2 && (i == 0 || j == 0)) ? v > thr : v >= thr);
                 V0[i] = live ? v : WDEAD;
                 if (live) {
                     lf = min(lf, i);
@@ -146,6 +149,7 @@ __global__ void __launch_bounds__(NT) k_wide(const Params P, const LevelIO io,
             const int32_t gl = __reduce_max_sync(0xffffffffu, q_ok ? s_l[par][lane] : INT32_MIN);
             const bool h0 = (gf != INT32_MAX);
             if (h0 && gv > best) { best = gv; ai = gi; aj = d - gi; }  // P:178, strict increase
+            if (h0) { li = gi; ld = d; }  // compat (c-amb-25): the last live antidiagonal's best cell
             if (h0 && P.zdrop >= 0) {  // Z-drop stop (c-amb-19)
                 const int32_t off = abs((gi - ai) - ((d - gi) - aj));
                 if (best - gv > P.zdrop - P.gap * off) break;
@@ -159,8 +163,8 @@ __global__ void __launch_bounds__(NT) k_wide(const Params P, const LevelIO io,
         if (tid == 0) {
             TaskRes tr;
             tr.best = best;
-            tr.i = ai;
-            tr.j = aj;
+            tr.i = P.compat ? li : ai;  // compat: the "longest extension" cell (c-amb-25)
+            tr.j = P.compat ? ld - li : aj;
             tr.flags = 0;
             tr.cells = cells;
             io.tres[task] = tr;

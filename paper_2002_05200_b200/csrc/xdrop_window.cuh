@@ -849,9 +849,10 @@ __global__ void __launch_bounds__(128, (G == 1 ? ((fmt_z(FMT) || fmt_base(FMT) =
         load_subst_tab(P, tab, threadIdx.x, blockDim.x);
         __syncthreads();
     }
-    // helpers: the last warp of the LAST io.helpers blocks (see the static first round below)
-    const bool helper = HR > 0 && (int)blockIdx.x >= (int)gridDim.x - io.helpers &&
-                        (threadIdx.x >> 5) == (blockDim.x >> 5) - 1;
+    // helpers: the warp that takes the LAST wave of the static first round (below)
+    // in the LAST io.helpers blocks, so the producers' static chunks are dense
+    const int hwarp = (io.sms > 0 && ((gridDim.x / (uint32_t)io.sms) & 1) == 0) ? 0 : (int)(blockDim.x >> 5) - 1;
+    const bool helper = HR > 0 && (int)blockIdx.x >= (int)gridDim.x - io.helpers && (int)(threadIdx.x >> 5) == hwarp;
     if (HR > 0 && helper) {
         constexpr int HG_ = HG > 0 ? HG : 32, HR_ = HR > 0 ? HR : 1;
         Window<HG_, HR_, FMT> w;
@@ -901,13 +902,15 @@ __global__ void __launch_bounds__(128, (G == 1 ? ((fmt_z(FMT) || fmt_base(FMT) =
     const int leader = lane - w.gl;
     // First level (io.sms > 0): a static first round spreads the LPT queue's head
     // over the SM sub-partitions. With blocks dispatched round-robin (block b on SM
-    // b mod #SM, warp w on sub-partition w), chunk c = (b mod #SM) + #SM * w +
-    // 4 #SM * (b div #SM) (32 / G tasks per warp) puts the longest 32/G-task chunks
-    // one per sub-partition before any doubles up -- what matters when the tasks
-    // are few (a strong-scaling share). The helpers (last warp of the last blocks)
-    // own the last chunk numbers, so the producers' chunks are dense. Later
+    // s = b mod #SM, block row r = b div #SM, warp w on sub-partition w), chunk
+    // c = s + #SM * k takes wave k = 4 r + (r even ? w : 3 - w) (32 / G tasks per
+    // warp): the longest #SM chunks go one per SM to sub-partition 0, the next to
+    // 1, ..., and the rows run serpentine so every sub-partition gets a balanced
+    // share of the long chunks -- what matters when the tasks are few (a
+    // strong-scaling share), harmless when they are many. The helpers own the
+    // last wave's last chunk numbers, so the producers' chunks are dense. Later
     // fetches take the dynamic cursor past the static region.
-    const int wib = threadIdx.x >> 5;
+    const uint32_t wib = threadIdx.x >> 5;
     const uint32_t gpw = 32 / G;  // groups per warp
     const uint32_t nprod = gridDim.x * (blockDim.x >> 5) - (uint32_t)io.helpers;  // producer warps
     const bool stat = io.sms > 0 && (gridDim.x % (uint32_t)io.sms) == 0 && (blockDim.x >> 5) == 4;
@@ -917,7 +920,9 @@ __global__ void __launch_bounds__(128, (G == 1 ? ((fmt_z(FMT) || fmt_base(FMT) =
         uint32_t p = 0xffffffffu;
         if (first) {
             first = false;
-            const uint32_t c = blockIdx.x % io.sms + io.sms * wib + 4u * io.sms * (blockIdx.x / io.sms);
+            const uint32_t r = blockIdx.x / io.sms;
+            const uint32_t k = 4u * r + ((r & 1u) ? 3u - wib : wib);
+            const uint32_t c = blockIdx.x % io.sms + io.sms * k;
             p = c * gpw + (uint32_t)(lane / G);
         } else {
             if (w.gl == 0) p = atomicAdd(io.cursor, 1u) + sbase;

@@ -285,9 +285,11 @@ struct Window16 {
         const uint32_t live = ~z & vmask & (H == 16 ? 0xffffffffu : ((1u << (2 * H)) - 1u));
         const uint32_t llo = live & 0x33333333u, lhi = live & 0xCCCCCCCCu;
         const bool h = live != 0;
-        const int pf = __ffs(llo ? llo : lhi) - 1, pl = 31 - __clz(lhi ? lhi : llo);
-        const int32_t f = (llo ? 0 : H) + ((pf & ~2) >> 1) + (pf & 1);
-        const int32_t l = (lhi ? H : 0) + ((pl & ~2) >> 1) + (pl & 1);
+        int32_t f, l;
+        if (llo) { const int p = __ffs(llo) - 1; f = (p >> 1) + (p & 1); }
+        else { const int p = __ffs(lhi) - 1; f = H + ((p - 2) >> 1) + (p & 1); }
+        if (lhi) { const int p = 31 - __clz(lhi); l = H + ((p - 2) >> 1) + (p & 1); }
+        else { const int p = 31 - __clz(llo); l = (p >> 1) + (p & 1); }
         st.sF[Qp] = h ? st.S0 + f : EMPTY_F;
         st.sL[Qp] = h ? st.S0 + l : EMPTY_L;
     }
@@ -442,20 +444,24 @@ struct Window16 {
     }
 
     // ---- window shifts (rare): in the split layout a shift by one slot moves
-    // whole words (both halves together), plus one PRMT at the seam
+    // whole words (both halves together), plus one PRMT at the seam. The words go
+    // through this thread's shared-memory slice so that the reloads land in the
+    // registers the arrays already occupy (a register rotation here makes the
+    // compiler copy both arrays on every step's common path)
     __device__ __forceinline__ void shift_slots(int by) {
+        volatile uint32_t *b = (volatile uint32_t *)sbase;
+#pragma unroll
+        for (int k = 0; k < H; ++k) { b[k] = E[k]; b[H + k] = O[k]; }
         if (by > 0) {  // new slot s = old slot s + 1
-            const uint32_t e0 = E[0], o0 = O[0];
 #pragma unroll
-            for (int k = 0; k < H - 1; ++k) { E[k] = E[k + 1]; O[k] = O[k + 1]; }
-            E[H - 1] = __byte_perm(e0, DEAD2, 0x5432);  // (old slot H, DEAD)
-            O[H - 1] = __byte_perm(o0, DEAD2, 0x5432);
+            for (int k = 0; k < H - 1; ++k) { E[k] = b[k + 1]; O[k] = b[H + k + 1]; }
+            E[H - 1] = __byte_perm(b[0], DEAD2, 0x5432);  // (old slot H, DEAD)
+            O[H - 1] = __byte_perm(b[H], DEAD2, 0x5432);
         } else {       // new slot s = old slot s - 1
-            const uint32_t eH = E[H - 1], oH = O[H - 1];
 #pragma unroll
-            for (int k = H - 1; k > 0; --k) { E[k] = E[k - 1]; O[k] = O[k - 1]; }
-            E[0] = __byte_perm(DEAD2, eH, 0x5410);  // (DEAD, old slot H - 1)
-            O[0] = __byte_perm(DEAD2, oH, 0x5410);
+            for (int k = 1; k < H; ++k) { E[k] = b[k - 1]; O[k] = b[H + k - 1]; }
+            E[0] = __byte_perm(DEAD2, b[H - 1], 0x5410);  // (DEAD, old slot H - 1)
+            O[0] = __byte_perm(DEAD2, b[2 * H - 1], 0x5410);
         }
     }
     __device__ __forceinline__ void shift_right(const Params &P, int32_t d) {

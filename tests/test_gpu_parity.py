@@ -712,3 +712,33 @@ def test_packed_first_window_equals_int32_window(cfg, X, lvl):
     ref = oracle.pairs(b.pool_2bit, 1, b.q_off[idx], b.q_len[idx], b.t_off[idx], b.t_len[idx], b.q_seed[idx],
                        b.t_seed[idx], w.k, 1, -1, -1, X, pool_len=b.pool_len)
     assert_same(res[0][0][idx], res[0][1][idx], *ref, what=f"packed vs oracle config {cfg} X={X}")
+
+
+# --------------------------------------------------------------------------
+# SeqAn-compat mode (options.flags bit 5; readings c-amb-24/25, CTA level)
+
+def test_compat_mode_matches_compat_oracle():
+    """Bit-exact against oracle.pairs_compat: random tiny and adversarial
+    pairs, C1, bursty C2 pairs (early drop-outs), with and without Z-drop."""
+    rng = random.Random(31)
+    pairs = []
+    for _ in range(300):
+        a = "".join(rng.choice("ACGT") for _ in range(rng.randint(1, 60)))
+        bb = "".join(ch if rng.random() > 0.2 else rng.choice("ACGT") for ch in a) if rng.random() < 0.6 else \
+            "".join(rng.choice("ACGT") for _ in range(rng.randint(1, 60)))
+        pairs.append((a, bb, rng.randint(0, len(a)), rng.randint(0, len(bb))))
+    batches = [datagen.from_strings(pairs, k=0), datagen.generate(datagen.CONFIGS[1], n_pairs=200),
+               datagen.generate(datagen.CONFIGS[2].with_(burst=0.5), n_pairs=150)]
+    for b in batches:
+        for X in (0, 2, 10, 50):
+            for Z in (None, 4):
+                ref = oracle.pairs_compat(b.pool_u8, 0, b.q_off, b.q_len, b.t_off, b.t_len, b.q_seed, b.t_seed,
+                                          b.workload.k, 1, -1, -1, X, -1 if Z is None else Z, pool_len=b.pool_len)
+                for fmt in FMTS:
+                    db = logan.to_device(b, fmt)
+                    st = logan.new_stats()
+                    out, cells = logan.xdrop_batch(db, 1, -1, -1, X, compat=True, zdrop=Z, stats=st)
+                    torch.cuda.synchronize()
+                    assert logan.stats_dict(st)["first_level"] == 8
+                    assert_same(out.cpu().numpy(), cells.cpu().numpy().view(np.uint64), *ref,
+                                what=f"compat X={X} Z={Z} fmt={fmt}")

@@ -349,3 +349,69 @@ def test_zdrop_truncates_the_xdrop_sweep():
         assert z.last_d <= full.last_d and z.best <= full.best and z.cells <= full.cells
         if z.last_d == full.last_d:
             assert z == full
+
+
+# ---------------------------------------------------------------------------
+# SeqAn-compat mode (oracle header step 6; [outside-PAPER] readings c-amb-24/25)
+
+def test_compat_golden(golden_dir):
+    """Hand-worked compat extensions (tests/golden/compat.tsv, DERIVATIONS.md):
+    C2 pins the strict boundary rule (the standard rule keeps (0,2) and reaches
+    (1,3)), all three the longest-extension end cell."""
+    rows = read_tsv(os.path.join(golden_dir, "compat.tsv"))
+    assert len(rows) >= 3
+    for (rid, A, B, X, ma, mi, g, best, i, j, cells, last_d) in rows:
+        r = oracle.extend_compat(A, B, int(X), int(ma), int(mi), int(g))
+        assert (r.best, r.i, r.j, r.cells, r.last_d) == (int(best), int(i), int(j), int(cells), int(last_d)), rid
+        assert oracle.extend_compat(A, B, int(X), int(ma), int(mi), int(g), full_scan=True) == r, rid
+    s = oracle.extend("A", "CCAA", 2)
+    assert (s.best, s.i, s.j, s.cells) == (0, 0, 0, 4)  # the standard rule on C2
+
+
+@pytest.mark.parametrize("scoring", [(1, -1, -1), (2, -3, -1)])
+def test_compat_infinite_x_ends_at_the_corner(scoring):
+    """X = inf: nothing drops, so the strict boundary rule changes nothing; best
+    and cells are the full DP's, and the longest extension is the corner (m, n),
+    the only cell of the last antidiagonal (an empty extension stays at (0,0))."""
+    ma, mi, g = scoring
+    for A in _all_strings("AC", 4):
+        for B in _all_strings("AC", 4):
+            r = oracle.extend_compat(A, B, INF, ma, mi, g)
+            assert (r.best, r.cells) == (full_dp_best(A, B, ma, mi, g)[0], len(A) * len(B))
+            assert (r.i, r.j) == ((len(A), len(B)) if A and B else (0, 0))  # empty extension: c-amb-13
+
+
+@pytest.mark.parametrize("X", [1, 2, 3, 6, 9])
+def test_compat_disjoint_alphabets(X):
+    """A-only vs C-only (S = -max(i,j)): best 0, the last live antidiagonal is 2X
+    holding only (X, X), cells (X+1)^2, as the standard rule."""
+    m = X + 7
+    r = oracle.extend_compat("A" * m, "C" * m, X)
+    assert (r.best, r.i, r.j, r.cells, r.last_d) == (0, X, X, (X + 1) ** 2, 2 * X + 2)
+
+
+def test_compat_cross_check_dict_reading():
+    """Second reading (not a pin): the dict-of-live-cells model with the compat rules."""
+    rng = random.Random(17)
+    for _ in range(1500):
+        A = "".join(rng.choice("ACGT") for _ in range(rng.randint(0, 10)))
+        B = "".join(rng.choice("ACGT") for _ in range(rng.randint(0, 10)))
+        X = rng.randint(0, 8)
+        ma, mi, g = rng.randint(1, 3), -rng.randint(1, 3), -rng.randint(1, 3)
+        r = oracle.extend_compat(A, B, X, ma, mi, g)
+        assert (r.best, r.i, r.j, r.cells) == xdrop_dict(A, B, X, ma, mi, g, compat=True), (A, B, X)
+
+
+def test_compat_pairs_assemble_extensions():
+    w = datagen.CONFIGS[1]
+    b = datagen.generate(w, n_pairs=24)
+    o, c = oracle.pairs_compat(b.pool_u8, 0, b.q_off, b.q_len, b.t_off, b.t_len, b.q_seed, b.t_seed, w.k,
+                               1, -1, -1, 50, pool_len=b.pool_len)
+    for p in range(6):
+        q = datagen.decode_2bit(b.pool_2bit, b.q_off[p], b.q_len[p]).decode()
+        t = datagen.decode_2bit(b.pool_2bit, b.t_off[p], b.t_len[p]).decode()
+        qs, ts, k = int(b.q_seed[p]), int(b.t_seed[p]), w.k
+        L = oracle.extend_compat(q[:qs][::-1], t[:ts][::-1], 50)
+        R = oracle.extend_compat(q[qs + k:], t[ts + k:], 50)
+        assert tuple(o[p]) == (k + L.best + R.best, qs - L.i, qs + k + R.i, ts - L.j, ts + k + R.j)
+        assert c[p] == L.cells + R.cells
