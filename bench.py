@@ -306,22 +306,27 @@ def run_reference(args):
 
 
 # --------------------------------------------------------------------------- roofline inputs
-def int_peak(sm_max_mhz):
-    """Peak int32 ALU-pipe ops/s of the B200: the measured per-SM per-clock
+def int_peak(sm_max_mhz, packed):
+    """Peak ALU-pipe integer ops/s of the B200: the measured per-SM per-clock
     throughput of the cell's ALU-pipe instructions (tools/int_peak.py,
-    profiles/int_peak.json) x 148 SMs x the max SM clock; without the file, the
-    guide's ALU pipe rate (16 lanes per SMSP, 64 per SM)."""
+    profiles/int_peak.json) x 148 SMs x the max SM clock -- for a kernel whose
+    cells run on packed .S16x2 DPX instructions (two lanes per instruction) the
+    16x2 peak ("must be stated with the 16x2 peak"), else the int32
+    one. Without the file, the guide's ALU pipe rate (16 lanes per SMSP, 64 per
+    SM; doubled for 16x2). Returns (peak TOP/s, derivation, int32 peak TOP/s)."""
     try:
         pk = json.load(open(PEAK_FILE))
-        lanes = float(pk["alu_int32_ops_per_clk_per_sm"])
-        how = (f"{B200_SMS} SMs x {lanes:.1f} int32 ALU ops/clk/SM (measured: {pk.get('source', PEAK_FILE)}) "
-               f"x {sm_max_mhz:.0f} MHz")
-        extra = {k: pk[k] for k in ("s16x2_ops_per_clk_per_sm", "issue_inst_per_clk_per_sm") if k in pk}
+        l32 = float(pk["alu_int32_ops_per_clk_per_sm"])
+        l16 = float(pk["s16x2_ops_per_clk_per_sm"])
+        src = f"measured: {pk.get('source', PEAK_FILE)}"
     except (OSError, ValueError, KeyError):
-        lanes = 64.0
-        how = f"{B200_SMS} SMs x 64 int32 lanes/clk (derived: 4 SMSPs x 16-lane ALU pipe) x {sm_max_mhz:.0f} MHz"
-        extra = {}
-    return B200_SMS * lanes * sm_max_mhz * 1e6 / 1e12, how, extra
+        l32, l16 = 64.0, 128.0
+        src = "derived: 4 SMSPs x 16-lane ALU pipe"
+    lanes = l16 if packed else l32
+    how = (f"{B200_SMS} SMs x {lanes:.1f} {'16x2 lane-ops' if packed else 'int32 ops'}/clk/SM on the ALU pipe "
+           f"({src}) x {sm_max_mhz:.0f} MHz")
+    f = B200_SMS * sm_max_mhz * 1e6 / 1e12
+    return lanes * f, how, l32 * f
 
 
 def ncu_evidence(key):
@@ -461,7 +466,11 @@ def main(argv=None):
     dom_ms = stage_ms[dom_stage] / args.steps
     dom_cells = stats["cells_per_level"][dom_level]
     sm_max = clocks.get("sm_max_mhz") or 1965.0
-    peak_tops, peak_how, peak_extra = int_peak(sm_max)
+    # the packed int16 kernels: the first window of a 2-bit pool at X <= 16000 (no
+    # Z-drop; options.flags bit 4 off) and the band level
+    packed = (dom_level == 0 and fmt == logan.LOGAN_SEQ_2BIT and w.xdrop <= 16000 and args.zdrop is None
+              and not protein) or dom_level == 6
+    peak_tops, peak_how, peak32 = int_peak(sm_max, packed)
     achieved_tops = N_REF_OPS_PER_CELL * dom_cells / (dom_ms / 1e3) / 1e12
     # the library picks window widths from X (from ceil(X / |gap|) with a substitution matrix)
     xband = -(-w.xdrop // -w.gap) if subst is not None else w.xdrop
@@ -476,7 +485,8 @@ def main(argv=None):
                           f"level {dom_level + 1} ({level_names[dom_level]})",
                 "kernel_ms": dom_ms, "kernel_share_of_step": dom_ms / (total_ms / args.steps),
                 "ops_per_cell": N_REF_OPS_PER_CELL, "cells_per_launch": dom_cells,
-                "peak_derivation": peak_how, **peak_extra}
+                "peak_derivation": peak_how, "packed_16x2": packed,
+                "frac_vs_int32_alu_peak": achieved_tops / peak32}
     if ev_ncu:
         roofline["ncu"] = {k: ev_ncu[k] for k in ("sass_thread_inst_per_cell", "int_thread_inst_per_cell",
                                                   "int_warp_gips", "alu_pipe_pct", "fma_pipe_pct", "issue_pct",

@@ -214,6 +214,13 @@ static __global__ void k_combine(const Params P, const TaskRes *tres, logan_resu
 #else
 #define LOGAN_HSHAPE(W) 32, ((W) / 32)
 #endif
+// helpers of the packed first window (A/B knob): 4 x 16 instead of 2 x 32 fits the
+// kernel into 128 registers (4 blocks per SM with LOGAN_PK_MINB 4), but measured
+// slower (C3 1309-1323 vs 1345 GCUPS, C2 1231 vs 1275: half the helper capacity
+// leaves a level-2 tail, and 16 warps per SM do not raise the ALU-bound rate)
+#ifndef LOGAN_PK_HSHAPE
+#define LOGAN_PK_HSHAPE LOGAN_HSHAPE(64)
+#endif
 
 template <int G, int R, int FMT, int HG, int HR, bool PK = false>
 static cudaError_t launch_win(const Params &P, const LevelIO &io_in, const LevelIO &hio, int sms, cudaStream_t s) {
@@ -248,15 +255,15 @@ static cudaError_t launch_first(int w0, bool helpers, const Params &P, const Lev
     if constexpr (FMT == LOGAN_SEQ_2BIT) {
         if (P.xdrop <= PACK_XMAX && !P.nopack) {
             switch (w0) {
-                case 16: return helpers ? launch_win<1, 16, FMT, LOGAN_HSHAPE(64), true>(P, io, hio, sms, s)
+                case 16: return helpers ? launch_win<1, 16, FMT, LOGAN_PK_HSHAPE, true>(P, io, hio, sms, s)
                                         : launch_win<1, 16, FMT, 0, 0, true>(P, io, hio, sms, s);
-                case 20: return helpers ? launch_win<1, 20, FMT, LOGAN_HSHAPE(64), true>(P, io, hio, sms, s)
+                case 20: return helpers ? launch_win<1, 20, FMT, LOGAN_PK_HSHAPE, true>(P, io, hio, sms, s)
                                         : launch_win<1, 20, FMT, 0, 0, true>(P, io, hio, sms, s);
-                case 24: return helpers ? launch_win<1, 24, FMT, LOGAN_HSHAPE(64), true>(P, io, hio, sms, s)
+                case 24: return helpers ? launch_win<1, 24, FMT, LOGAN_PK_HSHAPE, true>(P, io, hio, sms, s)
                                         : launch_win<1, 24, FMT, 0, 0, true>(P, io, hio, sms, s);
-                case 28: return helpers ? launch_win<1, 28, FMT, LOGAN_HSHAPE(64), true>(P, io, hio, sms, s)
+                case 28: return helpers ? launch_win<1, 28, FMT, LOGAN_PK_HSHAPE, true>(P, io, hio, sms, s)
                                         : launch_win<1, 28, FMT, 0, 0, true>(P, io, hio, sms, s);
-                default: return helpers ? launch_win<1, 32, FMT, LOGAN_HSHAPE(64), true>(P, io, hio, sms, s)
+                default: return helpers ? launch_win<1, 32, FMT, LOGAN_PK_HSHAPE, true>(P, io, hio, sms, s)
                                         : launch_win<1, 32, FMT, 0, 0, true>(P, io, hio, sms, s);
             }
         }

@@ -68,6 +68,10 @@ constexpr int32_t KNONE = INT32_MIN;  // "no pending maximum" (below every raise
 #ifndef LOGAN_L0_MINB
 #define LOGAN_L0_MINB 1
 #endif
+// the same for the packed first window (Window16; see LOGAN_PK_HSHAPE)
+#ifndef LOGAN_PK_MINB
+#define LOGAN_PK_MINB 1
+#endif
 
 #ifndef LOGAN_NCHAIN
 #define LOGAN_NCHAIN 4
@@ -832,7 +836,8 @@ template <int R, int FMT> struct Window16;  // xdrop_window16.cuh
 
 // PK: the producers run the packed int16 window (Window16, one lane per task)
 template <int G, int R, int FMT, int HG, int HR, bool PK = false>
-__global__ void __launch_bounds__(128, (G == 1 ? ((fmt_z(FMT) || fmt_base(FMT) == FMT_U8S) ? 3 : LOGAN_L0_MINB) : 1))
+__global__ void __launch_bounds__(128, (PK ? LOGAN_PK_MINB : (G == 1 ? ((fmt_z(FMT) || fmt_base(FMT) == FMT_U8S) ? 3
+                                                                                    : LOGAN_L0_MINB) : 1)))
     k_window(const Params P, const LevelIO io, const LevelIO hio) {
     using PW = typename std::conditional<PK, Window16<R, FMT>, Window<G, R, FMT>>::type;
     const uint32_t count = *io.count;
