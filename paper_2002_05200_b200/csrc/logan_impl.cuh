@@ -286,6 +286,37 @@ template <int FMT>
 static cudaError_t launch_width(int wi, bool latency, bool helpers, const Params &P, const LevelIO &io,
                                 const LevelIO &hio, int sms, cudaStream_t s, int w0, int w5) {
     if (wi == 0 && !(latency && w0 == 32)) return launch_first<FMT>(w0, helpers && !latency, P, io, hio, sms, s);
+    // 2-bit pools (no Z-drop) at X <= 16000: the packed int16 windows for the
+    // throughput shapes (G x 32 slots) and the one-warp shapes with >= 16 slots per lane
+    if constexpr (FMT == LOGAN_SEQ_2BIT) {
+        if (P.xdrop <= PACK_XMAX && !P.nopack) {
+            if (helpers && !latency) switch (wi) {
+                case 1: return launch_win<2, 32, FMT, LOGAN_HSHAPE(128), true>(P, io, hio, sms, s);
+                case 2: return launch_win<4, 32, FMT, LOGAN_HSHAPE(256), true>(P, io, hio, sms, s);
+                case 3: return launch_win<8, 32, FMT, LOGAN_HSHAPE(512), true>(P, io, hio, sms, s);
+                case 4:
+                    if (w5 == 640) return launch_win<16, 32, FMT, 32, 20, true>(P, io, hio, sms, s);
+                    if (w5 == 768) return launch_win<16, 32, FMT, 32, 24, true>(P, io, hio, sms, s);
+                    if (w5 == 896) return launch_win<16, 32, FMT, 32, 28, true>(P, io, hio, sms, s);
+                    return launch_win<16, 32, FMT, 32, 32, true>(P, io, hio, sms, s);
+                default: break;
+            }
+            if (wi == 5) {
+                if (w5 == 640) return launch_win<32, 20, FMT, 0, 0, true>(P, io, hio, sms, s);
+                if (w5 == 768) return launch_win<32, 24, FMT, 0, 0, true>(P, io, hio, sms, s);
+                if (w5 == 896) return launch_win<32, 28, FMT, 0, 0, true>(P, io, hio, sms, s);
+                return launch_win<32, 32, FMT, 0, 0, true>(P, io, hio, sms, s);
+            }
+            switch (wi * 2 + (latency ? 1 : 0)) {
+                case 2: return launch_win<2, 32, FMT, 0, 0, true>(P, io, hio, sms, s);
+                case 4: return launch_win<4, 32, FMT, 0, 0, true>(P, io, hio, sms, s);
+                case 6: return launch_win<8, 32, FMT, 0, 0, true>(P, io, hio, sms, s);
+                case 8: return launch_win<16, 32, FMT, 0, 0, true>(P, io, hio, sms, s);
+                case 9: return launch_win<32, 16, FMT, 0, 0, true>(P, io, hio, sms, s);
+                default: break;  // one-warp shapes with fewer than 16 slots per lane: int32
+            }
+        }
+    }
     constexpr bool HELP = true;
     if (HELP && helpers && !latency) {
         if constexpr (HELP) switch (wi) {

@@ -832,14 +832,14 @@ __device__ __forceinline__ void run_group(Win &w, const Params &P, const LevelIO
 // overflowing tasks then finish while this level is still running instead of
 // forming a serial tail after it. What the helpers do not take, the next
 // level's own launch does (it shares their cursor).
-template <int R, int FMT> struct Window16;  // xdrop_window16.cuh
+template <int G, int R, int FMT> struct Window16;  // xdrop_window16.cuh
 
-// PK: the producers run the packed int16 window (Window16, one lane per task)
+// PK: the producers run the packed int16 window (Window16)
 template <int G, int R, int FMT, int HG, int HR, bool PK = false>
-__global__ void __launch_bounds__(128, (PK ? LOGAN_PK_MINB : (G == 1 ? ((fmt_z(FMT) || fmt_base(FMT) == FMT_U8S) ? 3
-                                                                                    : LOGAN_L0_MINB) : 1)))
+__global__ void __launch_bounds__(128, (PK ? (G == 1 ? LOGAN_PK_MINB : 3)
+                                           : (G == 1 ? ((fmt_z(FMT) || fmt_base(FMT) == FMT_U8S) ? 3 : LOGAN_L0_MINB) : 1)))
     k_window(const Params P, const LevelIO io, const LevelIO hio) {
-    using PW = typename std::conditional<PK, Window16<R, FMT>, Window<G, R, FMT>>::type;
+    using PW = typename std::conditional<PK, Window16<G, R, FMT>, Window<G, R, FMT>>::type;
     const uint32_t count = *io.count;
     const uint32_t taken = *io.cursor;  // entries already taken (by in-kernel helpers)
     const uint32_t remaining = count - (taken < count ? taken : count);

@@ -1,8 +1,10 @@
-// xdrop_window16.cuh — the first-level register window with PACKED int16
-// pairs: one lane per task, W = R slots (R in {16, 20, 24, 28, 32}), 2-bit
-// pools, X <= 16000. The sweep is the one of xdrop_window.cuh (same method
-// citations, same pipelined "kill one antidiagonal late" state, same hand-over
-// records); only the per-slot arithmetic differs.
+// xdrop_window16.cuh — register windows with PACKED int16 pairs: G lanes per
+// task, R slots per lane (R in {16, 20, 24, 28, 32}), W = G * R, 2-bit pools,
+// X <= 16000. The first level (G = 1) and the throughput shapes of levels 2-5
+// (G = W / 32, R = 32) and the wide latency shapes (one warp, R >= 16). The
+// sweep is the one of xdrop_window.cuh (same method citations, same pipelined
+// "kill one antidiagonal late" state, same hand-over records); only the
+// per-slot arithmetic differs.
 //
 // Why: the int32 window is bound by instruction issue (~88
 // thread-instructions per SM clock, the practical limit measured by
@@ -10,10 +12,11 @@
 // (VIMNMX3.S16x2, VIADDMNMX.S16x2, VIADDMNMX.U16x2; VIADD.16x2 issues on the
 // FMA side) about halves the instructions per slot.
 //
-// Layout ("split pairs"): word k of E / O holds slot k in its low half and slot
-// k + H in its high half (H = R/2). Slot s's neighbours s+1 and s-1 are then
-// the next / previous WORD (both halves move together), so a cell pair needs
-// no realignment, except at the one seam word per step (one PRMT).
+// Layout ("split pairs"): word k of a lane's E / O holds its slot k in the low
+// half and slot k + H in the high half (H = R/2). Slot s's neighbours s+1 and
+// s-1 are then the next / previous WORD (both halves move together), so a cell
+// pair needs no realignment, except at the one seam word per step (one PRMT,
+// with one SHFL from the neighbouring lane when G > 1).
 // Values are int16 relative to the thresholds (live u <= X + 3*127 < 2^15,
 // DEAD16 = -16384, dead values stay in [DEAD16 - 3*127, DEAD16]).
 //
@@ -48,11 +51,11 @@ __device__ __forceinline__ uint32_t pk2(int32_t v) { return ((uint32_t)v & 0xfff
 __device__ __forceinline__ int32_t lo16(uint32_t w) { return (int32_t)(int16_t)(w & 0xffffu); }
 __device__ __forceinline__ int32_t hi16(uint32_t w) { return ((int32_t)w) >> 16; }
 
-template <int R, int FMT>
+template <int G, int R, int FMT>
 struct Window16 {
     static_assert(FMT == LOGAN_SEQ_2BIT, "packed window: 2-bit pools");
-    static_assert(R % 4 == 0 && R >= 16 && R <= 32, "packed window shape");
-    static constexpr int GG = 1, W = R, H = R / 2;
+    static_assert(R % 4 == 0 && R >= 16 && R <= 32 && (G & (G - 1)) == 0 && G * R <= 1024, "packed window shape");
+    static constexpr int GG = G, W = G * R, H = R / 2;
     static constexpr int CB = 4, FPW = 8;
     static constexpr int NW = (R + FPW - 1) / FPW;
     static constexpr int RL = R - (NW - 1) * FPW;
@@ -91,17 +94,18 @@ struct Window16 {
         if (RL < FPW) w[NW - 1] &= (1u << (CB * (RL < FPW ? RL : 0))) - 1u;
     }
     __device__ __forceinline__ void load_bases(const Params &P) {
+        const int32_t s0 = st.S0 + gl * R;
         const int32_t ch = ceil_half(st.d), fh = floor_half(st.d);
 #pragma unroll
         for (int q = 0; q < NW; ++q) { Aw[q] = 0; Bw[q] = 0; }
-        st.sa.seek(P, st.S0 + ch);
+        st.sa.seek(P, s0 + ch);
 #pragma unroll 1
         for (int r = 0; r < R; ++r) shift_down(Aw, st.sa.next(P, SA));
-        st.sb.seek(P, fh - (st.S0 + R - 1));
+        st.sb.seek(P, fh - (s0 + R - 1));
 #pragma unroll 1
         for (int r = R - 1; r >= 0; --r) shift_up(Bw, st.sb.next(P, SB));
-        st.sa.seek(P, st.S0 + W + ch);
-        st.sb.seek(P, fh - st.S0 + 1);
+        if (gl == G - 1) st.sa.seek(P, st.S0 + W + ch);  // sa.idx = S0 + W + ceil(d/2)
+        if (gl == 0) st.sb.seek(P, fh - st.S0 + 1);      // sb.idx = floor(d/2) - S0 + 1
     }
 
     // ---- task start / hand-over (canonical records, int32 per slot) -----------
@@ -111,7 +115,7 @@ struct Window16 {
         st.m = td.a.len;
         st.n = td.b.len;
         st.d = 0;
-        st.S0 = -(W / 2);  // the origin is slot H: the high half of word 0
+        st.S0 = -(W / 2);
         st.best = 0;
         st.arg_i = st.arg_j = 0;
         st.Tq[0] = st.Tq[1] = -P.xdrop;
@@ -124,9 +128,14 @@ struct Window16 {
         st.shifts = 0;
         st.cells_entry = 0;
         cd = -1;
+        // the origin is window slot W/2: lane (W/2) / R, local slot (W/2) % R
+        constexpr int OL = (W / 2) / R, OS = (W / 2) % R;
 #pragma unroll
         for (int k = 0; k < H; ++k) {
-            E[k] = k == 0 ? ((uint32_t)P.xdrop << 16) | (uint32_t)(DEAD16 & 0xffff) : DEAD2;
+            const bool here = gl == OL && k == OS % H;
+            const uint32_t xo = OS < H ? ((uint32_t)(DEAD16 & 0xffff) << 16) | ((uint32_t)P.xdrop & 0xffffu)
+                                       : ((uint32_t)P.xdrop << 16) | (uint32_t)(DEAD16 & 0xffff);
+            E[k] = here ? xo : DEAD2;
             O[k] = DEAD2;
         }
         st.sa.s = td.a;
@@ -138,10 +147,11 @@ struct Window16 {
     // holding the maximum): once per task, at its end or hand-over
     __device__ __forceinline__ void finalize() {
         if (cd < 0) return;
-        int s = R - 1;  // the maximum is in the copy: the smallest slot holding it
+        int s = INT32_MAX;  // the maximum is in the copy: the smallest slot holding it
 #pragma unroll
         for (int q = R - 1; q >= 0; --q)
-            if (get(C, q) == tv) s = q;
+            if (get(C, q) == tv) s = gl * R + q;
+        if (G > 1) s = grp_min<G>(s, gmask);
         st.arg_i = cS0 + s + ceil_half(cd);
         st.arg_j = cd - st.arg_i;
         cd = -1;
@@ -153,9 +163,10 @@ struct Window16 {
         const int p = d & 1;
 #pragma unroll
         for (int s = 0; s < R; ++s) {  // (unrolled: a run-time index would put the arrays in local memory)
-            rec[REC_HDR + s] = get(E, s);
-            rec[REC_HDR + W + s] = get(O, s);
+            rec[REC_HDR + gl * R + s] = get(E, s);
+            rec[REC_HDR + W + gl * R + s] = get(O, s);
         }
+        if (gl != 0) return;
         rec[0] = (int32_t)st.task; rec[1] = d; rec[2] = st.S0; rec[3] = st.best;
         rec[4] = st.arg_i; rec[5] = st.arg_j;
         rec[6] = st.best - P.xdrop;
@@ -209,7 +220,7 @@ struct Window16 {
         const int32_t rb = Td - Td1;
 #pragma unroll
         for (int s = 0; s < R; ++s) {
-            const int32_t q = st.S0 + s - S0src;
+            const int32_t q = st.S0 + gl * R + s - S0src;
             const bool in = q >= 0 && q < Wsrc;
             int32_t ve = in ? rec[REC_HDR + q] : DEAD;
             int32_t vo = in ? rec[REC_HDR + Wsrc + q] : DEAD;
@@ -274,22 +285,28 @@ struct Window16 {
         const uint32_t z = dead_z(a);
         const int32_t chq = e >> 1, fhq = (e - 1) >> 1;  // ceil((e-1)/2), floor((e-1)/2)
         const int32_t vlo = fhq - st.n, vhi = st.m - chq;
+        const int32_t base = st.S0 + gl * R;
         uint32_t vmask = 0xffffffffu;
-        if (vlo > st.S0 || vhi < st.S0 + R - 1) {  // near the matrix edges
+        if (vlo > base || vhi < base + R - 1) {  // near the matrix edges
             // valid slots [rlo, rhi] as a slot-order mask, then spread to the z
             // layout (bit s -> 4(s>>1) + (s&1) for s < H, 4((s-H)>>1) + 2 + ((s-H)&1))
-            const int32_t rlo = max(vlo - st.S0, 0), rhi = min(vhi - st.S0, R - 1);
+            const int32_t rlo = max(vlo - base, 0), rhi = min(vhi - base, R - 1);
             const uint32_t m = (rlo <= rhi) ? ((0xffffffffu >> (31 - rhi)) & ~((1u << rlo) - 1u)) : 0u;
             vmask = spread2(m & ((1u << H) - 1u)) | (spread2(m >> H) << 2);
         }
         const uint32_t live = ~z & vmask & (H == 16 ? 0xffffffffu : ((1u << (2 * H)) - 1u));
         const uint32_t llo = live & 0x33333333u, lhi = live & 0xCCCCCCCCu;
-        const bool h = live != 0;
+        bool h = live != 0;
         int32_t f, l;
         if (llo) { const int p = __ffs(llo) - 1; f = (p >> 1) + (p & 1); }
         else { const int p = __ffs(lhi) - 1; f = H + ((p - 2) >> 1) + (p & 1); }
         if (lhi) { const int p = 31 - __clz(lhi); l = H + ((p - 2) >> 1) + (p & 1); }
         else { const int p = 31 - __clz(llo); l = (p >> 1) + (p & 1); }
+        if (G > 1) {  // group extremes (sentinels for lanes without a live slot)
+            f = grp_min<G>(h ? gl * R + f : INT32_MAX, gmask);
+            l = grp_max<G>(h ? gl * R + l : INT32_MIN, gmask);
+            h = f != INT32_MAX;
+        }
         st.sF[Qp] = h ? st.S0 + f : EMPTY_F;
         st.sL[Qp] = h ? st.S0 + l : EMPTY_L;
     }
@@ -330,8 +347,12 @@ struct Window16 {
             // e-1's by at most one slot on each side, which only makes this test
             // more eager (the exact decision below is unaffected)
             const uint32_t lo0 = E[0] & O[0], hiR = E[H - 1] & O[H - 1];
-            const bool in0 = st.S0 >= ((e - 1) >> 1) - st.n, inR = st.S0 + R - 1 <= st.m - (e >> 1);
-            if (force || (!(lo0 & 0x8000u) && in0) || (!(hiR & 0x80000000u) && inR)) {
+            const bool in0 = st.S0 >= ((e - 1) >> 1) - st.n, inR = st.S0 + W - 1 <= st.m - (e >> 1);
+            bool edge = (gl == 0 && !(lo0 & 0x8000u) && in0) || (gl == G - 1 && !(hiR & 0x80000000u) && inR);
+            // (a shuffle, not a ballot: __ballot_sync over a per-group mask compiles to
+            //  WARPSYNC.EXCLUSIVE, which serialises the groups of the warp)
+            if (G > 1) edge = (__shfl_sync(gmask, int(edge), 0, G) | __shfl_sync(gmask, int(edge), G - 1, G)) != 0;
+            if (force || edge) {
                 extremes<Q>(e, E);
                 if (st.sF[0] == EMPTY_F && st.sF[1] == EMPTY_F) return 1;  // P:186, c-amb-7
                 bool ho = force;
@@ -357,9 +378,20 @@ struct Window16 {
             }
         }
 
-        // (e) bases for antidiagonal e
-        if (PAR == 1) shift_down(Aw, st.sa.next_fast(SA));
-        else shift_up(Bw, st.sb.next_fast(SB));
+        // (e) bases for antidiagonal e (lane G-1 reads the A stream, lane 0 the B one)
+        if (PAR == 1) {
+            uint32_t in = 0;
+            if (G > 1) in = __shfl_down_sync(gmask, Aw[0], 1, G) & FM;
+            const uint32_t x = st.sa.next_fast(SA);
+            if (gl == G - 1) in = x;
+            shift_down(Aw, in);
+        } else {
+            uint32_t in = 0;
+            if (G > 1) in = __shfl_up_sync(gmask, top_field(Bw), 1, G);
+            const uint32_t x = st.sb.next_fast(SB);
+            if (gl == 0) in = x;
+            shift_up(Bw, in);
+        }
 
         // (f) raw cells of e (relative to T_{e-1}), two slots per instruction
         const uint32_t gap2 = pk2(P.gap);
@@ -374,6 +406,12 @@ struct Window16 {
             asm("mad.lo.u32 %0, %1, %2, %3;" : "=r"(Y[q]) : "r"(Aw[q] ^ Bw[q]), "r"(one), "r"(0x77777777u));
             asm("mad.lo.u32 %0, %1, %2, 0;" : "=r"(Yl[q]) : "r"(Y[q]), "r"(sixteen));
         }
+        // the seam words' neighbours from the adjacent lanes (DEAD beyond the window)
+        uint32_t nbr = DEAD2;
+        if (G > 1) {
+            if (PAR == 1) { nbr = __shfl_down_sync(gmask, E[0], 1, G); if (gl == G - 1) nbr = DEAD2; }
+            else { nbr = __shfl_up_sync(gmask, O[H - 1], 1, G); if (gl == 0) nbr = DEAD2; }
+        }
 #pragma unroll
         for (int k = 0; k < H; ++k) {
             // mismatch masks of slots k (low half) and k + H (high half)
@@ -387,12 +425,14 @@ struct Window16 {
             asm("lop3.b32 %0, %1, %2, %3, 0xCA;" : "=r"(s2) : "r"(mask2), "r"(smi2), "r"(sma2));
             uint32_t up, left, diag;
             if (PAR == 1) {  // odd e: up = E[s+1], left = E[s], diag = O[s]
-                up = (k < H - 1) ? E[k + 1] : __byte_perm(E[0], DEAD2, 0x5432);
+                // seam: (slot H of this lane, slot 0 of the next lane)
+                up = (k < H - 1) ? E[k + 1] : __byte_perm(E[0], nbr, 0x5432);
                 left = E[k];
                 diag = O[k];
             } else {         // even e: up = O[s], left = O[s-1], diag = E[s]
                 up = O[k];
-                left = (k > 0) ? O[k - 1] : __byte_perm(DEAD2, O[H - 1], 0x5410);
+                // seam: (slot R-1 of the previous lane, slot H-1 of this lane)
+                left = (k > 0) ? O[k - 1] : __byte_perm(nbr, O[H - 1], 0x5432);
                 diag = E[k];
             }
             const uint32_t t0 = __vimax3_s16x2(up, left, fg2);
@@ -419,7 +459,9 @@ struct Window16 {
 #pragma unroll
         for (int q = 1; q < NM; q += 2)
             m2 = __vimax3_s16x2(m2, mx[q], (q + 1 < NM) ? mx[q + 1] : mx[q]);
-        st.K[PAR] = max(lo16(m2), hi16(m2));
+        int32_t kmx = max(lo16(m2), hi16(m2));
+        if (G > 1) kmx = grp_max<G>(kmx, gmask);
+        st.K[PAR] = kmx;
 
         // (b') live extremes of e-1 (band bookkeeping, off the cells' critical path)
         if (PAR) extremes<Q>(e, E);
@@ -449,26 +491,45 @@ struct Window16 {
     // registers the arrays already occupy (a register rotation here makes the
     // compiler copy both arrays on every step's common path)
     __device__ __forceinline__ void shift_slots(int by) {
+        uint32_t ne = DEAD2, no = DEAD2;  // the adjacent lane's word entering at the seam
+        if (G > 1) {
+            if (by > 0) {
+                ne = __shfl_down_sync(gmask, E[0], 1, G);
+                no = __shfl_down_sync(gmask, O[0], 1, G);
+                if (gl == G - 1) ne = no = DEAD2;
+            } else {
+                ne = __shfl_up_sync(gmask, E[H - 1], 1, G);
+                no = __shfl_up_sync(gmask, O[H - 1], 1, G);
+                if (gl == 0) ne = no = DEAD2;
+            }
+        }
         volatile uint32_t *b = (volatile uint32_t *)sbase;
 #pragma unroll
         for (int k = 0; k < H; ++k) { b[k] = E[k]; b[H + k] = O[k]; }
         if (by > 0) {  // new slot s = old slot s + 1
 #pragma unroll
             for (int k = 0; k < H - 1; ++k) { E[k] = b[k + 1]; O[k] = b[H + k + 1]; }
-            E[H - 1] = __byte_perm(b[0], DEAD2, 0x5432);  // (old slot H, DEAD)
-            O[H - 1] = __byte_perm(b[H], DEAD2, 0x5432);
+            E[H - 1] = __byte_perm(b[0], ne, 0x5432);  // (old slot H, the next lane's old slot 0)
+            O[H - 1] = __byte_perm(b[H], no, 0x5432);
         } else {       // new slot s = old slot s - 1
 #pragma unroll
             for (int k = 1; k < H; ++k) { E[k] = b[k - 1]; O[k] = b[H + k - 1]; }
-            E[0] = __byte_perm(DEAD2, b[H - 1], 0x5410);  // (DEAD, old slot H - 1)
-            O[0] = __byte_perm(DEAD2, b[2 * H - 1], 0x5410);
+            E[0] = __byte_perm(ne, b[H - 1], 0x5432);  // (the previous lane's old slot R-1, old slot H-1)
+            O[0] = __byte_perm(no, b[2 * H - 1], 0x5432);
         }
     }
     __device__ __forceinline__ void shift_right(const Params &P, int32_t d) {
+        uint32_t aIn = 0, bIn = 0;
+        if (G > 1) {
+            aIn = __shfl_down_sync(gmask, Aw[0], 1, G) & FM;
+            bIn = __shfl_down_sync(gmask, Bw[0], 1, G) & FM;
+        }
         const int32_t S1 = st.S0 + 1;
-        const uint32_t aIn = st.sa.next(P, SA);
-        const uint32_t bIn = seq_at<FMT>(P, st.sb.s, floor_half(d) - S1 - (W - 1), SB);
-        st.sb.seek(P, st.sb.idx - 1);
+        if (gl == G - 1) {
+            aIn = st.sa.next(P, SA);  // a_{S1 + W - 1 + ceil(d/2)}
+            bIn = seq_at<FMT>(P, st.sb.s, floor_half(d) - S1 - (W - 1), SB);
+        }
+        if (gl == 0) st.sb.seek(P, st.sb.idx - 1);  // b stream steps back one base
         shift_slots(+1);
         shift_down(Aw, aIn);
         shift_down(Bw, bIn);
@@ -476,10 +537,17 @@ struct Window16 {
         ++st.shifts;
     }
     __device__ __forceinline__ void shift_left(const Params &P, int32_t d) {
+        uint32_t aIn = 0, bIn = 0;
+        if (G > 1) {
+            aIn = __shfl_up_sync(gmask, top_field(Aw), 1, G);
+            bIn = __shfl_up_sync(gmask, top_field(Bw), 1, G);
+        }
         const int32_t S1 = st.S0 - 1;
-        const uint32_t aIn = seq_at<FMT>(P, st.sa.s, S1 + ceil_half(d), SA);
-        const uint32_t bIn = st.sb.next(P, SB);
-        st.sa.seek(P, st.sa.idx - 1);
+        if (gl == 0) {
+            aIn = seq_at<FMT>(P, st.sa.s, S1 + ceil_half(d), SA);
+            bIn = st.sb.next(P, SB);  // b_{floor(d/2) - S1}
+        }
+        if (gl == G - 1) st.sa.seek(P, st.sa.idx - 1);  // a stream steps back one base
         shift_slots(-1);
         shift_up(Aw, aIn);
         shift_up(Bw, bIn);

@@ -693,12 +693,14 @@ def test_partition_independence_multi_device_wrapper():
 
 
 @pytest.mark.parametrize("cfg,X,lvl", [(2, 5, None), (2, 12, None), (2, 20, None), (3, 20, None), (2, 60, 1),
-                                       (6, 300, 1), (2, 20, 1)])
+                                       (6, 300, 1), (2, 20, 1), (2, 50, None), (2, 100, None), (6, 200, None),
+                                       (6, 400, None), (4, 50, None), (2, 30, 2)])
 def test_packed_first_window_equals_int32_window(cfg, X, lvl):
-    """The packed int16 first window (2-bit pools, X <= 16000) against the
-    int32 window (options.flags bit 4) on every pair, and both against the
-    oracle on a sample; forced level 1 at large X makes most tasks overflow
-    (hand-over records written from the packed layout)."""
+    """The packed int16 windows (2-bit pools, X <= 16000: level 1 and the
+    throughput shapes of levels 2-5) against the int32 windows (options.flags
+    bit 4) on every pair, and both against the oracle on a sample; a forced low
+    first level at large X makes most tasks overflow (hand-over records written
+    from and read into the packed layout)."""
     w = datagen.CONFIGS[cfg].with_(xdrop=X)
     b = datagen.generate(w, n_pairs=20000 if cfg != 3 else 4000, u8=False)
     db = logan.to_device(b, logan.LOGAN_SEQ_2BIT)
@@ -742,3 +744,23 @@ def test_compat_mode_matches_compat_oracle():
                     assert logan.stats_dict(st)["first_level"] == 8
                     assert_same(out.cpu().numpy(), cells.cpu().numpy().view(np.uint64), *ref,
                                 what=f"compat X={X} Z={Z} fmt={fmt}")
+
+
+@pytest.mark.parametrize("lvl", [5, 6])
+def test_packed_one_warp_shapes(lvl):
+    """The packed one-warp shapes (32 lanes x 16 / 20..32 slots) as first level
+    (latency shape) and with forced hand-overs, against the int32 ones and the
+    oracle."""
+    b = _mixed_pairs(500 + lvl, n=200, maxlen=600)
+    for X in (3, 30, 120, 600):
+        ref = oracle_run(b, X)
+        for ho in (0, 6):
+            res = []
+            for nopack in (False, True):
+                db = logan.to_device(b, logan.LOGAN_SEQ_2BIT)
+                out, cells = logan.xdrop_batch(db, 1, -1, -1, X, first_level=lvl, latency_first=True, handover=ho,
+                                               nopack=nopack)
+                torch.cuda.synchronize()
+                res.append((out.cpu().numpy(), cells.cpu().numpy().view(np.uint64)))
+            assert_same(*res[0], *ref, what=f"packed one-warp level {lvl} X={X} ho={ho}")
+            assert_same(*res[1], *ref, what=f"int32 one-warp level {lvl} X={X} ho={ho}")
