@@ -62,6 +62,9 @@ def parse_args(argv=None):
     ap.add_argument("--zdrop", type=int, default=None,
                     help="also stop extensions by Z-drop with this Z (DESIGN.md c-amb-19; off by default)")
     ap.add_argument("--fmt", choices=["2bit", "u8"], default="2bit")
+    ap.add_argument("--no-pack-u8", action="store_true",
+                    help="--fmt u8: run the u8 kernels (default: logan_pack_2bit re-encodes an A/C/G/T pool "
+                         "on the device every step, then the 2-bit path)")
     ap.add_argument("--first-level", type=int, default=0)
     ap.add_argument("--latency-first", action="store_true",
                     help="run the first level in its latency shape (one warp per task)")
@@ -390,10 +393,15 @@ def main(argv=None):
     stream = torch.cuda.current_stream(dev)
     first = args.first_level or None
 
+    pack_u8 = fmt == logan.LOGAN_SEQ_U8 and subst is None and not args.no_pack_u8
+    u8_packed = False
+    if pack_u8:  # does the pool take the packed path (all bytes A/C/G/T)?
+        u8_packed = int(logan.pack_2bit(db, stream)[1].item()) == 0
+
     def step(events=None, stats=None):
         logan.xdrop_batch(db, w.match, w.mismatch, w.gap, w.xdrop, workspace=ws, out=out, cells=cells,
                           stats=stats, first_level=first, stream=stream, timing_events=events,
-                          latency_first=args.latency_first, subst=subst, zdrop=args.zdrop)
+                          latency_first=args.latency_first, subst=subst, zdrop=args.zdrop, pack_u8=pack_u8)
 
     # one untimed run with device stats: per-level task and cell counts (deterministic)
     st = logan.new_stats(dev)
@@ -446,7 +454,7 @@ def main(argv=None):
         except RuntimeError:
             pass  # stage not launched in this configuration
     n_launch_stages = [stg for stg in stage_ms if 1 <= stg <= nst - 2]
-    launches_per_step = 3 + len(n_launch_stages) + 1  # expand, scan, scatter, levels, combine
+    launches_per_step = 3 + len(n_launch_stages) + 1 + int(pack_u8)  # [pack,] expand, scan, scatter, levels, combine
 
     # max over ranks (time), sum over ranks (cells)
     t = torch.tensor([total_ms], dtype=torch.float64, device=dev)
@@ -468,7 +476,7 @@ def main(argv=None):
     sm_max = clocks.get("sm_max_mhz") or 1965.0
     # the packed int16 kernels: the first window of a 2-bit pool at X <= 16000 (no
     # Z-drop; options.flags bit 4 off) and the band level
-    packed = (dom_level == 0 and fmt == logan.LOGAN_SEQ_2BIT and w.xdrop <= 16000 and args.zdrop is None
+    packed = (dom_level == 0 and (fmt == logan.LOGAN_SEQ_2BIT or u8_packed) and w.xdrop <= 16000 and args.zdrop is None
               and not protein) or dom_level == 6
     peak_tops, peak_how, peak32 = int_peak(sm_max, packed)
     achieved_tops = N_REF_OPS_PER_CELL * dom_cells / (dom_ms / 1e3) / 1e12
@@ -606,7 +614,7 @@ def main(argv=None):
                 "warmup": args.warmup, "ms_per_step": total_ms_max / args.steps,
                 "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "int32",
                 "data": "synthetic (datagen, seeded; DESIGN.md §5)",
-                "config": config_dict(w, n, args.fmt, args.first_level, world, share),
+                "config": config_dict(w, n, args.fmt + (" (re-encoded to 2-bit on the device each step, logan_pack_2bit)" if u8_packed else ""), args.first_level, world, share),
                 "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e, "parity": parity,
                 "gpu_launches": launches_per_step * args.steps, "clocks": clocks,
                 "cells_per_step": cells_all, "pairs_this_gpu": n_local,

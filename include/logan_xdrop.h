@@ -1,5 +1,5 @@
 /*
- * logan_xdrop.h — C ABI v1 of the B200-native batched X-drop seed-and-extend
+ * logan_xdrop.h — C ABI v3 of the B200-native batched X-drop seed-and-extend
  * library (LOGAN, Zeni et al., arXiv 2002.05200).
  *
  * Citations are PAPER.md line numbers ("P:<line>") with the section, equation
@@ -37,7 +37,7 @@
 extern "C" {
 #endif
 
-#define LOGAN_ABI_VERSION 2
+#define LOGAN_ABI_VERSION 3
 
 /* Linear scoring scheme (eq. P:85, read with signed addends, c-amb-2).
  * Requirements: 0 < match <= 127, -127 <= mismatch < 0, -127 <= gap < 0,
@@ -287,6 +287,46 @@ int logan_xdrop_batch_host_async(const uint8_t *seq_pool, int32_t seq_fmt, int64
                                  const logan_options_t *opt,
                                  logan_result_t *out, uint64_t *cells,
                                  void *device_arena, size_t arena_bytes, void *stream);
+
+/*
+ * logan_pack_2bit — device pre-pass: re-encode a LOGAN_SEQ_U8 pool whose bases
+ * are the bytes 'A' 'C' 'G' 'T' (0x41 0x43 0x47 0x54) as a LOGAN_SEQ_2BIT pool
+ * (A=0 C=1 G=2 T=3), asynchronously on `stream`. The sweep compares bases by
+ * equality only (Alg. 1, the match / mismatch score of a
+ * cell), so on such a pool logan_xdrop_batch gives bit-identical results for
+ * the u8 pool and the packed one; the packed one runs the packed int16 first
+ * window and moves a quarter of the bytes.
+ *
+ *  u8_pool     : device, pool_len bytes, 4-byte aligned, readable for 16
+ *                bytes past its last byte (as seq_pool above). Not modified.
+ *  q_off, q_len, t_off, t_len, n_pairs: the batch's read descriptors (device,
+ *                as for logan_xdrop_batch); only the bytes inside these reads
+ *                are checked (the sweep never compares any other byte). Pairs
+ *                whose reads lie outside [0, pool_len) are skipped (they get
+ *                the invalid result in either format).
+ *  pool_2bit   : device, >= logan_pack_2bit_bytes(pool_len) bytes, 4-byte
+ *                aligned, caller-owned: receives the (pool_len + 3) / 4 packed
+ *                bytes followed by zero padding up to that size (so it meets
+ *                seq_pool's 16-byte read-ahead rule).
+ *  n_other     : device uint64 (8-byte aligned): set to the number of bytes
+ *                outside {A, C, G, T} inside the reads. If it is non-zero the
+ *                packed pool is NOT equivalent (the codes of other bytes are
+ *                unspecified): keep the u8 pool. Read it after `stream` has
+ *                been synchronised.
+ * Errors: negative pool_len / n_pairs, NULL or misaligned pointers -> LOGAN_EINVAL; a
+ * pool_2bit buffer smaller than logan_pack_2bit_bytes -> LOGAN_ENOSPC, both
+ * synchronously with nothing launched; a launch failure -> LOGAN_ECUDA.
+ *
+ * logan_xdrop_batch_host (the synchronous host entry point) runs this pass
+ * itself for a LOGAN_SEQ_U8 pool without a substitution matrix and takes the
+ * packed pool when n_other == 0 (its arena includes the packed copy, see
+ * logan_host_arena_bytes); the asynchronous variant never does (the choice
+ * needs a host synchronisation).
+ */
+size_t logan_pack_2bit_bytes(int64_t pool_len);
+int logan_pack_2bit(const uint8_t *u8_pool, int64_t pool_len, const int64_t *q_off, const int32_t *q_len,
+                    const int64_t *t_off, const int32_t *t_len, int64_t n_pairs, uint8_t *pool_2bit,
+                    size_t pool_2bit_bytes, uint64_t *n_other, void *stream);
 
 /* Human-readable text for a status code (static storage). */
 const char *logan_strerror(int status);

@@ -15,12 +15,12 @@ LIB_PATH = os.path.join(PKG, "liblogan_xdrop.so")
 LOGAN_SEQ_U8 = 0
 LOGAN_SEQ_2BIT = 1
 LOGAN_OK, LOGAN_EINVAL, LOGAN_ECUDA, LOGAN_ENOSPC = 0, 1, 2, 3
-ABI_VERSION = 2  # LOGAN_ABI_VERSION this binding marshals for
+ABI_VERSION = 3  # LOGAN_ABI_VERSION this binding marshals for
 
 #: every symbol include/logan_xdrop.h declares
 EXPORTS = ("logan_workspace_bytes", "logan_xdrop_batch", "logan_host_arena_bytes",
            "logan_xdrop_batch_host", "logan_xdrop_batch_host_async", "logan_strerror",
-           "logan_abi_version", "logan_level_width")
+           "logan_abi_version", "logan_level_width", "logan_pack_2bit_bytes", "logan_pack_2bit")
 
 
 class Scoring(ctypes.Structure):
@@ -88,6 +88,10 @@ def load(path: str | None = None) -> ctypes.CDLL:
     lib.logan_abi_version.restype = ctypes.c_int
     lib.logan_level_width.argtypes = [i32, i32, i64, i32]
     lib.logan_level_width.restype = ctypes.c_int
+    lib.logan_pack_2bit_bytes.argtypes = [i64]
+    lib.logan_pack_2bit_bytes.restype = sz
+    lib.logan_pack_2bit.argtypes = [vp, i64, vp, vp, vp, vp, i64, vp, sz, vp, vp]
+    lib.logan_pack_2bit.restype = ctypes.c_int
     if lib.logan_abi_version() != ABI_VERSION:
         raise LoganError(f"{path}: ABI version {lib.logan_abi_version()}, binding expects {ABI_VERSION} "
                          "(rebuild with `python -m paper_2002_05200_b200.build`)")

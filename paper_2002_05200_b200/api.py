@@ -120,16 +120,26 @@ def xdrop_batch(db: DeviceBatch, match: int, mismatch: int, gap: int, xdrop: int
                 first_level: int | None = None, stream=None, timing_events=None,
                 latency_first: bool = False, handover: int = 0, first_slots: int = 0,
                 poison: bool = False, subst=None, zdrop: int | None = None, throughput_first: bool = False,
-                nopack: bool = False, compat: bool = False):
+                nopack: bool = False, compat: bool = False, pack_u8: bool = False):
     """Run the whole hot path on ``db``'s device, asynchronously on ``stream``
     (default: torch's current stream).  Returns ``(out int32[n,5], cells int64[n])``
-    device tensors (cells holds uint64 bit patterns)."""
+    device tensors (cells holds uint64 bit patterns).
+
+    ``pack_u8=True`` with a ``LOGAN_SEQ_U8`` pool (no ``subst``): re-encode the pool
+    as 2-bit on the device first (``logan_pack_2bit``) and run on that copy if every
+    base is A/C/G/T -- identical results; this costs one synchronisation of
+    ``stream`` (reading the count of other bytes)."""
     torch = _require_cuda()
     lib = _lib.load()
     n = db.n_pairs
     dev = db.q_len.device
     if stream is None:
         stream = torch.cuda.current_stream(dev)
+    if pack_u8 and db.fmt == _lib.LOGAN_SEQ_U8 and subst is None and n > 0:
+        packed, other = pack_2bit(db, stream)
+        stream.synchronize()
+        if int(other.item()) == 0:
+            db = packed
     # the library launches on the current device: make it db's (multi-GPU callers)
     with torch.cuda.device(dev):
         if out is None:
@@ -155,6 +165,30 @@ def xdrop_batch(db: DeviceBatch, match: int, mismatch: int, gap: int, xdrop: int
             workspace.ptr(), workspace.nbytes, stream.cuda_stream)
     _lib.check(st)
     return out, cells
+
+
+def pack_2bit(db: DeviceBatch, stream=None):
+    """``logan_pack_2bit``: a 2-bit copy of ``db``'s u8 pool (same descriptors) and a
+    device int64 tensor with the number of bytes outside A/C/G/T inside ``db``'s reads
+    (the copy is equivalent only if it is 0), both on ``stream``; no synchronisation."""
+    torch = _require_cuda()
+    lib = _lib.load()
+    if db.fmt != _lib.LOGAN_SEQ_U8:
+        raise ValueError("pack_2bit needs a LOGAN_SEQ_U8 pool")
+    dev = db.pool.device
+    if stream is None:
+        stream = torch.cuda.current_stream(dev)
+    nb = int(lib.logan_pack_2bit_bytes(db.pool_len))
+    with torch.cuda.device(dev):
+        pool = torch.empty(nb, dtype=torch.uint8, device=dev)
+        other = torch.empty(1, dtype=torch.int64, device=dev)
+        for t in (pool, other):
+            t.record_stream(stream)
+        _lib.check(lib.logan_pack_2bit(db.pool.data_ptr(), db.pool_len, db.q_off.data_ptr(), db.q_len.data_ptr(),
+                                       db.t_off.data_ptr(), db.t_len.data_ptr(), db.n_pairs, pool.data_ptr(), nb,
+                                       other.data_ptr(), stream.cuda_stream))
+    return DeviceBatch(pool, _lib.LOGAN_SEQ_2BIT, db.pool_len, db.q_off, db.q_len, db.t_off, db.t_len,
+                       db.q_seed, db.t_seed, db.k, db.max_ext_len), other
 
 
 def new_stats(device=None):

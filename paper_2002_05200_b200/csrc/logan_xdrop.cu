@@ -150,6 +150,7 @@ size_t logan_host_arena_bytes(int64_t n_pairs, int64_t pool_len, int32_t seq_fmt
     o += 4 * align256(sizeof(int32_t) * (size_t)n_pairs);
     o += align256(sizeof(logan_result_t) * (size_t)n_pairs);
     o += align256(sizeof(uint64_t) * (size_t)n_pairs);
+    if (seq_fmt == LOGAN_SEQ_U8) o += align256(logan_pack_2bit_bytes(pool_len)) + 256;  // packed copy + n_other
     o += logan_workspace_bytes(n_pairs, max_ext_len);
     return o;
 }
@@ -213,6 +214,12 @@ static int host_batch(const uint8_t *seq_pool, int32_t seq_fmt, int64_t pool_len
     int32_t *d_ts = (int32_t *)(a + o);   o += align256(sizeof(int32_t) * (size_t)n_pairs);
     logan_result_t *d_out = (logan_result_t *)(a + o); o += align256(sizeof(logan_result_t) * (size_t)n_pairs);
     uint64_t *d_cells = (uint64_t *)(a + o); o += align256(sizeof(uint64_t) * (size_t)n_pairs);
+    uint8_t *d_pack = nullptr;
+    uint64_t *d_other = nullptr;
+    if (seq_fmt == LOGAN_SEQ_U8) {
+        d_pack = a + o;                 o += align256(logan_pack_2bit_bytes(pool_len));
+        d_other = (uint64_t *)(a + o);  o += 256;
+    }
     if (o > arena_bytes) return LOGAN_ENOSPC;
     cudaStream_t s = (cudaStream_t)stream;
     const size_t n8 = sizeof(int64_t) * (size_t)n_pairs, n4 = sizeof(int32_t) * (size_t)n_pairs;
@@ -226,7 +233,21 @@ static int host_batch(const uint8_t *seq_pool, int32_t seq_fmt, int64_t pool_len
         cudaMemcpyAsync(d_ts, t_seed, n4, cudaMemcpyHostToDevice, s) != cudaSuccess)
         return LOGAN_ECUDA;
     if (o + logan_workspace_bytes(n_pairs, max_ext) > arena_bytes) return LOGAN_ENOSPC;
-    st = logan_xdrop_batch(d_pool, seq_fmt, pool_len, d_qoff, d_qlen, d_toff, d_tlen, d_qs, d_ts, n_pairs, max_ext,
+    // the synchronous call re-encodes a u8 pool of A/C/G/T as 2-bit (logan_pack_2bit):
+    // identical results, the packed first window; the choice reads n_other (one sync)
+    const uint8_t *run_pool = d_pool;
+    int32_t run_fmt = seq_fmt;
+    if (sync && seq_fmt == LOGAN_SEQ_U8 && !(opt && opt->subst)) {
+        uint64_t other = 1;
+        st = logan_pack_2bit(d_pool, pool_len, d_qoff, d_qlen, d_toff, d_tlen, n_pairs, d_pack,
+                             logan_pack_2bit_bytes(pool_len), d_other, stream);
+        if (st != LOGAN_OK) return st;
+        if (cudaMemcpyAsync(&other, d_other, sizeof other, cudaMemcpyDeviceToHost, s) != cudaSuccess ||
+            cudaStreamSynchronize(s) != cudaSuccess)
+            return LOGAN_ECUDA;
+        if (other == 0) { run_pool = d_pack; run_fmt = LOGAN_SEQ_2BIT; }
+    }
+    st = logan_xdrop_batch(run_pool, run_fmt, pool_len, d_qoff, d_qlen, d_toff, d_tlen, d_qs, d_ts, n_pairs, max_ext,
                            k, sc, opt, d_out, d_cells, nullptr, a + o, arena_bytes - o, stream);
     if (st != LOGAN_OK) return st;
     if (cudaMemcpyAsync(out, d_out, sizeof(logan_result_t) * (size_t)n_pairs, cudaMemcpyDeviceToHost, s) !=

@@ -53,7 +53,7 @@ def test_library_is_sm100a(lib):
 
 
 def test_host_side_checks_without_gpu(lib):
-    assert lib.logan_abi_version() == 2
+    assert lib.logan_abi_version() == 3
     # window widths by level (diagnostics; results never depend on them)
     assert lib.logan_level_width(1, 20, 2500, 0) == 28 and lib.logan_level_width(1, 20, 10000, 0) == 32
     assert lib.logan_level_width(1, 20, 7700, 0) == 28 and lib.logan_level_width(1, 18, 7700, 0) == 28
@@ -131,3 +131,26 @@ def test_product_path_does_not_import_oracle():
             text = open(path).read()
             assert "import oracle" not in text and "from oracle" not in text, path
             assert "xdrop_oracle" not in text, path
+
+
+def test_pack_2bit_host_checks_without_gpu(lib):
+    # size: ceil(pool_len / 16) packed words plus 16 bytes of zero padding
+    assert [lib.logan_pack_2bit_bytes(n) for n in (0, 1, 16, 17, 1000)] == [16, 20, 20, 24, 268]
+    assert lib.logan_pack_2bit_bytes(-1) == 0
+    fake = 1 << 20  # never dereferenced: every check below returns before any CUDA call
+    d = (fake, fake, fake, fake)  # read descriptors
+
+    def pk(u8, n, desc, npairs, out, nb, other):
+        return lib.logan_pack_2bit(u8, n, *desc, npairs, out, nb, other, None)
+    assert pk(fake, -1, d, 1, fake, 64, fake) == _lib.LOGAN_EINVAL
+    assert pk(fake, 100, d, -1, fake, 64, fake) == _lib.LOGAN_EINVAL
+    assert pk(fake, 100, d, 1, fake, 64, None) == _lib.LOGAN_EINVAL
+    assert pk(fake, 100, d, 1, fake, 64, fake + 4) == _lib.LOGAN_EINVAL  # n_other misaligned
+    assert pk(None, 100, d, 1, fake, 64, fake) == _lib.LOGAN_EINVAL
+    assert pk(fake + 2, 100, d, 1, fake, 64, fake) == _lib.LOGAN_EINVAL
+    assert pk(fake, 100, (fake, None, fake, fake), 1, fake, 64, fake) == _lib.LOGAN_EINVAL
+    assert pk(fake, 100, d, 1, fake, 39, fake) == _lib.LOGAN_ENOSPC
+    # the host arena of a u8 pool includes the packed copy (the synchronous entry packs)
+    a8 = lib.logan_host_arena_bytes(100, 4000, _lib.LOGAN_SEQ_U8, 100)
+    a2 = lib.logan_host_arena_bytes(100, 4000, _lib.LOGAN_SEQ_2BIT, 100)
+    assert a8 >= a2 + 4000 - 1000 + lib.logan_pack_2bit_bytes(4000)

@@ -1,4 +1,9 @@
-timeout 1200 python -m pytest tests -m gpu -x -q -rf > gpurun_out/pytest_pk4.log 2>&1; echo "pytest rc=$?" >> gpurun_out/pytest_pk4.log; tail -3 gpurun_out/pytest_pk4.log
-for a in "--config 3" "--config 2" "--config 3 --share 0/8"; do
-  bash tools/ab_bench.sh "$a --steps 10 --warmup 3 --parity-seconds 0.5" cur=paper_2002_05200_b200/liblogan_xdrop.so v7=paper_2002_05200_b200/variants/liblogan_v7.so
+timeout 900 python -m pytest tests/test_gpu_pack.py tests/test_gpu_parity.py -x -q -k "pack or host" > gpurun_out/pt_pack.log 2>&1; tail -3 gpurun_out/pt_pack.log
+for a in "--fmt u8" "--fmt u8 --no-pack-u8" "--config 2 --fmt u8" "--config 2 --fmt u8 --no-pack-u8"; do
+  timeout 600 python bench.py $a --no-cpu-baseline --steps 10 2>/dev/null | python -c "
+import json,sys
+for l in sys.stdin:
+    if l.startswith('{'):
+        d=json.loads(l); print('$a', round(d['value'],1), round(d['ms_per_step'],3), d['gpu_launches'], d['e2e']['value'] if d.get('e2e') else None, d['parity']['mismatches'], d['config']['fmt'])
+"
 done
