@@ -254,54 +254,47 @@ struct Window16 {
         for (int q = 0; q < H; ++q) C[q] = raise ? arr[q] : C[q];
     }
 
-    // live slot mask of a killed array in the z layout (nibble j = slots 2j, 2j+1,
-    // 2j+H, 2j+1+H), 1 = dead
-    __device__ __forceinline__ static uint32_t dead_z(const uint32_t (&a)[H]) {
+    // Dead-slot mask of a killed array in "pair order": one PRMT takes the sign
+    // bytes of word j and word j + H/2 (slots j, j + H/2, j + H, j + 3H/2, each
+    // replicated to a whole byte) and one LOP3 keeps bit j of every byte, so bit
+    // 8b + j is slot (H/2) b + j. The bit order is monotone in the slot order: the
+    // first / last live slot are one FLO away (two ALU instructions per word pair;
+    // the earlier nibble layout took four plus a branchy decode).
+    static constexpr int HH = H / 2;
+    static constexpr uint32_t USED = 0x01010101u * ((1u << HH) - 1u);  // bits that hold a slot
+    __device__ __forceinline__ static uint32_t dead_m(const uint32_t (&a)[H]) {
         uint32_t z = 0;
 #pragma unroll
-        for (int j = H / 2 - 1; j >= 0; --j) {
-            const uint32_t g = prmt_s(a[2 * j], a[2 * j + 1], 0xFBD9u);  // sign bytes: 2j lo, 2j+1 lo, 2j hi, 2j+1 hi
-            uint32_t m;
-            asm("mad.lo.u32 %0, %1, %2, 0;" : "=r"(m) : "r"(g & 0x80402010u), "r"(0x01010101u));
-            z = __funnelshift_l(m, z, 4);  // (z << 4) | (m >> 28)
+        for (int j = 0; j < HH; ++j) {
+            const uint32_t g = prmt_s(a[j], a[j + HH], 0xFBD9u);  // sign bytes: j lo, j+HH lo, j hi, j+HH hi
+            z |= g & (0x01010101u << j);
         }
         return z;
     }
-    // 2-bit groups of a 16-bit value to 4-bit spacing: bit 2g + t -> 4g + t
-    __device__ __forceinline__ static uint32_t spread2(uint32_t x) {
-        x = (x | (x << 8)) & 0x00FF00FFu;
-        x = (x | (x << 4)) & 0x0F0F0F0Fu;
-        return (x | (x << 2)) & 0x33333333u;
+    __device__ __forceinline__ static int32_t bit_slot(int32_t b) {
+        return HH == 8 ? b : HH * (b >> 3) + (b & 7);
     }
-    // z-layout bit of slot s
-    __device__ __forceinline__ static int zbit(int s) {
-        return s < H ? 4 * (s >> 1) + (s & 1) : 4 * ((s - H) >> 1) + 2 + ((s - H) & 1);
+    __device__ __forceinline__ static int32_t slot_bit(int32_t s) {
+        return HH == 8 ? s : 8 * (s / HH) + s % HH;
     }
 
     // live extremes of the killed antidiagonal e-1 (parity Qp) in array a:
     // sF / sL[Qp] (validity-masked: cells past the matrix do not count)
     template <int Qp>
     __device__ __forceinline__ void extremes(int32_t e, const uint32_t (&a)[H]) {
-        const uint32_t z = dead_z(a);
+        const uint32_t z = dead_m(a);
         const int32_t chq = e >> 1, fhq = (e - 1) >> 1;  // ceil((e-1)/2), floor((e-1)/2)
         const int32_t vlo = fhq - st.n, vhi = st.m - chq;
         const int32_t base = st.S0 + gl * R;
-        uint32_t vmask = 0xffffffffu;
-        if (vlo > base || vhi < base + R - 1) {  // near the matrix edges
-            // valid slots [rlo, rhi] as a slot-order mask, then spread to the z
-            // layout (bit s -> 4(s>>1) + (s&1) for s < H, 4((s-H)>>1) + 2 + ((s-H)&1))
+        uint32_t vmask = USED;
+        if (vlo > base || vhi < base + R - 1) {  // near the matrix edges: valid slots [rlo, rhi]
             const int32_t rlo = max(vlo - base, 0), rhi = min(vhi - base, R - 1);
-            const uint32_t m = (rlo <= rhi) ? ((0xffffffffu >> (31 - rhi)) & ~((1u << rlo) - 1u)) : 0u;
-            vmask = spread2(m & ((1u << H) - 1u)) | (spread2(m >> H) << 2);
+            const int32_t blo = slot_bit(rlo), bhi = slot_bit(rhi);
+            vmask = (rlo <= rhi) ? ((0xffffffffu >> (31 - bhi)) & ~((1u << blo) - 1u) & USED) : 0u;
         }
-        const uint32_t live = ~z & vmask & (H == 16 ? 0xffffffffu : ((1u << (2 * H)) - 1u));
-        const uint32_t llo = live & 0x33333333u, lhi = live & 0xCCCCCCCCu;
+        const uint32_t live = ~z & vmask;
         bool h = live != 0;
-        int32_t f, l;
-        if (llo) { const int p = __ffs(llo) - 1; f = (p >> 1) + (p & 1); }
-        else { const int p = __ffs(lhi) - 1; f = H + ((p - 2) >> 1) + (p & 1); }
-        if (lhi) { const int p = 31 - __clz(lhi); l = H + ((p - 2) >> 1) + (p & 1); }
-        else { const int p = 31 - __clz(llo); l = (p >> 1) + (p & 1); }
+        int32_t f = bit_slot(__ffs(live) - 1), l = bit_slot(31 - __clz(live));
         if (G > 1) {  // group extremes (sentinels for lanes without a live slot)
             f = grp_min<G>(h ? gl * R + f : INT32_MAX, gmask);
             l = grp_max<G>(h ? gl * R + l : INT32_MIN, gmask);
