@@ -66,6 +66,8 @@ def parse_args(argv=None):
                     help="--fmt u8: run the u8 kernels (default: logan_pack_2bit re-encodes an A/C/G/T pool "
                          "on the device every step, then the 2-bit path)")
     ap.add_argument("--first-level", type=int, default=0)
+    ap.add_argument("--first-slots", type=int, default=0,
+                    help="tuning knob: force the first window's slots (16/20/24/28/32; 0 = automatic)")
     ap.add_argument("--latency-first", action="store_true",
                     help="run the first level in its latency shape (one warp per task)")
     ap.add_argument("--share", default=None,
@@ -401,7 +403,8 @@ def main(argv=None):
     def step(events=None, stats=None):
         logan.xdrop_batch(db, w.match, w.mismatch, w.gap, w.xdrop, workspace=ws, out=out, cells=cells,
                           stats=stats, first_level=first, stream=stream, timing_events=events,
-                          latency_first=args.latency_first, subst=subst, zdrop=args.zdrop, pack_u8=pack_u8)
+                          latency_first=args.latency_first, subst=subst, zdrop=args.zdrop, pack_u8=pack_u8,
+                          first_slots=args.first_slots)
 
     # one untimed run with device stats: per-level task and cell counts (deterministic)
     st = logan.new_stats(dev)

@@ -218,11 +218,14 @@ static __global__ void k_combine(const Params P, const TaskRes *tres, logan_resu
 // kernel into 128 registers (4 blocks per SM with LOGAN_PK_MINB 4), but measured
 // slower (C3 1309-1323 vs 1345 GCUPS, C2 1231 vs 1275: half the helper capacity
 // leaves a level-2 tail, and 16 warps per SM do not raise the ALU-bound rate)
+#ifndef LOGAN_L1_G2_WARPS  // level 1 below this many one-lane warps per SM: two lanes per task
+#define LOGAN_L1_G2_WARPS 0
+#endif
 #ifndef LOGAN_PK_HSHAPE
 #define LOGAN_PK_HSHAPE LOGAN_HSHAPE(64)
 #endif
 
-template <int G, int R, int FMT, int HG, int HR, bool PK = false>
+template <int G, int R, int FMT, int HG, int HR, int PK = 0>
 static cudaError_t launch_win(const Params &P, const LevelIO &io_in, const LevelIO &hio, int sms, cudaStream_t s) {
     constexpr int S1 = Window<G, R, FMT>::SB_STRIDE;
     constexpr int S2 = HR > 0 ? Window<(HG > 0 ? HG : 32), (HR > 0 ? HR : 1), FMT>::SB_STRIDE : 0;
@@ -246,26 +249,40 @@ static cudaError_t launch_win(const Params &P, const LevelIO &io_in, const Level
     return cudaGetLastError();
 }
 
+// the packed first window (2-bit pools, X <= 16000); PK 2 = match - mismatch = 2
+template <int FMT, int PK>
+static cudaError_t launch_first_pk(int w0, bool helpers, bool g2, const Params &P, const LevelIO &io,
+                                   const LevelIO &hio, int sms, cudaStream_t s) {
+    // few tasks: the 32-slot window on two lanes per task (2 x 16 slots)
+    if (g2 && w0 == 32)
+        return helpers ? launch_win<2, 16, FMT, LOGAN_PK_HSHAPE, PK>(P, io, hio, sms, s)
+                       : launch_win<2, 16, FMT, 0, 0, PK>(P, io, hio, sms, s);
+    switch (w0) {
+        case 16: return helpers ? launch_win<1, 16, FMT, LOGAN_PK_HSHAPE, PK>(P, io, hio, sms, s)
+                                : launch_win<1, 16, FMT, 0, 0, PK>(P, io, hio, sms, s);
+        case 20: return helpers ? launch_win<1, 20, FMT, LOGAN_PK_HSHAPE, PK>(P, io, hio, sms, s)
+                                : launch_win<1, 20, FMT, 0, 0, PK>(P, io, hio, sms, s);
+        case 24: return helpers ? launch_win<1, 24, FMT, LOGAN_PK_HSHAPE, PK>(P, io, hio, sms, s)
+                                : launch_win<1, 24, FMT, 0, 0, PK>(P, io, hio, sms, s);
+        case 28: return helpers ? launch_win<1, 28, FMT, LOGAN_PK_HSHAPE, PK>(P, io, hio, sms, s)
+                                : launch_win<1, 28, FMT, 0, 0, PK>(P, io, hio, sms, s);
+        default: return helpers ? launch_win<1, 32, FMT, LOGAN_PK_HSHAPE, PK>(P, io, hio, sms, s)
+                                : launch_win<1, 32, FMT, 0, 0, PK>(P, io, hio, sms, s);
+    }
+}
+
 // wi = width index; latency = run the latency shape; helpers = first level with
 // in-kernel escalation helpers running the next width
 template <int FMT>
-static cudaError_t launch_first(int w0, bool helpers, const Params &P, const LevelIO &io, const LevelIO &hio,
-                                int sms, cudaStream_t s) {
+static cudaError_t launch_first(int w0, bool helpers, bool g2, const Params &P, const LevelIO &io,
+                                const LevelIO &hio, int sms, cudaStream_t s) {
     // 2-bit pools (no Z-drop) at X <= 16000: the packed int16 window (xdrop_window16.cuh)
     if constexpr (FMT == LOGAN_SEQ_2BIT) {
         if (P.xdrop <= PACK_XMAX && !P.nopack) {
-            switch (w0) {
-                case 16: return helpers ? launch_win<1, 16, FMT, LOGAN_PK_HSHAPE, true>(P, io, hio, sms, s)
-                                        : launch_win<1, 16, FMT, 0, 0, true>(P, io, hio, sms, s);
-                case 20: return helpers ? launch_win<1, 20, FMT, LOGAN_PK_HSHAPE, true>(P, io, hio, sms, s)
-                                        : launch_win<1, 20, FMT, 0, 0, true>(P, io, hio, sms, s);
-                case 24: return helpers ? launch_win<1, 24, FMT, LOGAN_PK_HSHAPE, true>(P, io, hio, sms, s)
-                                        : launch_win<1, 24, FMT, 0, 0, true>(P, io, hio, sms, s);
-                case 28: return helpers ? launch_win<1, 28, FMT, LOGAN_PK_HSHAPE, true>(P, io, hio, sms, s)
-                                        : launch_win<1, 28, FMT, 0, 0, true>(P, io, hio, sms, s);
-                default: return helpers ? launch_win<1, 32, FMT, LOGAN_PK_HSHAPE, true>(P, io, hio, sms, s)
-                                        : launch_win<1, 32, FMT, 0, 0, true>(P, io, hio, sms, s);
-            }
+#ifndef LOGAN_NO_M2
+            if (P.match - P.mismatch == 2) return launch_first_pk<FMT, 2>(w0, helpers, g2, P, io, hio, sms, s);
+#endif
+            return launch_first_pk<FMT, 1>(w0, helpers, g2, P, io, hio, sms, s);
         }
     }
     switch (w0) {
@@ -282,38 +299,56 @@ static cudaError_t launch_first(int w0, bool helpers, const Params &P, const Lev
     }
 }
 
+// the packed windows of levels 2-6 (2-bit pools, X <= 16000); PK 2 = match - mismatch = 2;
+// cudaErrorNotSupported = no packed shape (the int32 one runs)
+template <int FMT, int PK>
+static cudaError_t launch_width_pk(int wi, bool latency, bool helpers, const Params &P, const LevelIO &io,
+                                   const LevelIO &hio, int sms, cudaStream_t s, int w5) {
+    if (helpers && !latency) switch (wi) {
+        case 1: return launch_win<2, 32, FMT, LOGAN_HSHAPE(128), PK>(P, io, hio, sms, s);
+        case 2: return launch_win<4, 32, FMT, LOGAN_HSHAPE(256), PK>(P, io, hio, sms, s);
+        case 3: return launch_win<8, 32, FMT, LOGAN_HSHAPE(512), PK>(P, io, hio, sms, s);
+        case 4:
+            if (w5 == 640) return launch_win<16, 32, FMT, 32, 20, PK>(P, io, hio, sms, s);
+            if (w5 == 768) return launch_win<16, 32, FMT, 32, 24, PK>(P, io, hio, sms, s);
+            if (w5 == 896) return launch_win<16, 32, FMT, 32, 28, PK>(P, io, hio, sms, s);
+            return launch_win<16, 32, FMT, 32, 32, PK>(P, io, hio, sms, s);
+        default: break;
+    }
+    if (wi == 5) {
+        if (w5 == 640) return launch_win<32, 20, FMT, 0, 0, PK>(P, io, hio, sms, s);
+        if (w5 == 768) return launch_win<32, 24, FMT, 0, 0, PK>(P, io, hio, sms, s);
+        if (w5 == 896) return launch_win<32, 28, FMT, 0, 0, PK>(P, io, hio, sms, s);
+        return launch_win<32, 32, FMT, 0, 0, PK>(P, io, hio, sms, s);
+    }
+    switch (wi * 2 + (latency ? 1 : 0)) {
+        case 2: return launch_win<2, 32, FMT, 0, 0, PK>(P, io, hio, sms, s);
+        case 4: return launch_win<4, 32, FMT, 0, 0, PK>(P, io, hio, sms, s);
+        case 6: return launch_win<8, 32, FMT, 0, 0, PK>(P, io, hio, sms, s);
+        case 8: return launch_win<16, 32, FMT, 0, 0, PK>(P, io, hio, sms, s);
+        case 9: return launch_win<32, 16, FMT, 0, 0, PK>(P, io, hio, sms, s);
+        default: break;  // one-warp shapes with fewer than 16 slots per lane: int32
+    }
+    return cudaErrorNotSupported;
+}
+
 template <int FMT>
 static cudaError_t launch_width(int wi, bool latency, bool helpers, const Params &P, const LevelIO &io,
-                                const LevelIO &hio, int sms, cudaStream_t s, int w0, int w5) {
-    if (wi == 0 && !(latency && w0 == 32)) return launch_first<FMT>(w0, helpers && !latency, P, io, hio, sms, s);
+                                const LevelIO &hio, int sms, cudaStream_t s, int w0, int w5, bool g2 = false) {
+    if (wi == 0 && !(latency && w0 == 32)) return launch_first<FMT>(w0, helpers && !latency, g2, P, io, hio, sms, s);
     // 2-bit pools (no Z-drop) at X <= 16000: the packed int16 windows for the
     // throughput shapes (G x 32 slots) and the one-warp shapes with >= 16 slots per lane
     if constexpr (FMT == LOGAN_SEQ_2BIT) {
         if (P.xdrop <= PACK_XMAX && !P.nopack) {
-            if (helpers && !latency) switch (wi) {
-                case 1: return launch_win<2, 32, FMT, LOGAN_HSHAPE(128), true>(P, io, hio, sms, s);
-                case 2: return launch_win<4, 32, FMT, LOGAN_HSHAPE(256), true>(P, io, hio, sms, s);
-                case 3: return launch_win<8, 32, FMT, LOGAN_HSHAPE(512), true>(P, io, hio, sms, s);
-                case 4:
-                    if (w5 == 640) return launch_win<16, 32, FMT, 32, 20, true>(P, io, hio, sms, s);
-                    if (w5 == 768) return launch_win<16, 32, FMT, 32, 24, true>(P, io, hio, sms, s);
-                    if (w5 == 896) return launch_win<16, 32, FMT, 32, 28, true>(P, io, hio, sms, s);
-                    return launch_win<16, 32, FMT, 32, 32, true>(P, io, hio, sms, s);
-                default: break;
-            }
-            if (wi == 5) {
-                if (w5 == 640) return launch_win<32, 20, FMT, 0, 0, true>(P, io, hio, sms, s);
-                if (w5 == 768) return launch_win<32, 24, FMT, 0, 0, true>(P, io, hio, sms, s);
-                if (w5 == 896) return launch_win<32, 28, FMT, 0, 0, true>(P, io, hio, sms, s);
-                return launch_win<32, 32, FMT, 0, 0, true>(P, io, hio, sms, s);
-            }
-            switch (wi * 2 + (latency ? 1 : 0)) {
-                case 2: return launch_win<2, 32, FMT, 0, 0, true>(P, io, hio, sms, s);
-                case 4: return launch_win<4, 32, FMT, 0, 0, true>(P, io, hio, sms, s);
-                case 6: return launch_win<8, 32, FMT, 0, 0, true>(P, io, hio, sms, s);
-                case 8: return launch_win<16, 32, FMT, 0, 0, true>(P, io, hio, sms, s);
-                case 9: return launch_win<32, 16, FMT, 0, 0, true>(P, io, hio, sms, s);
-                default: break;  // one-warp shapes with fewer than 16 slots per lane: int32
+#ifndef LOGAN_NO_M2
+            if (P.match - P.mismatch == 2) {
+                const cudaError_t e = launch_width_pk<FMT, 2>(wi, latency, helpers, P, io, hio, sms, s, w5);
+                if (e != cudaErrorNotSupported) return e;
+            } else
+#endif
+            {
+                const cudaError_t e = launch_width_pk<FMT, 1>(wi, latency, helpers, P, io, hio, sms, s, w5);
+                if (e != cudaErrorNotSupported) return e;
             }
         }
     }
@@ -382,12 +417,14 @@ static int auto_top_width(int32_t xdrop) {
 // 617 GCUPS vs 20: 555; X = 8: 20 754 vs 16: 614 (2% of tasks overflow); X = 10:
 // 20 ~ 24 on 2.5-7.5 kb reads, 24 +10% on 10 kb reads; X = 12: 24 881 vs 20: 730;
 // X = 14, 16: 24 best; X = 18, 20: 28 best on 2.5-7.5 kb reads (C6 X = 20: 1168 vs
-// 32: 1109), 32 on 10 kb reads (profiles/r01_ab_first_slots_mid_x.txt).
+// 32: 1109), 32 on 10 kb reads (profiles/r01_ab_first_slots_mid_x.txt). Round 2,
+// packed window (profiles/r02/ab_slots_v10.txt, ab_slots_v12.txt): X = 10 takes 24
+// slots (C3 998 vs 32: 948; C2 920 vs 20: 870), X in (10, 20] 32 slots on every read
+// length (C3 X = 16: 1370 vs 28: 1255, 24: 766; C2 X = 20: 1391 vs 28: 1334).
 static int auto_first_slots(int32_t xdrop, int64_t max_ext) {
+    (void)max_ext;
     if (xdrop <= 5) return 16;
-    if (xdrop <= 10) return max_ext > 9000 ? 24 : 20;
-    if (xdrop <= 16) return 24;
-    if (xdrop <= 20) return max_ext > 9000 ? 32 : 28;
+    if (xdrop <= 10) return 24;
     return 32;
 }
 
@@ -480,6 +517,11 @@ int run_batch(const Params &P, const logan_options_t *opt, bool wide_only, logan
     const bool few_tasks = (first > 0 && first < NWIDTH && groups_needed < (int64_t)sms * 8) ||
                            (first == 0 && w0 == 32 && groups_needed < (int64_t)sms * 2);
     const bool latency_first = (opt && (opt->flags & 1)) || (few_tasks && !(opt && (opt->flags & 8)));
+    // Level 1 with few tasks but more than the latency shape's limit: the packed
+    // 32-slot window on two lanes per task (twice the warps, half the dependent
+    // chain per antidiagonal)
+    const bool l1_g2 = first == 0 && w0 == 32 && !latency_first &&
+                       groups_needed < (int64_t)sms * LOGAN_L1_G2_WARPS;
     // the first level's launch, recorded in stats (diagnostics: which kernel ran)
     Params Pe = P;
     if (stats) {
@@ -525,7 +567,7 @@ int run_batch(const Params &P, const logan_options_t *opt, bool wide_only, logan
                     if (cudaMemsetAsync(lists[out_sel], 0xff, sizeof(uint32_t) * (size_t)L.ntask, s) != cudaSuccess)
                         return LOGAN_ECUDA;
                 }
-                e = launch_width<FMT>(lv, latency_first, helpers, P, io, hio, sms, s, w0, w5);
+                e = launch_width<FMT>(lv, latency_first, helpers, P, io, hio, sms, s, w0, w5, l1_g2);
             } else {
                 io.max_count = latency_below;
                 e = launch_width<FMT>(lv, true, false, P, io, io, sms, s, w0, w5);

@@ -117,6 +117,11 @@ int logan_xdrop_batch(const uint8_t *seq_pool, int32_t seq_fmt, int64_t pool_len
     P.alphabet = (opt && opt->subst) ? opt->alphabet : 0;
     P.stats = stats;
     P.info[0] = P.info[1] = P.info[2] = P.info[3] = 0;
+    auto pk2h = [](int32_t v) { return ((uint32_t)v & 0xffffu) * 0x10001u; };
+    P.gap2 = pk2h(sc.gap);
+    P.fg2 = pk2h(-16384 - sc.gap);  // DEAD16 - gap (xdrop_window16.cuh)
+    P.match2 = pk2h(sc.match);
+    P.mis2 = pk2h(sc.mismatch);
     // X' = min(X, 4 max_ext w): no cell of any extension of the batch can drop
     // at or above that bound, so the results equal those at X (header, scoring)
     const int64_t w = P.subst ? 127 : std::max<int64_t>(sc.match, std::max<int64_t>(-sc.mismatch, -sc.gap));

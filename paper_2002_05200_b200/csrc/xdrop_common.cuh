@@ -37,6 +37,9 @@ struct Params {
     int32_t alphabet;
     int32_t zdrop;        // Z-drop threshold (c-amb-19), < 0 = off
     uint32_t info[4];     // the first level's launch (k_expand copies it into stats)
+    // packed int16-pair constants of the packed windows (xdrop_window16.cuh), set
+    // on the host: both halves = gap, DEAD16 - gap, match, mismatch (mod 2^16)
+    uint32_t gap2, fg2, match2, mis2;
 };
 
 // Result of one extension task (L or R of one pair), 24 bytes.

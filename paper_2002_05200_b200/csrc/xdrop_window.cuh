@@ -832,14 +832,15 @@ __device__ __forceinline__ void run_group(Win &w, const Params &P, const LevelIO
 // overflowing tasks then finish while this level is still running instead of
 // forming a serial tail after it. What the helpers do not take, the next
 // level's own launch does (it shares their cursor).
-template <int G, int R, int FMT> struct Window16;  // xdrop_window16.cuh
+template <int G, int R, int FMT, bool M2> struct Window16;  // xdrop_window16.cuh
 
-// PK: the producers run the packed int16 window (Window16)
-template <int G, int R, int FMT, int HG, int HR, bool PK = false>
+// PK: 0 = the producers run the int32 window (Window), 1 = the packed int16
+// window (Window16), 2 = the packed window specialised for match - mismatch = 2
+template <int G, int R, int FMT, int HG, int HR, int PK = 0>
 __global__ void __launch_bounds__(128, (PK ? (G == 1 ? LOGAN_PK_MINB : 3)
                                            : (G == 1 ? ((fmt_z(FMT) || fmt_base(FMT) == FMT_U8S) ? 3 : LOGAN_L0_MINB) : 1)))
     k_window(const Params P, const LevelIO io, const LevelIO hio) {
-    using PW = typename std::conditional<PK, Window16<G, R, FMT>, Window<G, R, FMT>>::type;
+    using PW = typename std::conditional<(PK != 0), Window16<G, R, FMT, PK == 2>, Window<G, R, FMT>>::type;
     const uint32_t count = *io.count;
     const uint32_t taken = *io.cursor;  // entries already taken (by in-kernel helpers)
     const uint32_t remaining = count - (taken < count ? taken : count);

@@ -47,11 +47,24 @@ __device__ __forceinline__ uint32_t prmt_s(uint32_t a, uint32_t b, uint32_t sel)
     return r;
 }
 
+// v's low half in both halves (one PRMT)
+#ifdef LOGAN_PK2_MUL
 __device__ __forceinline__ uint32_t pk2(int32_t v) { return ((uint32_t)v & 0xffffu) * 0x10001u; }
+#else
+__device__ __forceinline__ uint32_t pk2(int32_t v) { return __byte_perm((uint32_t)v, 0u, 0x1010u); }
+#endif
+__device__ __forceinline__ uint32_t vadd2(uint32_t a, uint32_t b) {
+    uint32_t r;
+    asm("add.s16x2 %0, %1, %2;" : "=r"(r) : "r"(a), "r"(b));
+    return r;
+}
 __device__ __forceinline__ int32_t lo16(uint32_t w) { return (int32_t)(int16_t)(w & 0xffffu); }
 __device__ __forceinline__ int32_t hi16(uint32_t w) { return ((int32_t)w) >> 16; }
 
-template <int G, int R, int FMT>
+// M2: match - mismatch = 2 (the paper's +1/-1 scoring): the substitution is
+// diag + (match - dl) + 2 * mask (two FMA-pipe adds of the sign-replicated
+// mismatch mask) instead of a LOP3 select (ALU pipe, the bound)
+template <int G, int R, int FMT, bool M2>
 struct Window16 {
     static_assert(FMT == LOGAN_SEQ_2BIT, "packed window: 2-bit pools");
     static_assert(R % 4 == 0 && R >= 16 && R <= 32 && (G & (G - 1)) == 0 && G * R <= 1024, "packed window shape");
@@ -387,9 +400,16 @@ struct Window16 {
         }
 
         // (f) raw cells of e (relative to T_{e-1}), two slots per instruction
+#ifdef LOGAN_OLD_CONST
         const uint32_t gap2 = pk2(P.gap);
         const uint32_t fg2 = pk2(DEAD16 - P.gap);
         const uint32_t sma2 = pk2(P.match - dl), smi2 = pk2(P.mismatch - dl);
+#else
+        const uint32_t gap2 = P.gap2;
+        const uint32_t fg2 = P.fg2;
+        // (match - dl, mismatch - dl in both halves: two FMA-pipe adds of the packed constants)
+        const uint32_t sma2 = vadd2(P.match2, ndl2), smi2 = vadd2(P.mis2, ndl2);
+#endif
         // (FMA-pipe IMADs with an opaque run-time 1 / 16: the ALU pipe is the bound)
         const uint32_t one = (uint32_t)P.one, sixteen = (uint32_t)P.one << 4;
         uint32_t Y[NW], Yl[NW];
@@ -415,7 +435,8 @@ struct Window16 {
             const uint32_t sel = (8u | b0) | ((8u | b0) << 4) | ((12u | b1) << 8) | ((12u | b1) << 12);
             const uint32_t mask2 = prmt_s(a, b, sel);
             uint32_t s2;
-            asm("lop3.b32 %0, %1, %2, %3, 0xCA;" : "=r"(s2) : "r"(mask2), "r"(smi2), "r"(sma2));
+            if (M2) s2 = vadd2(mask2, mask2);  // -2 or 0 per half; sma2 added below
+            else asm("lop3.b32 %0, %1, %2, %3, 0xCA;" : "=r"(s2) : "r"(mask2), "r"(smi2), "r"(sma2));
             uint32_t up, left, diag;
             if (PAR == 1) {  // odd e: up = E[s+1], left = E[s], diag = O[s]
                 // seam: (slot H of this lane, slot 0 of the next lane)
@@ -431,6 +452,7 @@ struct Window16 {
             const uint32_t t0 = __vimax3_s16x2(up, left, fg2);
             uint32_t dps;
             asm("add.s16x2 %0, %1, %2;" : "=r"(dps) : "r"(diag), "r"(s2));
+            if (M2) dps = vadd2(dps, sma2);
             const uint32_t u = __viaddmax_s16x2(t0, gap2, dps);
             if (PAR == 1) O[k] = u;
             else E[k] = u;

@@ -55,10 +55,10 @@ def test_library_is_sm100a(lib):
 def test_host_side_checks_without_gpu(lib):
     assert lib.logan_abi_version() == 3
     # window widths by level (diagnostics; results never depend on them)
-    assert lib.logan_level_width(1, 20, 2500, 0) == 28 and lib.logan_level_width(1, 20, 10000, 0) == 32
-    assert lib.logan_level_width(1, 20, 7700, 0) == 28 and lib.logan_level_width(1, 18, 7700, 0) == 28
-    assert lib.logan_level_width(1, 10, 2500, 0) == 20 and lib.logan_level_width(1, 20, 2500, 24) == 24
-    assert [lib.logan_level_width(1, x, 2500, 0) for x in (0, 5, 6, 10, 11, 12, 16)] == [16, 16, 20, 20, 24, 24, 24]
+    assert lib.logan_level_width(1, 20, 2500, 0) == 32 and lib.logan_level_width(1, 20, 10000, 0) == 32
+    assert lib.logan_level_width(1, 20, 7700, 0) == 32 and lib.logan_level_width(1, 18, 7700, 0) == 32
+    assert lib.logan_level_width(1, 10, 2500, 0) == 24 and lib.logan_level_width(1, 20, 2500, 24) == 24
+    assert [lib.logan_level_width(1, x, 2500, 0) for x in (0, 5, 6, 10, 11, 12, 16)] == [16, 16, 24, 24, 32, 32, 32]
     assert lib.logan_level_width(1, 10, 10000, 0) == 24 and lib.logan_level_width(1, 20, 2500, 16) == 16
     assert [lib.logan_level_width(lv, 50, 2500, 0) for lv in range(2, 6)] == [64, 128, 256, 512]
     assert [lib.logan_level_width(6, x, 2500, 0) for x in (50, 500, 600, 700, 1000)] == [1024, 640, 768, 896, 1024]

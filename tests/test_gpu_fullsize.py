@@ -35,7 +35,7 @@ CASES = {
     "c3_x100": (3, 100, 100_000, 3, 128),  # k_window<4,32,2bit,8,32>
     "c2_x150": (2, 150, 100_000, 4, 256),  # k_window<8,32,2bit,16,32>
     "c2_x300": (2, 300, 20_000, 5, 512),   # k_window<16,32,2bit,32,32>
-    "c2_x20": (2, 20, 100_000, 1, 28),     # k_window<1,28,2bit,2,32> (bench --config 2)
+    "c2_x20": (2, 20, 100_000, 1, 32),     # k_window<1,32,2bit,2,32> (bench --config 2)
     "c4": (4, 50, 100_000, 2, 64),         # BELLA-like: spurious pairs escalate to 512 / 1024 / CTA
     "c5": (5, 100, 20_000, 3, 128),        # 50-100 kb reads
 }

@@ -399,12 +399,13 @@ def test_first_window_widths(slots):
     with in-kernel helpers (forced: 300 pairs would pick the latency shape at 32
     slots) and in the automatic choice."""
     b = _mixed_pairs(300 + slots)
-    for X in (0, 5, 12, 20):
-        ref = oracle_run(b, X)
+    # +1/-1/-1 takes the match - mismatch = 2 build of the packed window, (2, -3, -2) the general one
+    for (ma, mi, g), X in itertools.product(((1, -1, -1), (2, -3, -2)), (0, 5, 12, 20)):
+        ref = oracle_run(b, X, ma, mi, g)
         for tp in (True, False):
             db = logan.to_device(b, logan.LOGAN_SEQ_2BIT)
             st = logan.new_stats()
-            out, cells = logan.xdrop_batch(db, 1, -1, -1, X, first_level=1, first_slots=slots, stats=st,
+            out, cells = logan.xdrop_batch(db, ma, mi, g, X, first_level=1, first_slots=slots, stats=st,
                                            throughput_first=tp)
             torch.cuda.synchronize()
             s = logan.stats_dict(st)
@@ -412,7 +413,7 @@ def test_first_window_widths(slots):
             if tp:
                 assert (s["first_shape"], s["first_helpers"]) == ("throughput", True), s
             assert_same(out.cpu().numpy(), cells.cpu().numpy().view(np.uint64), *ref,
-                        what=f"first window {slots} X={X} throughput_first={tp}")
+                        what=f"first window {slots} X={X} scoring={(ma, mi, g)} throughput_first={tp}")
 
 
 # --------------------------------------------------------------------------

@@ -23,11 +23,12 @@ constexpr int ITERS = 4096; // loop trips (each: NCH ops)
 constexpr int THREADS = 256;
 
 enum Op { VMAX3, VADDMAX, VMINU32, LOP3, IADD3, SHF, IMAD, VMAX3_S16X2, VADDMAX_S16X2, MIX_VMAX3_IMAD, VADD16X2, PRMT,
-          MIX_VADD16X2_VMAX3, MIX_PRMT_IMAD, NOPS };
+          MIX_VADD16X2_VMAX3, MIX_PRMT_IMAD, IMADHI, IMADSHL, VADDMIN_U16X2, MIX_2VMAX3_IMAD, NOPS };
 static const char *kName[NOPS] = {"VIMNMX3", "VIADDMNMX", "VIMNMX.U32", "LOP3", "IADD3", "SHF", "IMAD",
                                   "VIMNMX3.S16x2", "VIADDMNMX.S16x2", "VIMNMX3+IMAD (1:1)", "VIADD.16x2", "PRMT",
-                                  "VIADD.16x2+VIMNMX3 (1:1)", "PRMT+IMAD (1:1)"};
-static const int kLanesPerOp[NOPS] = {1, 1, 1, 1, 1, 1, 1, 2, 2, 1, 2, 1, 1, 1};
+                                  "VIADD.16x2+VIMNMX3 (1:1)", "PRMT+IMAD (1:1)", "IMAD.HI", "IMAD.SHL",
+                                  "VIADDMNMX.U16x2", "VIMNMX3+IMAD (2:1)"};
+static const int kLanesPerOp[NOPS] = {1, 1, 1, 1, 1, 1, 1, 2, 2, 1, 2, 1, 1, 1, 1, 1, 2, 1};
 
 template <int OP>
 __global__ void __launch_bounds__(THREADS) k_op(uint32_t seed, uint32_t *sink, unsigned long long *cyc) {
@@ -60,6 +61,13 @@ __global__ void __launch_bounds__(THREADS) k_op(uint32_t seed, uint32_t *sink, u
                 if (q & 1) asm volatile("mad.lo.u32 %0, %0, %1, %2;" : "+r"(a[q]) : "r"(b), "r"(c));
                 else a[q] = __byte_perm(a[q], b, 0x5432);
             }
+            if (OP == IMADHI) asm volatile("mad.hi.u32 %0, %0, %1, %2;" : "+r"(a[q]) : "r"(b), "r"(c));
+            if (OP == IMADSHL) asm volatile("mul.lo.u32 %0, %0, 16;" : "+r"(a[q]));
+            if (OP == VADDMIN_U16X2) a[q] = __viaddmin_u16x2(a[q], b, c);
+            if (OP == MIX_2VMAX3_IMAD) {
+                if (q % 3 == 2) asm volatile("mad.lo.u32 %0, %0, %1, %2;" : "+r"(a[q]) : "r"(b), "r"(c));
+                else a[q] = (uint32_t)__vimax3_s32((int)a[q], (int)b, (int)d);
+            }
             if (OP == MIX_VMAX3_IMAD) {
                 if (q & 1) asm volatile("mad.lo.u32 %0, %0, %1, %2;" : "+r"(a[q]) : "r"(b), "r"(c));
                 else a[q] = (uint32_t)__vimax3_s32((int)a[q], (int)b, (int)d);
@@ -75,7 +83,7 @@ __global__ void __launch_bounds__(THREADS) k_op(uint32_t seed, uint32_t *sink, u
 }
 
 // SASS instructions per chain step of each form
-static const int kInstPerStep[NOPS] = {1, 1, 1, 1, 1, 1, 1, 1, 1, 1, 1, 1, 1, 1};
+static const int kInstPerStep[NOPS] = {1, 1, 1, 1, 1, 1, 1, 1, 1, 1, 1, 1, 1, 1, 1, 1, 1, 1};
 
 template <int OP>
 static double run(int sms, int blocks_per_sm, uint32_t *sink, unsigned long long *cyc) {
@@ -120,6 +128,10 @@ int main() {
     r[PRMT] = run<PRMT>(sms, bps, sink, cyc);
     r[MIX_VADD16X2_VMAX3] = run<MIX_VADD16X2_VMAX3>(sms, bps, sink, cyc);
     r[MIX_PRMT_IMAD] = run<MIX_PRMT_IMAD>(sms, bps, sink, cyc);
+    r[IMADHI] = run<IMADHI>(sms, bps, sink, cyc);
+    r[IMADSHL] = run<IMADSHL>(sms, bps, sink, cyc);
+    r[VADDMIN_U16X2] = run<VADDMIN_U16X2>(sms, bps, sink, cyc);
+    r[MIX_2VMAX3_IMAD] = run<MIX_2VMAX3_IMAD>(sms, bps, sink, cyc);
     if (cudaGetLastError() != cudaSuccess) { fprintf(stderr, "CUDA error\n"); return 1; }
     printf("{\"gpu\": \"%s\", \"sms\": %d, \"clock_khz_attr\": %d, \"threads_per_sm\": %d, \"inst_per_clk_per_sm\": {",
            p.name, sms, clk, bps * THREADS);
