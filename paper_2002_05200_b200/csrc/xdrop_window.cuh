@@ -737,32 +737,35 @@ __device__ __forceinline__ uint32_t ld_relaxed(const uint32_t *p) {
     return v;
 }
 
+// Starts or resumes the next task of a group (false: none left). The hot loop
+// below always starts with an odd antidiagonal (a task resumed after an odd one
+// takes the even one here), so it has a single code path; `rc` returns the
+// outcome of that step (0 = go on). (A function, not a lambda: the inliner must
+// not outline it, or the window's register arrays would move to local memory.)
+template <class Win, class Fetch>
+__device__ __forceinline__ bool start_next(Win &w, const Params &P, const LevelIO &io, Fetch &fetch, int &rc) {
+    rc = 0;
+    uint32_t pos;
+    if (!fetch(pos)) return false;
+    const uint32_t task = io.list[pos];
+    const uint32_t rec = io.in_recs ? io.in_recs[pos] : NO_REC;
+    if (rec != NO_REC) w.resume(P, io.rec_in + (size_t)rec * io.rec_in_stride);
+    else w.init(P, task);
+    if (io.stats && w.gl == 0) {
+        atomicAdd((unsigned long long *)&io.stats->tasks_started[io.level], 1ull);
+        if (io.is_helper) atomicAdd((unsigned long long *)&io.stats->helper_tasks, 1ull);
+    }
+    if (w.st.d & 1) rc = w.template step<0>(P, false);
+    return true;
+}
+
 template <class Win, class Fetch>
 __device__ __forceinline__ void run_group(Win &w, const Params &P, const LevelIO &io, Fetch fetch) {
     constexpr int G = Win::GG;
     const int lane = threadIdx.x & 31;
     const int leader = lane - w.gl;
-    // start or resume the next task; the hot loop below always starts with an odd
-    // antidiagonal (a task resumed after an odd one takes the even one here), so
-    // it has a single code path. `rc` returns the outcome of that step (0 = go on).
-    auto next_task = [&](int &rc) -> bool {
-        rc = 0;
-        uint32_t pos;
-        if (!fetch(pos)) return false;
-        const uint32_t task = io.list[pos];
-        const uint32_t rec = io.in_recs ? io.in_recs[pos] : NO_REC;
-        if (rec != NO_REC) w.resume(P, io.rec_in + (size_t)rec * io.rec_in_stride);
-        else w.init(P, task);
-        if (io.stats && w.gl == 0) {
-            atomicAdd((unsigned long long *)&io.stats->tasks_started[io.level], 1ull);
-            if (io.is_helper) atomicAdd((unsigned long long *)&io.stats->helper_tasks, 1ull);
-        }
-        if (w.st.d & 1) rc = w.template step<0>(P, false);
-        return true;
-    };
-
     int rc = 0;
-    bool active = next_task(rc);
+    bool active = start_next(w, P, io, fetch, rc);
     int32_t since = 0;  // antidiagonals at this level (hand-over test knob)
     while (active) {
         // one iteration = the odd then the even antidiagonal
@@ -815,7 +818,7 @@ __device__ __forceinline__ void run_group(Win &w, const Params &P, const LevelIO
             }
             if (rc == 2) w.st.shifts = 0;
             since = 0;
-            active = next_task(rc);
+            active = start_next(w, P, io, fetch, rc);
         }
     }
 }
