@@ -864,9 +864,13 @@ __global__ void __launch_bounds__(128, (PK ? (G == 1 ? LOGAN_PK_MINB : 3)
     const bool helper = HR > 0 && (int)blockIdx.x >= (int)gridDim.x - io.helpers && (int)(threadIdx.x >> 5) == hwarp;
     if (HR > 0 && helper) {
         constexpr int HG_ = HG > 0 ? HG : 32, HR_ = HR > 0 ? HR : 1;
-        Window<HG_, HR_, FMT> w;
+        // packed producers get packed helpers (the same int16 window one width up):
+        // a task that overflows late in its life finishes at the packed rate
+        constexpr bool HPK = PK != 0 && HR_ >= 16 && HR_ % 4 == 0;
+        using HW = typename std::conditional<HPK, Window16<HG_, HR_, FMT, PK == 2>, Window<HG_, HR_, FMT>>::type;
+        HW w;
         w.tab = tab;
-        w.sbase = win_smem + threadIdx.x * Window<HG_, HR_, FMT>::SB_STRIDE;
+        w.sbase = win_smem + threadIdx.x * HW::SB_STRIDE;
         w.gl = lane % HG_;
         w.gmask = (HG_ == 32) ? 0xffffffffu : (((1u << HG_) - 1u) << (lane - w.gl));
         const int leader = lane - w.gl;
