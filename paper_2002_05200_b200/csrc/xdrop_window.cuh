@@ -68,7 +68,9 @@ constexpr int32_t KNONE = INT32_MIN;  // "no pending maximum" (below every raise
 #ifndef LOGAN_L0_MINB
 #define LOGAN_L0_MINB 1
 #endif
-// the same for the packed first window (Window16; see LOGAN_PK_HSHAPE)
+// the same for the packed first window (Window16; see LOGAN_PK_HSHAPE) with 28 or 32
+// slots; 24 slots and fewer take 4 blocks (128 registers, no spill): C3 X = 10 +3.5%,
+// while 4 blocks cost 32 slots 5% (profiles/r02/ab_minb4.txt)
 #ifndef LOGAN_PK_MINB
 #define LOGAN_PK_MINB 1
 #endif
@@ -840,7 +842,7 @@ template <int G, int R, int FMT, bool M2> struct Window16;  // xdrop_window16.cu
 // PK: 0 = the producers run the int32 window (Window), 1 = the packed int16
 // window (Window16), 2 = the packed window specialised for match - mismatch = 2
 template <int G, int R, int FMT, int HG, int HR, int PK = 0>
-__global__ void __launch_bounds__(128, (PK ? (G == 1 ? LOGAN_PK_MINB : 3)
+__global__ void __launch_bounds__(128, (PK ? (G == 1 ? (R <= 24 ? 4 : LOGAN_PK_MINB) : 3)
                                            : (G == 1 ? ((fmt_z(FMT) || fmt_base(FMT) == FMT_U8S) ? 3 : LOGAN_L0_MINB) : 1)))
     k_window(const Params P, const LevelIO io, const LevelIO hio) {
     using PW = typename std::conditional<(PK != 0), Window16<G, R, FMT, PK == 2>, Window<G, R, FMT>>::type;

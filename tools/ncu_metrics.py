@@ -54,12 +54,19 @@ def main():
     ap.add_argument("bench_json")
     ap.add_argument("--out", default=os.path.join(ROOT, "profiles", "ncu_metrics.json"))
     ap.add_argument("--tag", default="")
+    ap.add_argument("--int-rep", default=None,
+                    help="a second capture of the same launch with --metrics "
+                         "smsp__sass_thread_inst_executed_op_integer_pred_on.sum (not in --set full)")
     args = ap.parse_args()
     line = json.loads([ln for ln in open(args.bench_json) if ln.startswith("{")][-1])
     cfg = line["config"]
     level = line["levels"]["first"][0]
     cells = line["levels"]["cells_per_level"][level - 1]
     m = raw_metrics(args.rep)
+    if args.int_rep and os.path.exists(args.int_rep):
+        mi = raw_metrics(args.int_rep)
+        if "int_thread_inst" in mi:
+            m["int_thread_inst"] = mi["int_thread_inst"]
     dur = m["duration_ns"] * 1e-9
     entry = {
         "kernel": m["kernel"], "level": level, "cells_per_launch": cells,
