@@ -45,6 +45,7 @@ struct Layout {
 constexpr int WIDE_CTAS = 296;  // 2 per SM on B200
 constexpr int NCTR = 64;
 constexpr int CTR_OUT = 16, CTR_FILL = 32, CTR_DONE = 48;
+constexpr int CTR_BAND2_CURSOR = 10, CTR_BAND2_OUT = 25;  // the band level's second stage
 
 static size_t align256(size_t x) { return (x + 255) & ~(size_t)255; }
 
@@ -428,6 +429,18 @@ static int auto_first_slots(int32_t xdrop, int64_t max_ext) {
     return 32;
 }
 
+// one persistent launch of the band level in configuration C (xdrop_band.cuh)
+template <int FMT, class C>
+static cudaError_t launch_band(const Params &P, const LevelIO &io, int sms, cudaStream_t s) {
+    const int smem = (int)BandSmem<FMT, C>::BYTES;
+    cudaError_t e = cudaFuncSetAttribute(k_band<FMT, C>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    int per_sm = 0;
+    if (e == cudaSuccess) e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_band<FMT, C>, C::NT, smem);
+    if (e != cudaSuccess) return e;
+    k_band<FMT, C><<<sms * (per_sm > 0 ? per_sm : 1), C::NT, smem, s>>>(P, io);
+    return cudaGetLastError();
+}
+
 template <int FMT>
 int run_batch(const Params &P, const logan_options_t *opt, bool wide_only, logan_result_t *out, uint64_t *cells,
                      logan_stats_t *stats, uint8_t *ws, const Layout &L, cudaStream_t s) {
@@ -545,6 +558,7 @@ int run_batch(const Params &P, const logan_options_t *opt, bool wide_only, logan
     if (cudaGetLastError() != cudaSuccess) return LOGAN_ECUDA;
     if (!mark(0, 1)) return LOGAN_ECUDA;
 
+    bool band2 = false;  // the band level ran its second stage (its output list is the other one)
     for (int lv = first; lv < NLEVEL; ++lv) {
         // substitution matrices have no band level: tasks that outgrow the widest
         // window go straight on to the CTA level (which restarts them)
@@ -579,14 +593,20 @@ int run_batch(const Params &P, const logan_options_t *opt, bool wide_only, logan
             }
         } else if (lv == BAND_LEVEL) {
           if constexpr (!no_band) {
-            const int smem = (int)BandSmem<FMT>::BYTES;
-            e = cudaFuncSetAttribute(k_band<FMT>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-            int per_sm = 0;
-            if (e == cudaSuccess)
-                e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_band<FMT>, BAND_NT, smem);
+            // stage 1: one warp per task, a 4096-slot ring; the bands that outgrow it
+            // restart in stage 2 (four warps, 8192 slots), whose overflow goes on to level 8
+            e = launch_band<FMT, BandSmall>(P, io, sms, s);
             if (e == cudaSuccess) {
-                k_band<FMT><<<sms * (per_sm > 0 ? per_sm : 1), BAND_NT, smem, s>>>(P, io);
-                e = cudaGetLastError();
+                LevelIO io2 = io;
+                io2.list = lists[out_sel];
+                io2.count = &ctr[CTR_OUT + lv];
+                io2.in_recs = nullptr;
+                io2.rec_in = nullptr;
+                io2.cursor = &ctr[CTR_BAND2_CURSOR];
+                io2.out_list = lists[out_sel ^ 1];
+                io2.out_count = &ctr[CTR_BAND2_OUT];
+                e = launch_band<FMT, BandBig>(P, io2, sms, s);
+                band2 = true;
             }
           }
         } else {
@@ -598,12 +618,13 @@ int run_batch(const Params &P, const logan_options_t *opt, bool wide_only, logan
         }
         if (e != cudaSuccess) return LOGAN_ECUDA;
         if (!mark(1 + lv, 1)) return LOGAN_ECUDA;
-        in_list = lists[out_sel];
+        in_list = band2 ? lists[out_sel ^ 1] : lists[out_sel];
         in_recs = (lv < NWIDTH) ? recs[out_sel] : nullptr;
         rec_in = (lv < NWIDTH) ? (const int32_t *)(ws + L.pool[lv]) : nullptr;
         rec_in_stride = (lv < NWIDTH) ? rec_ints(width_of(lv)) : 0;
-        in_count = &ctr[CTR_OUT + lv];
+        in_count = band2 ? &ctr[CTR_BAND2_OUT] : &ctr[CTR_OUT + lv];
         out_sel ^= 1;
+        band2 = false;
     }
     int grid3 = (int)((P.n_pairs + per_block - 1) / per_block);
     if (grid3 > sms * 8) grid3 = sms * 8;

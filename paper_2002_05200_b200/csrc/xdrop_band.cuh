@@ -1,5 +1,6 @@
 // xdrop_band.cuh — level 7, wide bands: one CTA per task sweeps the band as
-// packed int16 pairs held in a shared-memory ring.
+// packed int16 pairs held in a shared-memory ring (stage 1: one warp per task,
+// 4096 slots; stage 2, for the bands that outgrow it: four warps, 8192 slots).
 //
 // Same method and cell rule as the register windows (eq. P:85, drop rule P:89,
 // best after the complete antidiagonal P:178, band trimming and termination
@@ -10,8 +11,8 @@
 // row 1), where the band is the whole antidiagonal of the extension's matrix.
 //
 // B200 design:
-//  * Values are int16 in a ring of BAND_SLOTS slots per parity; slot s lives
-//    at ring index s mod BAND_SLOTS, two slots per 32-bit word, so the band
+//  * Values are int16 in a ring of SLOTS slots per parity (BandCfg); slot s
+//    lives at ring index s mod SLOTS, two slots per 32-bit word, so the band
 //    never has to be re-centred. Live u <= X + 2*127 < 2^15 for X <= 30000;
 //    every dead value is exactly D16 = -16384.
 //  * The cell runs on the pairs directly (DPX .S16x2: VIMNMX3, VIADDMNMX, and
@@ -45,29 +46,31 @@
 
 namespace logan {
 
-constexpr int BAND_SLOTS = 8192;              // ring slots per parity
-constexpr int BAND_WORDS = BAND_SLOTS / 2;    // int16x2 words per parity
 constexpr int BAND_XMAX = 30000;              // live u <= X + 2*127 must fit int16
 constexpr int BAND_MARGIN = 128;              // slots kept free between the band's ends
-#ifndef LOGAN_BAND_CAP
-#define LOGAN_BAND_CAP 8192
-#endif
 #ifndef LOGAN_BAND_PAD
 #define LOGAN_BAND_PAD 48
 #endif
-// code positions per read buffer (circular): the codes a planned antidiagonal
-// needs span at most BAND_SLOTS - BAND_MARGIN + 2 positions; with BAND_PAD of
-// slack on both sides and word rounding they must fit
-constexpr int BAND_CAP = LOGAN_BAND_CAP;
 constexpr int BAND_PAD = LOGAN_BAND_PAD;      // codes staged beyond the needed range
-static_assert(BAND_SLOTS - BAND_MARGIN + 2 + 2 * BAND_PAD + 16 <= BAND_CAP, "code buffer too small for the ring");
 constexpr uint32_t D16X2 = 0xC000C000u;       // two dead slots (-16384 each)
-#ifndef LOGAN_BAND_NT
-#define LOGAN_BAND_NT 128
-#endif
-constexpr int BAND_NT = LOGAN_BAND_NT;        // threads per task (= per block)
-constexpr int BAND_NW = BAND_NT / 32;
-constexpr int BAND_ARG_WARP = BAND_NW > 1 ? 1 : 0;  // the warp that keeps the argmax
+
+// Launch configuration of the band level: threads per task (= per block) and
+// ring slots per parity. The band level runs in two stages (logan_impl.cuh):
+// one warp per task with a 4096-slot ring (20 KB of shared memory: 11 tasks per
+// SM; no barrier waits, the per-antidiagonal scalar work done once per task
+// instead of once per warp), then the bands that outgrow it on 4 warps with an
+// 8192-slot ring. Code positions per read buffer (circular): the codes a planned
+// antidiagonal needs span at most SLOTS - BAND_MARGIN + 2 positions; with
+// BAND_PAD of slack on both sides and word rounding they must fit CAP.
+template <int NT_, int SLOTS_>
+struct BandCfg {
+    static constexpr int NT = NT_, NW = NT_ / 32;
+    static constexpr int ARG_WARP = NW > 1 ? 1 : 0;  // the warp that keeps the argmax
+    static constexpr int SLOTS = SLOTS_, WORDS = SLOTS_ / 2, CAP = SLOTS_;
+    static_assert(SLOTS - BAND_MARGIN + 2 + 2 * BAND_PAD + 16 <= CAP, "code buffer too small for the ring");
+};
+using BandSmall = BandCfg<32, 4096>;
+using BandBig = BandCfg<128, 8192>;
 
 template <int FMT> struct BandFmt;
 template <> struct BandFmt<LOGAN_SEQ_2BIT> { static constexpr int CB = 4; };  // one nibble per base
@@ -76,17 +79,17 @@ template <> struct BandFmt<LOGAN_SEQ_U8> { static constexpr int CB = 8; };    //
 // Shared-memory layout (32-bit words). Each code buffer has CAPW words plus
 // MIRROR copies of its first words behind the end, so the words a chunk needs
 // are consecutive without a second wrap.
-template <int FMT>
+template <int FMT, class C>
 struct BandSmem {
     static constexpr int CB = BandFmt<FMT>::CB;
     static constexpr int CPW = 32 / CB;                 // codes per word
-    static constexpr int CAPW = BAND_CAP / CPW;         // words per read buffer
+    static constexpr int CAPW = C::CAP / CPW;         // words per read buffer
     static constexpr int MIRROR = 4;
-    static constexpr size_t VAL = 0;                    // uint32 val[2][BAND_WORDS]
-    static constexpr size_t CA = VAL + 2 * BAND_WORDS;  // uint32 ca[CAPW + MIRROR]
+    static constexpr size_t VAL = 0;                    // uint32 val[2][C::WORDS]
+    static constexpr size_t CA = VAL + 2 * C::WORDS;  // uint32 ca[CAPW + MIRROR]
     static constexpr size_t CBUF = CA + CAPW + MIRROR;  // uint32 cb[CAPW + MIRROR]
-    static constexpr size_t RED = CBUF + CAPW + MIRROR; // int4 red[2][BAND_NW]
-    static constexpr size_t WORDS = RED + 2 * BAND_NW * 4;
+    static constexpr size_t RED = CBUF + CAPW + MIRROR; // int4 red[2][C::NW]
+    static constexpr size_t WORDS = RED + 2 * C::NW * 4;
     static constexpr size_t BYTES = WORDS * sizeof(uint32_t);
     static_assert(RED % 4 == 0, "int4 alignment");
 };
@@ -117,10 +120,10 @@ __device__ __forceinline__ int32_t sext_hi(uint32_t w) { return (int32_t)w >> 16
 
 // Mismatch masks of the 4 slot pairs of a chunk: mk[k] has 0xffff in the half
 // of slot 2k (low) / 2k+1 (high) iff the two codes differ.
-template <int FMT> struct BandCodes;
+template <int FMT, class C> struct BandCodes;
 
-template <> struct BandCodes<LOGAN_SEQ_2BIT> {
-    using S = BandSmem<LOGAN_SEQ_2BIT>;
+template <class C> struct BandCodes<LOGAN_SEQ_2BIT, C> {
+    using S = BandSmem<LOGAN_SEQ_2BIT, C>;
     uint32_t x;  // nibble r = code of slot s0 + r
     // the chunk's codes start at position q = 8 * c8 + off: word c8 + (off >> 3),
     // bit offset 4 * (off & 7)
@@ -146,8 +149,8 @@ template <> struct BandCodes<LOGAN_SEQ_2BIT> {
     }
 };
 
-template <> struct BandCodes<LOGAN_SEQ_U8> {
-    using S = BandSmem<LOGAN_SEQ_U8>;
+template <class C> struct BandCodes<LOGAN_SEQ_U8, C> {
+    using S = BandSmem<LOGAN_SEQ_U8, C>;
     uint32_t lo, hi;  // byte r = code of slot s0 + r
     // the chunk's codes start at position q = 8 * c8 + off: word 2 * c8 + (off >> 2)
     __device__ __forceinline__ static int32_t wstep() { return 2; }
@@ -186,18 +189,18 @@ struct BandTask {
     uint64_t cells, cells_entry;
 };
 
-template <int FMT>
+template <int FMT, class C>
 struct BandCta {
-    using S = BandSmem<FMT>;
-    using Codes = BandCodes<FMT>;
+    using S = BandSmem<FMT, C>;
+    using Codes = BandCodes<FMT, C>;
     int tid, lane, warp;
     BandTask t;
 
     __device__ __forceinline__ static uint32_t *sm() { return (uint32_t *)band_smem; }
-    __device__ __forceinline__ static uint32_t *val(int p) { return sm() + S::VAL + p * BAND_WORDS; }
+    __device__ __forceinline__ static uint32_t *val(int p) { return sm() + S::VAL + p * C::WORDS; }
     __device__ __forceinline__ static uint32_t *ca() { return sm() + S::CA; }
     __device__ __forceinline__ static uint32_t *cb() { return sm() + S::CBUF; }
-    __device__ __forceinline__ static int4 *red(int p) { return (int4 *)(sm() + S::RED) + p * BAND_NW; }
+    __device__ __forceinline__ static int4 *red(int p) { return (int4 *)(sm() + S::RED) + p * C::NW; }
 
     // Stage the codes of unwrapped positions [q_lo, q_hi) into buf: a uses
     // code(q) = a_q, b uses code(q) = b_{-q}; positions outside the read hold 0
@@ -207,7 +210,7 @@ struct BandCta {
         constexpr int CPW = S::CPW, CB = S::CB;
         const int32_t w0 = q_lo >> (CB == 4 ? 3 : 2), w1 = (q_hi - 1) >> (CB == 4 ? 3 : 2);
 #pragma unroll 1
-        for (int32_t w = w0 + tid; w <= w1; w += BAND_NT) {
+        for (int32_t w = w0 + tid; w <= w1; w += C::NT) {
             uint32_t x = 0;
 #pragma unroll 1
             for (int r = 0; r < CPW; ++r) {
@@ -231,9 +234,9 @@ struct BandCta {
         uint4 *v4 = (uint4 *)val(0);
         const uint4 z = make_uint4(D16X2, D16X2, D16X2, D16X2);
 #pragma unroll 4
-        for (int q = tid; q < 2 * BAND_WORDS / 4; q += BAND_NT) v4[q] = z;
+        for (int q = tid; q < 2 * C::WORDS / 4; q += C::NT) v4[q] = z;
         if (P.poison) {  // test knob: code buffers start as garbage (stale smem is arbitrary)
-            for (int q = tid; q < 2 * (S::CAPW + S::MIRROR); q += BAND_NT) ca()[q] = 0xffffffffu;  // every nibble 15: the worst case for the mismatch-flag carry
+            for (int q = tid; q < 2 * (S::CAPW + S::MIRROR); q += C::NT) ca()[q] = 0xffffffffu;  // every nibble 15: the worst case for the mismatch-flag carry
         }
         __syncthreads();
     }
@@ -276,8 +279,8 @@ struct BandCta {
         t.cells = (uint64_t)(uint32_t)rec[16] | ((uint64_t)(uint32_t)rec[17] << 32);
         t.cells_entry = t.cells;
         uint16_t *v0 = (uint16_t *)val(0), *v1 = (uint16_t *)val(1);
-        for (int q = tid; q < Wsrc; q += BAND_NT) {
-            const int32_t ri = (S0src + q) & (BAND_SLOTS - 1);
+        for (int q = tid; q < Wsrc; q += C::NT) {
+            const int32_t ri = (S0src + q) & (C::SLOTS - 1);
             // live values are < 2^15 (X <= BAND_XMAX); every dead value becomes D16
             const int32_t e = rec[REC_HDR + q], o = rec[REC_HDR + Wsrc + q];
             v0[ri] = (uint16_t)(e < 0 ? -16384 : e);
@@ -291,7 +294,7 @@ struct BandCta {
     // First / last live slot of the chunk at slot c (8-aligned) of array p:
     // sign-replicated high bytes of the four pairs give one dead flag per slot.
     __device__ __forceinline__ void chunk_live(int p, int32_t c, uint32_t &live0, uint32_t &live1) const {
-        const uint4 w = *(const uint4 *)(val(p) + ((c >> 1) & (BAND_WORDS - 1)));
+        const uint4 w = *(const uint4 *)(val(p) + ((c >> 1) & (C::WORDS - 1)));
         live0 = ~prmt(w.x, w.y, 0xFDB9u);  // bytes: slots 0..3, 0xff = live
         live1 = ~prmt(w.z, w.w, 0xFDB9u);  // slots 4..7
     }
@@ -367,20 +370,20 @@ struct BandCta {
             // the highest warp takes the first chunks of every pass: in a partial
             // last pass warp 0, which has the per-antidiagonal extra work (exact
             // extents, cell count, argmax) after the barrier, is the idle one
-            for (int32_t c8w = c8base + 32 * (BAND_NW - 1 - warp); c8w <= c8last; c8w += BAND_NT) {
+            for (int32_t c8w = c8base + 32 * (C::NW - 1 - warp); c8w <= c8last; c8w += C::NT) {
                 const int32_t c8 = c8w + lane;
                 const int32_t s0 = 8 * c8;
                 const bool active = c8 <= c8last;
-                const int32_t ri = (c8 & (BAND_SLOTS / 8 - 1)) * 4;  // word of slot s0
+                const int32_t ri = (c8 & (C::SLOTS / 8 - 1)) * 4;  // word of slot s0
                 const uint4 dw = *(const uint4 *)(cur + ri);  // d-2 (diag)
                 const uint4 pw = *(const uint4 *)(oth + ri);  // d-1
                 uint32_t nb;  // the neighbouring pair of d-1 beyond this chunk
                 if (PAR) {
                     nb = __shfl_down_sync(0xffffffffu, pw.x, 1);
-                    if (lane == 31) nb = oth[(ri + 4) & (BAND_WORDS - 1)];
+                    if (lane == 31) nb = oth[(ri + 4) & (C::WORDS - 1)];
                 } else {
                     nb = __shfl_up_sync(0xffffffffu, pw.w, 1);
-                    if (lane == 0) nb = oth[(ri - 1) & (BAND_WORDS - 1)];
+                    if (lane == 0) nb = oth[(ri - 1) & (C::WORDS - 1)];
                 }
                 Codes A, B;
                 A.load(ca(), Codes::wstep() * c8 + wa, sha);  // slot s0 + r holds a_{s0 + r + ch}
@@ -442,7 +445,7 @@ struct BandCta {
         __syncthreads();
         // fold the NW partials: lane w reads warp w's (one LDS), CREDUX combines
         int4 r = make_int4(INT32_MIN, -1, -1, 0);
-        if (lane < BAND_NW) r = red(PAR)[lane];
+        if (lane < C::NW) r = red(PAR)[lane];
         const int32_t K = __reduce_max_sync(0xffffffffu, r.x);
         const uint32_t FC = __reduce_min_sync(0xffffffffu, (uint32_t)r.y);
         const int32_t LC = __reduce_max_sync(0xffffffffu, r.z);
@@ -456,9 +459,9 @@ struct BandCta {
             const int32_t V = M + Tc;
             if (V > t.best) {
                 t.best = V;
-                if (warp == BAND_ARG_WARP) {  // (warp 0 has the exact extents and the cell count)
+                if (warp == C::ARG_WARP) {  // (warp 0 has the exact extents and the cell count)
                     const int32_t c = hbase + 8 * (1023 - (K & 1023));
-                    const uint4 w = *(const uint4 *)(cur + ((c >> 1) & (BAND_WORDS - 1)));
+                    const uint4 w = *(const uint4 *)(cur + ((c >> 1) & (C::WORDS - 1)));
                     const uint32_t W4[4] = {w.x, w.y, w.z, w.w};
                     int32_t r = 7;
 #pragma unroll
@@ -497,18 +500,18 @@ struct BandCta {
         // (8) the next antidiagonal touches at most the span of both arrays'
         //     written slots widened by 9 on each side: it must fit the ring
         const int32_t lo = min(t.Dlo[0], t.Dlo[1]), hi = max(t.Dhi[0], t.Dhi[1]);
-        if (hi - lo + 1 > BAND_SLOTS - BAND_MARGIN) return 2;
+        if (hi - lo + 1 > C::SLOTS - BAND_MARGIN) return 2;
         return 0;
     }
 };
 
 // Persistent kernel: each CTA pulls tasks (or hand-over records) from the
 // level's list and sweeps them to the end; overflow goes to the next level.
-template <int FMT>
-__global__ void __launch_bounds__(BAND_NT) k_band(const Params P, const LevelIO io) {
+template <int FMT, class C>
+__global__ void __launch_bounds__(C::NT) k_band(const Params P, const LevelIO io) {
     __shared__ uint32_t s_pos;
     __shared__ int32_t s_arg[2];  // the argmax warp's result, for the writer (thread 0)
-    BandCta<FMT> c;
+    BandCta<FMT, C> c;
     c.tid = threadIdx.x;
     c.lane = threadIdx.x & 31;
     c.warp = threadIdx.x >> 5;
@@ -531,7 +534,7 @@ __global__ void __launch_bounds__(BAND_NT) k_band(const Params P, const LevelIO 
                 rc = (c.t.d & 1) ? c.template step<0>(P) : c.template step<1>(P);
             } while (rc == 0);
         }
-        if (c.tid == 32 * BAND_ARG_WARP) { s_arg[0] = c.t.arg_i; s_arg[1] = c.t.arg_j; }
+        if (c.tid == 32 * C::ARG_WARP) { s_arg[0] = c.t.arg_i; s_arg[1] = c.t.arg_j; }
         __syncthreads();
         if (c.tid == 0) {
             if (rc == 1) {
