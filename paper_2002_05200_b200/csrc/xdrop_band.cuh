@@ -436,19 +436,28 @@ struct BandCta {
         }
 
         // (5) antidiagonal reductions: warp CREDUX, one barrier, fold NW partials
+        //     (one warp per task: the warp's CREDUX results are final, and a warp
+        //     barrier orders the ring writes for the next antidiagonal)
+        int32_t K, LC;
+        uint32_t FC;
         {
-            const int32_t K = __reduce_max_sync(0xffffffffu, runkey);
-            const uint32_t FC = __reduce_min_sync(0xffffffffu, fc);
-            const int32_t LC = __reduce_max_sync(0xffffffffu, lc);
-            if (lane == 0) red(PAR)[warp] = make_int4(K, (int32_t)FC, LC, 0);
+            const int32_t K0 = __reduce_max_sync(0xffffffffu, runkey);
+            const uint32_t FC0 = __reduce_min_sync(0xffffffffu, fc);
+            const int32_t LC0 = __reduce_max_sync(0xffffffffu, lc);
+            if constexpr (C::NW == 1) {
+                K = K0; FC = FC0; LC = LC0;
+                __syncwarp();
+            } else {
+                if (lane == 0) red(PAR)[warp] = make_int4(K0, (int32_t)FC0, LC0, 0);
+                __syncthreads();
+                // fold the NW partials: lane w reads warp w's (one LDS), CREDUX combines
+                int4 r = make_int4(INT32_MIN, -1, -1, 0);
+                if (lane < C::NW) r = red(PAR)[lane];
+                K = __reduce_max_sync(0xffffffffu, r.x);
+                FC = __reduce_min_sync(0xffffffffu, (uint32_t)r.y);
+                LC = __reduce_max_sync(0xffffffffu, r.z);
+            }
         }
-        __syncthreads();
-        // fold the NW partials: lane w reads warp w's (one LDS), CREDUX combines
-        int4 r = make_int4(INT32_MIN, -1, -1, 0);
-        if (lane < C::NW) r = red(PAR)[lane];
-        const int32_t K = __reduce_max_sync(0xffffffffu, r.x);
-        const uint32_t FC = __reduce_min_sync(0xffffffffu, (uint32_t)r.y);
-        const int32_t LC = __reduce_max_sync(0xffffffffu, r.z);
         const bool h = LC >= 0;
 
         // (6) best after the complete antidiagonal, strict increase;
@@ -514,7 +523,7 @@ __global__ void __launch_bounds__(C::NT) k_band(const Params P, const LevelIO io
     BandCta<FMT, C> c;
     c.tid = threadIdx.x;
     c.lane = threadIdx.x & 31;
-    c.warp = threadIdx.x >> 5;
+    c.warp = C::NW == 1 ? 0 : (int)(threadIdx.x >> 5);  // (a constant with one warp per task)
     const uint32_t count = *io.count;
     for (;;) {
         if (c.tid == 0) s_pos = atomicAdd(io.cursor, 1u);

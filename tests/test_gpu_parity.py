@@ -487,6 +487,30 @@ def test_ring_overflow_and_large_x_go_to_cta_level():
             assert s["tasks_finished"][7] >= 1  # the 9 kb extension finished on the CTA level
 
 
+def test_band_level_second_stage():
+    """Bands between the first stage's 4096-slot ring and the second stage's 8192
+    slots (two 6 kb near-identical reads at X = 20000: the band is the whole
+    antidiagonal): the first stage restarts them on the second, which finishes
+    them exactly; nothing reaches the CTA level. Both pool formats."""
+    rng = np.random.default_rng(11)
+    base = "".join(rng.choice(list("ACGT"), 6000))
+    mut = list(base)
+    for p in rng.choice(6000, 200, replace=False):
+        mut[p] = "ACGT"[("ACGT".index(mut[p]) + 1) % 4]
+    pairs = [(base, "".join(mut), 0, 0), (base[:2000], "".join(mut)[:2000], 1000, 1000)]
+    b = datagen.from_strings(pairs, k=5)
+    X = 20000
+    ref = oracle_run(b, X)
+    for fmt in FMTS:
+        for lvl in (7, None):
+            st = logan.new_stats()
+            got = gpu_run(b, X, fmt=fmt, first_level=lvl, stats=st)
+            assert_same(*got, *ref, what=f"band stage 2 fmt={fmt} level={lvl}")
+            s = logan.stats_dict(st)
+            assert s["tasks_finished"][7] == 0 and s["tasks_finished"][6] >= 1, s
+            assert s["tasks_started"][6] > s["tasks_finished"][6], s  # a stage-1 restart
+
+
 def test_band_level_restages_codes_on_long_reads():
     """Extensions much longer than the band level's staged code window (a 16384-
     position circular buffer, refilled when the band drifts out of it): 14 kb
