@@ -70,6 +70,8 @@ def parse_args(argv=None):
                     help="tuning knob: force the first window's slots (16/20/24/28/32; 0 = automatic)")
     ap.add_argument("--latency-first", action="store_true",
                     help="run the first level in its latency shape (one warp per task)")
+    ap.add_argument("--throughput-first", action="store_true",
+                    help="tuning knob: run the first level in its throughput shape even with few tasks")
     ap.add_argument("--share", default=None,
                     help="r/N: run only rank r's share of an N-way split of the batch, on one GPU")
     ap.add_argument("--no-e2e", action="store_true")
@@ -404,7 +406,7 @@ def main(argv=None):
         logan.xdrop_batch(db, w.match, w.mismatch, w.gap, w.xdrop, workspace=ws, out=out, cells=cells,
                           stats=stats, first_level=first, stream=stream, timing_events=events,
                           latency_first=args.latency_first, subst=subst, zdrop=args.zdrop, pack_u8=pack_u8,
-                          first_slots=args.first_slots)
+                          first_slots=args.first_slots, throughput_first=args.throughput_first)
 
     # one untimed run with device stats: per-level task and cell counts (deterministic)
     st = logan.new_stats(dev)
