@@ -327,8 +327,10 @@ static cudaError_t launch_width_pk(int wi, bool latency, bool helpers, const Par
         case 4: return launch_win<4, 32, FMT, 0, 0, PK>(P, io, hio, sms, s);
         case 6: return launch_win<8, 32, FMT, 0, 0, PK>(P, io, hio, sms, s);
         case 8: return launch_win<16, 32, FMT, 0, 0, PK>(P, io, hio, sms, s);
+        case 5: return launch_win<32, 4, FMT, 0, 0, PK>(P, io, hio, sms, s);   // W = 128, one warp
+        case 7: return launch_win<32, 8, FMT, 0, 0, PK>(P, io, hio, sms, s);   // W = 256, one warp
         case 9: return launch_win<32, 16, FMT, 0, 0, PK>(P, io, hio, sms, s);
-        default: break;  // one-warp shapes with fewer than 16 slots per lane: int32
+        default: break;  // W = 64 on one warp (2 slots per lane): int32
     }
     return cudaErrorNotSupported;
 }
@@ -338,7 +340,7 @@ static cudaError_t launch_width(int wi, bool latency, bool helpers, const Params
                                 const LevelIO &hio, int sms, cudaStream_t s, int w0, int w5, bool g2 = false) {
     if (wi == 0 && !(latency && w0 == 32)) return launch_first<FMT>(w0, helpers && !latency, g2, P, io, hio, sms, s);
     // 2-bit pools (no Z-drop) at X <= 16000: the packed int16 windows for the
-    // throughput shapes (G x 32 slots) and the one-warp shapes with >= 16 slots per lane
+    // throughput shapes (G x 32 slots) and the one-warp shapes of W >= 128 (4 or more slots per lane)
     if constexpr (FMT == LOGAN_SEQ_2BIT) {
         if (P.xdrop <= PACK_XMAX && !P.nopack) {
 #ifndef LOGAN_NO_M2

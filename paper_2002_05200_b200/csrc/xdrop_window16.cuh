@@ -67,7 +67,9 @@ __device__ __forceinline__ int32_t hi16(uint32_t w) { return ((int32_t)w) >> 16;
 template <int G, int R, int FMT, bool M2>
 struct Window16 {
     static_assert(FMT == LOGAN_SEQ_2BIT, "packed window: 2-bit pools");
-    static_assert(R % 4 == 0 && R >= 16 && R <= 32 && (G & (G - 1)) == 0 && G * R <= 1024, "packed window shape");
+    // R = 4 and 8 only as one-warp latency shapes (W = 128, 256): one base word per lane
+    static_assert(R % 4 == 0 && R >= 4 && R <= 32 && (R >= 16 || G == 32) && (G & (G - 1)) == 0 && G * R <= 1024,
+                  "packed window shape");
     static constexpr int GG = G, W = G * R, H = R / 2;
     static constexpr int CB = 4, FPW = 8;
     static constexpr int NW = (R + FPW - 1) / FPW;
