@@ -479,16 +479,20 @@ def main(argv=None):
     dom_ms = stage_ms[dom_stage] / args.steps
     dom_cells = stats["cells_per_level"][dom_level]
     sm_max = clocks.get("sm_max_mhz") or 1965.0
-    # the packed int16 kernels: the first window of a 2-bit pool at X <= 16000 (no
-    # Z-drop; options.flags bit 4 off) and the band level
-    packed = (dom_level == 0 and (fmt == logan.LOGAN_SEQ_2BIT or u8_packed) and w.xdrop <= 16000 and args.zdrop is None
-              and not protein) or dom_level == 6
+    # the packed int16 kernels: the register windows of a 2-bit pool at X <= 16000 (no
+    # Z-drop, no matrix; options.flags bit 4 off) except the int32 one-warp shapes of
+    # W <= 64, and the band level
+    first = stats.get("first_level", 0) - 1
+    lat_narrow = (dom_level == first and stats.get("first_shape") == "latency"
+                  and 0 < stats.get("first_width", 0) <= 64)
+    packed = (dom_level <= 5 and (fmt == logan.LOGAN_SEQ_2BIT or u8_packed) and w.xdrop <= 16000
+              and args.zdrop is None and not protein and not lat_narrow) or dom_level == 6
     peak_tops, peak_how, peak32 = int_peak(sm_max, packed)
     achieved_tops = N_REF_OPS_PER_CELL * dom_cells / (dom_ms / 1e3) / 1e12
     # the library picks window widths from X (from ceil(X / |gap|) with a substitution matrix)
     xband = -(-w.xdrop // -w.gap) if subst is not None else w.xdrop
     level_names = [f"window{logan._lib.load().logan_level_width(lv + 1, xband, db.max_ext_len, 0)}"
-                   for lv in range(6)] + ["band8192", "wide_cta"]
+                   for lv in range(6)] + ["band, 4096 / 8192-slot rings", "wide_cta"]
     ncu_key = f"{w.name}/{args.fmt}/level{dom_level + 1}"
     ev_ncu = ncu_evidence(ncu_key)
     roofline = {"bound": "alu", "achieved": achieved_tops, "peak": peak_tops, "unit": "TOP/s",
