@@ -22,3 +22,8 @@ done
 ncu --metrics gpu__time_duration.sum --clock-control none -c 200 --csv --log-file gpurun_out/${TAG}_launches.csv \
   python bench.py --steps 2 --warmup 1 --no-e2e --no-cpu-baseline --parity-seconds 0.3 > gpurun_out/${TAG}_launches_bench.log 2>&1
 ls -la gpurun_out
+timeout 600 python bench.py --impl reference --steps 2 --warmup 3 > gpurun_out/${TAG}_ref.json 2> gpurun_out/${TAG}_ref.err
+for a in "--config 3 --xdrop 10" "--config 3 --xdrop 50" "--config 3 --xdrop 100" "--config 4" "--config 5" "--fmt u8" "--zdrop 20" "--config 6 --xdrop 5000"; do
+  n=$(echo "$a" | tr -d ' -')
+  timeout 900 python bench.py $a --steps 3 --warmup 3 --no-cpu-baseline 2>/dev/null | grep "^{" > gpurun_out/${TAG}_cfg_$n.json
+done
