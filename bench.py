@@ -459,7 +459,12 @@ def main(argv=None):
         except RuntimeError:
             pass  # stage not launched in this configuration
     n_launch_stages = [stg for stg in stage_ms if 1 <= stg <= nst - 2]
-    launches_per_step = 3 + len(n_launch_stages) + 1 + int(pack_u8)  # [pack,] expand, scan, scatter, levels, combine
+    # [pack,] expand, scan, scatter, the levels, combine: the first level is one launch, a
+    # later window level two (latency and throughput shapes, one exits at once), the band
+    # level two (its two stages), the CTA level one
+    first_stage = stats["first_level"]  # stage of the first level (stage s = level s)
+    per_stage = lambda stg: 1 if (stg == first_stage or stg == nst - 2) else 2
+    launches_per_step = 3 + sum(per_stage(stg) for stg in n_launch_stages) + 1 + int(pack_u8)
 
     # max over ranks (time), sum over ranks (cells)
     t = torch.tensor([total_ms], dtype=torch.float64, device=dev)
@@ -621,7 +626,10 @@ def main(argv=None):
     if rank == 0:
         line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
                 "warmup": args.warmup, "ms_per_step": total_ms_max / args.steps,
-                "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "int32",
+                "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
+                # the dominant kernel's arithmetic: int16 pairs (two cells per DPX .S16x2
+                # instruction) in the packed windows and the band level, int32 otherwise
+                "dtype": "int16x2" if packed else "int32",
                 "data": "synthetic (datagen, seeded; DESIGN.md §5)",
                 "config": config_dict(w, n, args.fmt + (" (re-encoded to 2-bit on the device each step, logan_pack_2bit)" if u8_packed else ""), args.first_level, world, share),
                 "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e, "parity": parity,
