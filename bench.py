@@ -524,19 +524,22 @@ def main(argv=None):
         pin = lambda a: torch.from_numpy(np.ascontiguousarray(a)).pin_memory().numpy()
         hp = [pin(x) for x in (pool_np, batch.q_off, batch.q_len, batch.t_off, batch.t_len,
                                batch.q_seed, batch.t_seed)]
-        hout = [torch.empty((n_local, 5), dtype=torch.int32).pin_memory().numpy() for _ in range(2)]
-        hcells = [torch.empty(n_local, dtype=torch.int64).pin_memory().numpy().view(np.uint64) for _ in range(2)]
-        arenas = [logan.HostArena(n_local, batch.pool_len, fmt, db.max_ext_len, device=dev) for _ in range(2)]
-        streams = [torch.cuda.Stream(dev) for _ in range(2)]
+        # three arenas / streams: step s's copies overlap the sweeps of steps s-1 and s-2
+        # (two: C3 25.9 ms per step, three: 25.0; profiles/r02/e2e_probe_v21.txt)
+        NE2E = 3
+        hout = [torch.empty((n_local, 5), dtype=torch.int32).pin_memory().numpy() for _ in range(NE2E)]
+        hcells = [torch.empty(n_local, dtype=torch.int64).pin_memory().numpy().view(np.uint64) for _ in range(NE2E)]
+        arenas = [logan.HostArena(n_local, batch.pool_len, fmt, db.max_ext_len, device=dev) for _ in range(NE2E)]
+        streams = [torch.cuda.Stream(dev) for _ in range(NE2E)]
         pool_bytes = (batch.pool_len + 3) // 4 if fmt == logan.LOGAN_SEQ_2BIT else batch.pool_len
 
         def e2e_step(s):
             logan.xdrop_batch_host(hp[0], fmt, batch.pool_len, *hp[1:], w.k, w.match, w.mismatch,
-                                   w.gap, w.xdrop, arenas[s % 2], out=hout[s % 2], cells=hcells[s % 2],
-                                   first_level=first, stream=streams[s % 2], asynchronous=True, subst=subst,
+                                   w.gap, w.xdrop, arenas[s % NE2E], out=hout[s % NE2E], cells=hcells[s % NE2E],
+                                   first_level=first, stream=streams[s % NE2E], asynchronous=True, subst=subst,
                                    zdrop=args.zdrop)
 
-        for s_ in range(2):
+        for s_ in range(NE2E):
             e2e_step(s_)
         torch.cuda.synchronize()
         ke = max(4, args.steps)  # same K as the device-timed steps (steady state)
@@ -545,11 +548,12 @@ def main(argv=None):
         torch.cuda.synchronize()
         a0 = torch.cuda.Event(enable_timing=True)
         a0.record(streams[0])
-        streams[1].wait_event(a0)
+        for st_ in streams[1:]:
+            st_.wait_event(a0)
         for s_ in range(ke):
-            if s_ >= 2:
-                streams[s_ % 2].synchronize()  # step s-2's outputs are read before its buffers are reused
-                assert int(hcells[s_ % 2].sum()) == cells_step
+            if s_ >= NE2E:
+                streams[s_ % NE2E].synchronize()  # step s-NE2E's outputs are read before its buffers are reused
+                assert int(hcells[s_ % NE2E].sum()) == cells_step
             e2e_step(s_)
         ends = []
         for st_ in streams:
@@ -561,12 +565,12 @@ def main(argv=None):
         te = torch.tensor([e2e_ms], dtype=torch.float64, device=dev)
         if world > 1:
             dist.all_reduce(te, op=dist.ReduceOp.MAX)
-        for k_ in range(2):
+        for k_ in range(NE2E):
             assert int(hcells[k_].sum()) == cells_step
             assert (hout[k_] == out_h).all()  # the host entry point gives the device entry point's results
         e2e = {"value": cells_all * ke / (float(te.item()) / 1e3) / 1e9, "unit": UNIT,
                "h2d_bytes_per_step": int(pool_bytes + 32 * n_local), "d2h_bytes_per_step": int(28 * n_local),
-               "steps": ke, "api": "logan_xdrop_batch_host_async (2 arenas / 2 streams, pinned)"}
+               "steps": ke, "api": f"logan_xdrop_batch_host_async ({NE2E} arenas / {NE2E} streams, pinned)"}
 
     # CPU baseline (rank 0 at N = 1 only) and the parity sample: the oracle on this
     # host's cores over a bounded sample of this rank's pairs, compared element by

@@ -7,9 +7,9 @@ groups only.
 """
 from . import _lib
 from ._lib import LOGAN_SEQ_2BIT, LOGAN_SEQ_U8, LoganError
-from .api import (DeviceBatch, HostArena, make_workspace, new_stats, pack_2bit, stats_dict, to_device,
-                  workspace_bytes, xdrop_batch, xdrop_batch_host)
+from .api import (DeviceBatch, HostArena, clear_workspace_cache, make_workspace, new_stats, pack_2bit,
+                  stats_dict, to_device, workspace_bytes, xdrop_batch, xdrop_batch_host)
 
 __all__ = ["LOGAN_SEQ_2BIT", "LOGAN_SEQ_U8", "LoganError", "DeviceBatch", "HostArena",
-           "make_workspace", "new_stats", "pack_2bit", "stats_dict", "to_device", "workspace_bytes",
+           "clear_workspace_cache", "make_workspace", "new_stats", "pack_2bit", "stats_dict", "to_device", "workspace_bytes",
            "xdrop_batch", "xdrop_batch_host", "_lib"]

@@ -41,6 +41,29 @@ def workspace_bytes(n_pairs: int, max_ext_len: int) -> int:
     return int(_lib.load().logan_workspace_bytes(int(n_pairs), int(max_ext_len)))
 
 
+# One workspace per (device, stream), grown on demand and reused by every call on that
+# stream that passes none: stream order makes the reuse safe, and a call does not leave
+# a multi-GB block to the caching allocator that it cannot hand out again until the
+# stream's kernels finish (record_stream).
+_WS_CACHE: dict = {}
+
+
+def _cached_workspace(n_pairs: int, max_ext_len: int, device, stream) -> Workspace:
+    key = (str(device), int(stream.cuda_stream))
+    ws = _WS_CACHE.get(key)
+    if ws is None or ws.n_pairs < n_pairs or ws.max_ext_len < max_ext_len:
+        if ws is not None:
+            n_pairs, max_ext_len = max(n_pairs, ws.n_pairs), max(max_ext_len, ws.max_ext_len)
+        ws = make_workspace(n_pairs, max_ext_len, device)
+        _WS_CACHE[key] = ws
+    return ws
+
+
+def clear_workspace_cache() -> None:
+    """Drop the per-stream workspaces ``xdrop_batch`` keeps when it is passed none."""
+    _WS_CACHE.clear()
+
+
 def make_workspace(n_pairs: int, max_ext_len: int, device=None) -> Workspace:
     torch = _require_cuda()
     nb = workspace_bytes(n_pairs, max_ext_len)
@@ -146,7 +169,9 @@ def xdrop_batch(db: DeviceBatch, match: int, mismatch: int, gap: int, xdrop: int
             out = torch.empty((n, 5), dtype=torch.int32, device=dev)
         if cells is None:
             cells = torch.empty(n, dtype=torch.int64, device=dev)
-        if workspace is None or workspace.n_pairs < n or workspace.max_ext_len < db.max_ext_len:
+        if workspace is None:
+            workspace = _cached_workspace(n, db.max_ext_len, dev, stream)
+        elif workspace.n_pairs < n or workspace.max_ext_len < db.max_ext_len:
             workspace = make_workspace(n, db.max_ext_len, dev)
         # the kernels run asynchronously on `stream`: keep the caching allocator from
         # handing these blocks to another stream's allocation before they finish
