@@ -524,20 +524,25 @@ def main(argv=None):
         pin = lambda a: torch.from_numpy(np.ascontiguousarray(a)).pin_memory().numpy()
         hp = [pin(x) for x in (pool_np, batch.q_off, batch.q_len, batch.t_off, batch.t_len,
                                batch.q_seed, batch.t_seed)]
-        # three arenas / streams: step s's copies overlap the sweeps of steps s-1 and s-2
-        # (two: C3 25.9 ms per step, three: 25.0; profiles/r02/e2e_probe_v21.txt)
+        # one compute stream and a ring of three arenas, the library copying each step's
+        # inputs ahead on its own stream as soon as the arena is free (options.flags bit 6):
+        # every copy overlaps the previous sweeps, and sweeps never overlap each other
+        # (C3: 2 streams 25.9 ms per step, 3 streams 25.0, one stream + copy-ahead 23.7;
+        # profiles/r02/e2e_probe_v22.txt)
         NE2E = 3
         hout = [torch.empty((n_local, 5), dtype=torch.int32).pin_memory().numpy() for _ in range(NE2E)]
         hcells = [torch.empty(n_local, dtype=torch.int64).pin_memory().numpy().view(np.uint64) for _ in range(NE2E)]
         arenas = [logan.HostArena(n_local, batch.pool_len, fmt, db.max_ext_len, device=dev) for _ in range(NE2E)]
-        streams = [torch.cuda.Stream(dev) for _ in range(NE2E)]
+        es = torch.cuda.Stream(dev)
+        done = [torch.cuda.Event() for _ in range(NE2E)]
         pool_bytes = (batch.pool_len + 3) // 4 if fmt == logan.LOGAN_SEQ_2BIT else batch.pool_len
 
         def e2e_step(s):
             logan.xdrop_batch_host(hp[0], fmt, batch.pool_len, *hp[1:], w.k, w.match, w.mismatch,
                                    w.gap, w.xdrop, arenas[s % NE2E], out=hout[s % NE2E], cells=hcells[s % NE2E],
-                                   first_level=first, stream=streams[s % NE2E], asynchronous=True, subst=subst,
-                                   zdrop=args.zdrop)
+                                   first_level=first, stream=es, asynchronous=True, subst=subst,
+                                   zdrop=args.zdrop, copy_ahead=True)
+            done[s % NE2E].record(es)
 
         for s_ in range(NE2E):
             e2e_step(s_)
@@ -547,21 +552,16 @@ def main(argv=None):
             dist.barrier(device_ids=[local])
         torch.cuda.synchronize()
         a0 = torch.cuda.Event(enable_timing=True)
-        a0.record(streams[0])
-        for st_ in streams[1:]:
-            st_.wait_event(a0)
+        a0.record(es)
         for s_ in range(ke):
             if s_ >= NE2E:
-                streams[s_ % NE2E].synchronize()  # step s-NE2E's outputs are read before its buffers are reused
+                done[s_ % NE2E].synchronize()  # step s-NE2E's outputs are read before its buffers are reused
                 assert int(hcells[s_ % NE2E].sum()) == cells_step
             e2e_step(s_)
-        ends = []
-        for st_ in streams:
-            evx = torch.cuda.Event(enable_timing=True)
-            evx.record(st_)
-            ends.append(evx)
+        evx = torch.cuda.Event(enable_timing=True)
+        evx.record(es)
         torch.cuda.synchronize()
-        e2e_ms = max(a0.elapsed_time(evx) for evx in ends)
+        e2e_ms = a0.elapsed_time(evx)
         te = torch.tensor([e2e_ms], dtype=torch.float64, device=dev)
         if world > 1:
             dist.all_reduce(te, op=dist.ReduceOp.MAX)
@@ -570,7 +570,7 @@ def main(argv=None):
             assert (hout[k_] == out_h).all()  # the host entry point gives the device entry point's results
         e2e = {"value": cells_all * ke / (float(te.item()) / 1e3) / 1e9, "unit": UNIT,
                "h2d_bytes_per_step": int(pool_bytes + 32 * n_local), "d2h_bytes_per_step": int(28 * n_local),
-               "steps": ke, "api": f"logan_xdrop_batch_host_async ({NE2E} arenas / {NE2E} streams, pinned)"}
+               "steps": ke, "api": f"logan_xdrop_batch_host_async (one stream, {NE2E} arenas, copy-ahead, pinned)"}
 
     # CPU baseline (rank 0 at N = 1 only) and the parity sample: the oracle on this
     # host's cores over a bounded sample of this rank's pairs, compared element by

@@ -115,6 +115,18 @@ enum {
  *                  live cell -- instead of the argmax; score = seed + best_L +
  *                  best_R as usual. Runs on the CTA level (8) only; match /
  *                  mismatch scoring only (a substitution matrix -> EINVAL).
+ *                  bit 6 = copy-ahead (logan_xdrop_batch_host_async only):
+ *                  the host inputs are copied on a library stream of the
+ *                  device as soon as the device arena is free again (the
+ *                  last call on that arena has written its results), instead
+ *                  of when `stream` reaches this call; `stream` waits for the
+ *                  copies before the sweep. One compute stream with a ring of
+ *                  arenas then overlaps every step's copies with the previous
+ *                  sweeps. The caller must not modify the host inputs after
+ *                  the call until `stream` completes it (as without the flag)
+ *                  and must not rely on earlier work on `stream` producing
+ *                  them (they may be read before it runs). Ignored by the
+ *                  synchronous entry point.
  *                  bit 4 = test / A-B knob: the first window of a 2-bit pool
  *                  runs on int32 values instead of packed int16 pairs.
  *                  bit 1 = test knob: the band level fills its shared-memory

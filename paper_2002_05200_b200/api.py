@@ -74,17 +74,19 @@ def make_workspace(n_pairs: int, max_ext_len: int, device=None) -> Workspace:
 
 def _opts(first_level: int | None, timing_events=None, latency_first: bool = False,
           handover: int = 0, first_slots: int = 0, poison: bool = False, subst=None, zdrop: int | None = None,
-          throughput_first: bool = False, nopack: bool = False, compat: bool = False):
+          throughput_first: bool = False, nopack: bool = False, compat: bool = False,
+          copy_ahead: bool = False):
     """Options struct; ``timing_events`` = list of 2*N_STAGES torch.cuda.Event;
     ``subst`` = square int8 CUDA tensor (alphabet x alphabet) or None."""
     if not first_level and timing_events is None and not latency_first and not handover \
             and not first_slots and not poison and subst is None and zdrop is None and not throughput_first \
-            and not nopack and not compat:
+            and not nopack and not compat and not copy_ahead:
         return None
     o = _lib.Options()
     o.first_level = int(first_level or 0)
     o.flags = (1 if latency_first else 0) | (2 if poison else 0) | (4 if zdrop is not None else 0) \
-        | (8 if throughput_first else 0) | (16 if nopack else 0) | (32 if compat else 0)
+        | (8 if throughput_first else 0) | (16 if nopack else 0) | (32 if compat else 0) \
+        | (64 if copy_ahead else 0)
     o.zdrop = int(zdrop) if zdrop is not None else 0
     o.handover = int(handover)
     o.first_slots = int(first_slots)
@@ -245,12 +247,16 @@ def xdrop_batch_host(pool: np.ndarray, fmt: int, pool_len: int, q_off, q_len, t_
                      q_seed, t_seed, k: int, match: int, mismatch: int, gap: int, xdrop: int,
                      arena: HostArena, out: np.ndarray | None = None,
                      cells: np.ndarray | None = None, first_level: int | None = None, stream=None,
-                     asynchronous: bool = False, subst=None, zdrop: int | None = None):
+                     asynchronous: bool = False, subst=None, zdrop: int | None = None,
+                     copy_ahead: bool = False):
     """End-to-end call with HOST buffers (numpy; pinned memory copies fastest).
 
     ``asynchronous=True`` returns right after enqueuing (``logan_xdrop_batch_host_async``):
     the outputs are valid once ``stream`` is synchronised and the inputs must stay alive
-    until then."""
+    until then. ``copy_ahead=True`` (asynchronous calls; options.flags bit 6) copies the
+    inputs on a library stream as soon as ``arena`` is free instead of when ``stream``
+    reaches the call: with one stream and a ring of arenas, every step's copies overlap
+    the previous sweeps."""
     torch = _require_cuda()
     lib = _lib.load()
     n = len(q_len)
@@ -269,7 +275,7 @@ def xdrop_batch_host(pool: np.ndarray, fmt: int, pool_len: int, q_off, q_len, t_
     fn = lib.logan_xdrop_batch_host_async if asynchronous else lib.logan_xdrop_batch_host
     with torch.cuda.device(dev):
         st = fn(ptr(pool), fmt, pool_len, *[ptr(a) for a in arrs], n, k, sc,
-                _opts(first_level, subst=subst, zdrop=zdrop), ptr(out), ptr(cells),
+                _opts(first_level, subst=subst, zdrop=zdrop, copy_ahead=copy_ahead), ptr(out), ptr(cells),
                 arena.tensor.data_ptr(), arena.nbytes, stream.cuda_stream)
     _lib.check(st)
     return out, cells

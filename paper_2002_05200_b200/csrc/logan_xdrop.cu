@@ -16,6 +16,8 @@
 //   6. level 8    : k_wide, one CTA per task, unbounded band (restart)
 //   7. k_combine  : seed score + L + R -> logan_result_t, cells (c-amb-8/10)
 #include <algorithm>
+#include <mutex>
+#include <unordered_map>
 
 #include "logan_impl.cuh"
 
@@ -187,6 +189,42 @@ int logan_xdrop_batch_host_async(const uint8_t *seq_pool, int32_t seq_fmt, int64
 
 }  // extern "C"
 
+// Copy-ahead (options.flags bit 6, asynchronous host calls): the inputs are copied
+// on a library stream of the device as soon as the ARENA is free (its last call's
+// results are out), not when `stream` reaches the call, so one compute stream with
+// a ring of arenas overlaps every copy with the previous sweeps. Per-arena "free"
+// events and one copy stream per device live for the process.
+struct CopyAhead {
+    cudaStream_t cs = nullptr;
+    cudaEvent_t free_ev = nullptr, copied_ev = nullptr;
+};
+static int copy_ahead_for(const void *arena, CopyAhead &ca) {
+    static std::mutex mu;
+    static std::unordered_map<int, cudaStream_t> streams;
+    static std::unordered_map<const void *, std::pair<cudaEvent_t, cudaEvent_t>> events;
+    int dev = 0;
+    if (cudaGetDevice(&dev) != cudaSuccess) return LOGAN_ECUDA;
+    std::lock_guard<std::mutex> lk(mu);
+    auto it = streams.find(dev);
+    if (it == streams.end()) {
+        cudaStream_t cs;
+        if (cudaStreamCreateWithFlags(&cs, cudaStreamNonBlocking) != cudaSuccess) return LOGAN_ECUDA;
+        it = streams.emplace(dev, cs).first;
+    }
+    ca.cs = it->second;
+    auto ie = events.find(arena);
+    if (ie == events.end()) {
+        cudaEvent_t a, b;
+        if (cudaEventCreateWithFlags(&a, cudaEventDisableTiming) != cudaSuccess ||
+            cudaEventCreateWithFlags(&b, cudaEventDisableTiming) != cudaSuccess)
+            return LOGAN_ECUDA;
+        ie = events.emplace(arena, std::make_pair(a, b)).first;  // never recorded: waits return at once
+    }
+    ca.free_ev = ie->second.first;
+    ca.copied_ev = ie->second.second;
+    return LOGAN_OK;
+}
+
 static int host_batch(const uint8_t *seq_pool, int32_t seq_fmt, int64_t pool_len, const int64_t *q_off,
                       const int32_t *q_len, const int64_t *t_off, const int32_t *t_len, const int32_t *q_seed,
                       const int32_t *t_seed, int64_t n_pairs, int32_t k, logan_scoring_t sc,
@@ -227,15 +265,26 @@ static int host_batch(const uint8_t *seq_pool, int32_t seq_fmt, int64_t pool_len
     }
     if (o > arena_bytes) return LOGAN_ENOSPC;
     cudaStream_t s = (cudaStream_t)stream;
+    const bool ahead = !sync && opt && (opt->flags & 64);
+    CopyAhead ca;
+    if (ahead) {
+        st = copy_ahead_for(device_arena, ca);
+        if (st != LOGAN_OK) return st;
+        if (cudaStreamWaitEvent(ca.cs, ca.free_ev, 0) != cudaSuccess) return LOGAN_ECUDA;
+    }
+    cudaStream_t cs = ahead ? ca.cs : s;  // the inputs' stream
     const size_t n8 = sizeof(int64_t) * (size_t)n_pairs, n4 = sizeof(int32_t) * (size_t)n_pairs;
-    if (cudaMemsetAsync(d_pool + pool_bytes, 0, 16, s) != cudaSuccess) return LOGAN_ECUDA;
-    if (cudaMemcpyAsync(d_pool, seq_pool, (size_t)pool_bytes, cudaMemcpyHostToDevice, s) != cudaSuccess ||
-        cudaMemcpyAsync(d_qoff, q_off, n8, cudaMemcpyHostToDevice, s) != cudaSuccess ||
-        cudaMemcpyAsync(d_toff, t_off, n8, cudaMemcpyHostToDevice, s) != cudaSuccess ||
-        cudaMemcpyAsync(d_qlen, q_len, n4, cudaMemcpyHostToDevice, s) != cudaSuccess ||
-        cudaMemcpyAsync(d_tlen, t_len, n4, cudaMemcpyHostToDevice, s) != cudaSuccess ||
-        cudaMemcpyAsync(d_qs, q_seed, n4, cudaMemcpyHostToDevice, s) != cudaSuccess ||
-        cudaMemcpyAsync(d_ts, t_seed, n4, cudaMemcpyHostToDevice, s) != cudaSuccess)
+    if (cudaMemsetAsync(d_pool + pool_bytes, 0, 16, cs) != cudaSuccess) return LOGAN_ECUDA;
+    if (cudaMemcpyAsync(d_pool, seq_pool, (size_t)pool_bytes, cudaMemcpyHostToDevice, cs) != cudaSuccess ||
+        cudaMemcpyAsync(d_qoff, q_off, n8, cudaMemcpyHostToDevice, cs) != cudaSuccess ||
+        cudaMemcpyAsync(d_toff, t_off, n8, cudaMemcpyHostToDevice, cs) != cudaSuccess ||
+        cudaMemcpyAsync(d_qlen, q_len, n4, cudaMemcpyHostToDevice, cs) != cudaSuccess ||
+        cudaMemcpyAsync(d_tlen, t_len, n4, cudaMemcpyHostToDevice, cs) != cudaSuccess ||
+        cudaMemcpyAsync(d_qs, q_seed, n4, cudaMemcpyHostToDevice, cs) != cudaSuccess ||
+        cudaMemcpyAsync(d_ts, t_seed, n4, cudaMemcpyHostToDevice, cs) != cudaSuccess)
+        return LOGAN_ECUDA;
+    if (ahead && (cudaEventRecord(ca.copied_ev, ca.cs) != cudaSuccess ||
+                  cudaStreamWaitEvent(s, ca.copied_ev, 0) != cudaSuccess))
         return LOGAN_ECUDA;
     if (o + logan_workspace_bytes(n_pairs, max_ext) > arena_bytes) return LOGAN_ENOSPC;
     // the synchronous call re-encodes a u8 pool of A/C/G/T as 2-bit (logan_pack_2bit):
@@ -261,6 +310,7 @@ static int host_batch(const uint8_t *seq_pool, int32_t seq_fmt, int64_t pool_len
     if (cells && cudaMemcpyAsync(cells, d_cells, sizeof(uint64_t) * (size_t)n_pairs, cudaMemcpyDeviceToHost, s) !=
                      cudaSuccess)
         return LOGAN_ECUDA;
+    if (ahead && cudaEventRecord(ca.free_ev, s) != cudaSuccess) return LOGAN_ECUDA;  // the arena is free again
     if (sync && cudaStreamSynchronize(s) != cudaSuccess) return LOGAN_ECUDA;
     return LOGAN_OK;
 }

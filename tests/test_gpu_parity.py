@@ -241,6 +241,33 @@ def test_host_entry_point_matches_device_entry():
         assert (out == dev[0]).all() and (cells == dev[1]).all()
 
 
+def test_host_copy_ahead_ring():
+    """Asynchronous host calls with copy-ahead (options.flags bit 6): one stream, a
+    ring of two arenas, eight steps over four DIFFERENT batches (an arena reused
+    before its inputs are copied again would mix batches): every step's outputs
+    equal the device entry point's on that batch."""
+    w = datagen.CONFIGS[1]
+    batches = [datagen.generate(w, n_pairs=400, pair_base=1000 * i) for i in range(4)]
+    pool_len = max(b.pool_len for b in batches)
+    ref = [gpu_run(b, w.xdrop) for b in batches]
+    pin = lambda a: torch.from_numpy(np.ascontiguousarray(a)).pin_memory().numpy()
+    hp = [[pin(x) for x in (b.pool_2bit, b.q_off, b.q_len, b.t_off, b.t_len, b.q_seed, b.t_seed)] for b in batches]
+    arenas = [logan.HostArena(400, pool_len, logan.LOGAN_SEQ_2BIT, max(b.max_ext_len() for b in batches))
+              for _ in range(2)]
+    outs = [np.zeros((400, 5), np.int32) for _ in range(8)]
+    cells = [np.zeros(400, np.uint64) for _ in range(8)]
+    s = torch.cuda.Stream()
+    for step in range(8):
+        b, h = batches[step % 4], hp[step % 4]
+        logan.xdrop_batch_host(h[0], logan.LOGAN_SEQ_2BIT, b.pool_len, *h[1:], w.k, 1, -1, -1, w.xdrop,
+                               arenas[step % 2], out=outs[step], cells=cells[step], stream=s,
+                               asynchronous=True, copy_ahead=True)
+    s.synchronize()
+    for step in range(8):
+        r = ref[step % 4]
+        assert (outs[step] == r[0]).all() and (cells[step] == r[1]).all(), f"step {step}"
+
+
 def test_repeatable_and_permutation_invariant():
     w = datagen.CONFIGS[1]
     b = datagen.generate(w, n_pairs=500)
