@@ -490,8 +490,10 @@ def main(argv=None):
     first = stats.get("first_level", 0) - 1
     lat_narrow = (dom_level == first and stats.get("first_shape") == "latency"
                   and 0 < stats.get("first_width", 0) <= 64)
+    # (a Z >= X' never fires: the library then runs the plain, packed build)
+    zdrop_on = args.zdrop is not None and args.zdrop < w.xdrop
     packed = (dom_level <= 5 and (fmt == logan.LOGAN_SEQ_2BIT or u8_packed) and w.xdrop <= 16000
-              and args.zdrop is None and not protein and not lat_narrow) or dom_level == 6
+              and not zdrop_on and not protein and not lat_narrow) or dom_level == 6
     peak_tops, peak_how, peak32 = int_peak(sm_max, packed)
     achieved_tops = N_REF_OPS_PER_CELL * dom_cells / (dom_ms / 1e3) / 1e12
     # the library picks window widths from X (from ceil(X / |gap|) with a substitution matrix)
@@ -516,8 +518,7 @@ def main(argv=None):
 
     # End-to-end through the host-buffer C-ABI entry point, from pinned host memory:
     # every step copies its inputs in (H2D) and its results out (D2H) inside the timed
-    # region. Steps alternate between two arenas / streams (logan_xdrop_batch_host_async),
-    # so one step's copies overlap the previous step's sweep.
+    # region (logan_xdrop_batch_host_async, one stream, a ring of arenas, copy-ahead).
     e2e = None
     if not args.no_e2e:
         pool_np = batch.pool_2bit if fmt == logan.LOGAN_SEQ_2BIT else batch.pool_u8
@@ -530,6 +531,7 @@ def main(argv=None):
         # (C3: 2 streams 25.9 ms per step, 3 streams 25.0, one stream + copy-ahead 23.7;
         # profiles/r02/e2e_probe_v22.txt)
         NE2E = 3
+        E2E_COPY_AHEAD = os.environ.get("LOGAN_E2E_COPY_AHEAD", "1") != "0"  # (A/B knob)
         hout = [torch.empty((n_local, 5), dtype=torch.int32).pin_memory().numpy() for _ in range(NE2E)]
         hcells = [torch.empty(n_local, dtype=torch.int64).pin_memory().numpy().view(np.uint64) for _ in range(NE2E)]
         arenas = [logan.HostArena(n_local, batch.pool_len, fmt, db.max_ext_len, device=dev) for _ in range(NE2E)]
@@ -541,7 +543,7 @@ def main(argv=None):
             logan.xdrop_batch_host(hp[0], fmt, batch.pool_len, *hp[1:], w.k, w.match, w.mismatch,
                                    w.gap, w.xdrop, arenas[s % NE2E], out=hout[s % NE2E], cells=hcells[s % NE2E],
                                    first_level=first, stream=es, asynchronous=True, subst=subst,
-                                   zdrop=args.zdrop, copy_ahead=True)
+                                   zdrop=args.zdrop, copy_ahead=E2E_COPY_AHEAD)
             done[s % NE2E].record(es)
 
         for s_ in range(NE2E):
@@ -551,6 +553,9 @@ def main(argv=None):
         if world > 1:
             dist.barrier(device_ids=[local])
         torch.cuda.synchronize()
+        e2e_sampler = ClockSampler(sampler.uuid)
+        e2e_sampler.start()
+        time.sleep(0.1)
         a0 = torch.cuda.Event(enable_timing=True)
         a0.record(es)
         for s_ in range(ke):
@@ -561,6 +566,7 @@ def main(argv=None):
         evx = torch.cuda.Event(enable_timing=True)
         evx.record(es)
         torch.cuda.synchronize()
+        e2e_clocks = e2e_sampler.stop()
         e2e_ms = a0.elapsed_time(evx)
         te = torch.tensor([e2e_ms], dtype=torch.float64, device=dev)
         if world > 1:
@@ -570,7 +576,8 @@ def main(argv=None):
             assert (hout[k_] == out_h).all()  # the host entry point gives the device entry point's results
         e2e = {"value": cells_all * ke / (float(te.item()) / 1e3) / 1e9, "unit": UNIT,
                "h2d_bytes_per_step": int(pool_bytes + 32 * n_local), "d2h_bytes_per_step": int(28 * n_local),
-               "steps": ke, "api": f"logan_xdrop_batch_host_async (one stream, {NE2E} arenas, copy-ahead, pinned)"}
+               "steps": ke, "api": f"logan_xdrop_batch_host_async (one stream, {NE2E} arenas, copy-ahead, pinned)",
+               "clocks": e2e_clocks}
 
     # CPU baseline (rank 0 at N = 1 only) and the parity sample: the oracle on this
     # host's cores over a bounded sample of this rank's pairs, compared element by

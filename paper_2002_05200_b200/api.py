@@ -161,7 +161,14 @@ def xdrop_batch(db: DeviceBatch, match: int, mismatch: int, gap: int, xdrop: int
     if stream is None:
         stream = torch.cuda.current_stream(dev)
     if pack_u8 and db.fmt == _lib.LOGAN_SEQ_U8 and subst is None and n > 0:
-        packed, other = pack_2bit(db, stream)
+        # the 2-bit copy goes to a buffer kept per (device, stream), like the workspace
+        key = ("pack", str(dev), int(stream.cuda_stream))
+        nb = int(lib.logan_pack_2bit_bytes(db.pool_len))
+        buf = _WS_CACHE.get(key)
+        if buf is None or buf[0].numel() < nb:
+            buf = (torch.empty(nb, dtype=torch.uint8, device=dev), torch.empty(1, dtype=torch.int64, device=dev))
+            _WS_CACHE[key] = buf
+        packed, other = pack_2bit(db, stream, into=buf)
         stream.synchronize()
         if int(other.item()) == 0:
             db = packed
@@ -194,10 +201,11 @@ def xdrop_batch(db: DeviceBatch, match: int, mismatch: int, gap: int, xdrop: int
     return out, cells
 
 
-def pack_2bit(db: DeviceBatch, stream=None):
+def pack_2bit(db: DeviceBatch, stream=None, into=None):
     """``logan_pack_2bit``: a 2-bit copy of ``db``'s u8 pool (same descriptors) and a
     device int64 tensor with the number of bytes outside A/C/G/T inside ``db``'s reads
-    (the copy is equivalent only if it is 0), both on ``stream``; no synchronisation."""
+    (the copy is equivalent only if it is 0), both on ``stream``; no synchronisation.
+    ``into`` = (uint8 tensor, int64 tensor) to write instead of fresh allocations."""
     torch = _require_cuda()
     lib = _lib.load()
     if db.fmt != _lib.LOGAN_SEQ_U8:
@@ -207,8 +215,11 @@ def pack_2bit(db: DeviceBatch, stream=None):
         stream = torch.cuda.current_stream(dev)
     nb = int(lib.logan_pack_2bit_bytes(db.pool_len))
     with torch.cuda.device(dev):
-        pool = torch.empty(nb, dtype=torch.uint8, device=dev)
-        other = torch.empty(1, dtype=torch.int64, device=dev)
+        if into is not None and into[0].numel() >= nb:
+            pool, other = into
+        else:
+            pool = torch.empty(nb, dtype=torch.uint8, device=dev)
+            other = torch.empty(1, dtype=torch.int64, device=dev)
         for t in (pool, other):
             t.record_stream(stream)
         _lib.check(lib.logan_pack_2bit(db.pool.data_ptr(), db.pool_len, db.q_off.data_ptr(), db.q_len.data_ptr(),

@@ -10,12 +10,14 @@ import paper_2002_05200_b200 as logan  # noqa: E402
 
 cfg = int(sys.argv[1]) if len(sys.argv) > 1 else 3
 w = datagen.CONFIGS[cfg]
+if len(sys.argv) > 2:
+    w = w.with_(xdrop=int(sys.argv[2]))
 b = datagen.generate(w, n_pairs=w.n_pairs, u8=False)
 pin = lambda a: torch.from_numpy(np.ascontiguousarray(a)).pin_memory()
 hp = [pin(x) for x in (b.pool_2bit, b.q_off, b.q_len, b.t_off, b.t_len, b.q_seed, b.t_seed)]
 n = b.n_pairs
 db = logan.to_device(b, logan.LOGAN_SEQ_2BIT)
-K = 10
+K = int(os.environ.get("E2E_K", "10"))
 
 def timed(fn, streams):
     torch.cuda.synchronize()
@@ -63,3 +65,45 @@ for ns in (1, 2, 3):
     run(); torch.cuda.synchronize()
     t0 = time.perf_counter(); ms = timed(run, streams); wall = (time.perf_counter() - t0) / K * 1e3
     print(f"host entry, {ns} stream(s): {ms:.2f} ms per step (host wall {wall:.2f})")
+
+# the ideal pipelining: every sweep on ONE compute stream, each step's inputs copied on a
+# separate copy stream (pinned -> device buffers) while the previous sweep runs
+cs = torch.cuda.Stream()
+NB = 2
+dbs = [logan.to_device(b, logan.LOGAN_SEQ_2BIT) for _ in range(NB)]
+hdev = [[hp[i] for i in range(7)] for _ in range(NB)]
+free = [torch.cuda.Event() for _ in range(NB)]
+done = [torch.cuda.Event() for _ in range(NB)]
+def piped():
+    for s in range(K):
+        j = s % NB
+        d = dbs[j]
+        with torch.cuda.stream(cs):
+            cs.wait_event(free[j])
+            d.pool.copy_(hp[0], non_blocking=True)
+            for dst, src in zip((d.q_off, d.q_len, d.t_off, d.t_len, d.q_seed, d.t_seed), hp[1:]):
+                dst.copy_(src, non_blocking=True)
+            done[j].record(cs)
+        s0.wait_event(done[j])
+        o, c = logan.xdrop_batch(d, w.match, w.mismatch, w.gap, w.xdrop, out=out, cells=cells, stream=s0)
+        with torch.cuda.stream(s0):
+            hout[j][:] = 0  # (host buffers unused here; results stay on the device)
+        free[j].record(s0)
+for e in free:
+    e.record(s0)
+piped(); torch.cuda.synchronize()
+print(f"copy stream + one compute stream: {timed(piped, [s0, cs]):.2f} ms per step")
+
+# the library's copy-ahead (options.flags bit 6): one stream, a ring of three arenas
+es = torch.cuda.Stream()
+done = [torch.cuda.Event() for _ in range(3)]
+def ca_run():
+    for s in range(K):
+        if s >= 3:
+            done[s % 3].synchronize()
+        logan.xdrop_batch_host(hpn[0], logan.LOGAN_SEQ_2BIT, b.pool_len, *hpn[1:], w.k, w.match, w.mismatch,
+                               w.gap, w.xdrop, arenas[s % 3], out=hout[s % 3], cells=hcells[s % 3], stream=es,
+                               asynchronous=True, copy_ahead=True)
+        done[s % 3].record(es)
+ca_run(); torch.cuda.synchronize()
+print(f"library copy-ahead, one stream, 3 arenas: {timed(ca_run, [es]):.2f} ms per step")
