@@ -558,16 +558,31 @@ def main(argv=None):
         time.sleep(0.1)
         a0 = torch.cuda.Event(enable_timing=True)
         a0.record(es)
+        dbg = os.environ.get("LOGAN_E2E_DEBUG") == "1"
+        marks, host_t = [], []
         for s_ in range(ke):
             if s_ >= NE2E:
                 done[s_ % NE2E].synchronize()  # step s-NE2E's outputs are read before its buffers are reused
                 assert int(hcells[s_ % NE2E].sum()) == cells_step
+            t0_ = time.perf_counter()
             e2e_step(s_)
+            if dbg:
+                host_t.append((time.perf_counter() - t0_) * 1e3)
+                m = torch.cuda.Event(enable_timing=True)
+                m.record(es)
+                marks.append(m)
         evx = torch.cuda.Event(enable_timing=True)
         evx.record(es)
         torch.cuda.synchronize()
         e2e_clocks = e2e_sampler.stop()
         e2e_ms = a0.elapsed_time(evx)
+        if dbg:
+            prev = a0
+            per = []
+            for m in marks:
+                per.append(round(prev.elapsed_time(m), 2))
+                prev = m
+            print(f"e2e debug: per-step GPU ms {per}; host enqueue ms {[round(x, 2) for x in host_t]}", file=sys.stderr)
         te = torch.tensor([e2e_ms], dtype=torch.float64, device=dev)
         if world > 1:
             dist.all_reduce(te, op=dist.ReduceOp.MAX)
