@@ -487,8 +487,8 @@ def main(argv=None):
     # the packed int16 kernels: the register windows of a 2-bit pool at X <= 16000 (no
     # Z-drop, no matrix; options.flags bit 4 off) except the int32 one-warp shapes of
     # W <= 64, and the band level
-    first = stats.get("first_level", 0) - 1
-    lat_narrow = (dom_level == first and stats.get("first_shape") == "latency"
+    first_lv = stats.get("first_level", 0) - 1  # (not `first`: that is the e2e calls' first_level)
+    lat_narrow = (dom_level == first_lv and stats.get("first_shape") == "latency"
                   and 0 < stats.get("first_width", 0) <= 64)
     # (a Z >= X' never fires: the library then runs the plain, packed build)
     zdrop_on = args.zdrop is not None and args.zdrop < w.xdrop
@@ -539,11 +539,17 @@ def main(argv=None):
         done = [torch.cuda.Event() for _ in range(NE2E)]
         pool_bytes = (batch.pool_len + 3) // 4 if fmt == logan.LOGAN_SEQ_2BIT else batch.pool_len
 
+        stage_ev = None
+        if os.environ.get("LOGAN_E2E_DEBUG") == "1":  # per-stage times of the e2e sweeps (debug)
+            stage_ev = [torch.cuda.Event(enable_timing=True) for _ in range(2 * nst)]
+            for e in stage_ev:
+                e.record(es)
+
         def e2e_step(s):
             logan.xdrop_batch_host(hp[0], fmt, batch.pool_len, *hp[1:], w.k, w.match, w.mismatch,
                                    w.gap, w.xdrop, arenas[s % NE2E], out=hout[s % NE2E], cells=hcells[s % NE2E],
                                    first_level=first, stream=es, asynchronous=True, subst=subst,
-                                   zdrop=args.zdrop, copy_ahead=E2E_COPY_AHEAD)
+                                   zdrop=args.zdrop, copy_ahead=E2E_COPY_AHEAD, timing_events=stage_ev)
             done[s % NE2E].record(es)
 
         for s_ in range(NE2E):
@@ -583,6 +589,9 @@ def main(argv=None):
                 per.append(round(prev.elapsed_time(m), 2))
                 prev = m
             print(f"e2e debug: per-step GPU ms {per}; host enqueue ms {[round(x, 2) for x in host_t]}", file=sys.stderr)
+            st_ms = {k: round(stage_ev[2 * k].elapsed_time(stage_ev[2 * k + 1]), 2) for k in range(nst)}
+            print(f"e2e debug: last step's stage ms {st_ms}; device-timed stage ms "
+                  f"{ {k: round(v / args.steps, 2) for k, v in stage_ms.items()} }", file=sys.stderr)
         te = torch.tensor([e2e_ms], dtype=torch.float64, device=dev)
         if world > 1:
             dist.all_reduce(te, op=dist.ReduceOp.MAX)

@@ -259,7 +259,7 @@ def xdrop_batch_host(pool: np.ndarray, fmt: int, pool_len: int, q_off, q_len, t_
                      arena: HostArena, out: np.ndarray | None = None,
                      cells: np.ndarray | None = None, first_level: int | None = None, stream=None,
                      asynchronous: bool = False, subst=None, zdrop: int | None = None,
-                     copy_ahead: bool = False):
+                     copy_ahead: bool = False, timing_events=None):
     """End-to-end call with HOST buffers (numpy; pinned memory copies fastest).
 
     ``asynchronous=True`` returns right after enqueuing (``logan_xdrop_batch_host_async``):
@@ -286,7 +286,7 @@ def xdrop_batch_host(pool: np.ndarray, fmt: int, pool_len: int, q_off, q_len, t_
     fn = lib.logan_xdrop_batch_host_async if asynchronous else lib.logan_xdrop_batch_host
     with torch.cuda.device(dev):
         st = fn(ptr(pool), fmt, pool_len, *[ptr(a) for a in arrs], n, k, sc,
-                _opts(first_level, subst=subst, zdrop=zdrop, copy_ahead=copy_ahead), ptr(out), ptr(cells),
+                _opts(first_level, timing_events, subst=subst, zdrop=zdrop, copy_ahead=copy_ahead), ptr(out), ptr(cells),
                 arena.tensor.data_ptr(), arena.nbytes, stream.cuda_stream)
     _lib.check(st)
     return out, cells
