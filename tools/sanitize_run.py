@@ -42,3 +42,22 @@ for fs in (16, 20):
         out, cells = logan.xdrop_batch(db, 1, -1, -1, X, first_level=1, first_slots=fs)
         torch.cuda.synchronize()
         print("slots", fs, X, int(cells.sum()), flush=True)
+# the band level's second stage (bands wider than the one-warp 4096-slot ring) and the
+# packed one-warp latency shapes (W = 128 / 256)
+rng = np.random.default_rng(5)
+L = 4200
+base = "".join(rng.choice(list("ACGT"), L))
+mut = list(base)
+for p in rng.choice(L, 60, replace=False):
+    mut[p] = "ACGT"[("ACGT".index(mut[p]) + 1) % 4]
+wb = datagen.from_strings([(base, "".join(mut), 0, 0)], k=5)
+dwb = logan.to_device(wb, logan.LOGAN_SEQ_2BIT)
+st = logan.new_stats()
+out, cells = logan.xdrop_batch(dwb, 1, -1, -1, 20000, first_level=7, stats=st)
+torch.cuda.synchronize()
+s = logan.stats_dict(st)
+print("band stage 2", int(cells.sum()), s["tasks_started"][6], s["tasks_finished"][6], flush=True)
+for lvl in (3, 4):
+    out, cells = logan.xdrop_batch(db, 1, -1, -1, 100, first_level=lvl, latency_first=True)
+    torch.cuda.synchronize()
+    print("one-warp packed", lvl, int(cells.sum()), flush=True)
