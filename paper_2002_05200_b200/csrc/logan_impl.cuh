@@ -207,8 +207,8 @@ static __global__ void k_combine(const Params P, const TaskRes *tres, logan_resu
 #ifndef LOGAN_HELPER_THROUGHPUT
 #define LOGAN_HELPER_THROUGHPUT 1
 #endif
-#ifndef LOGAN_HELPER_WARPS  // 48 since the helpers are packed (profiles/r02/ab_helper_warps.txt: C3 X = 50 +2%, shares -3.5%)
-#define LOGAN_HELPER_WARPS 48
+#ifndef LOGAN_HELPER_WARPS  // 24 since the helpers are packed (profiles/r02/ab_helper_warps*.txt: 96 -> 48 -> 24:
+#define LOGAN_HELPER_WARPS 24  // C3 X = 50 +3%, the C3 3/8 share 9.97 -> 8.88 ms, C3 / C2 / C4 unchanged)
 #endif
 #if LOGAN_HELPER_THROUGHPUT
 #define LOGAN_HSHAPE(W) ((W) / 32), 32
